@@ -1,0 +1,151 @@
+// tests/native/libm_check.cpp — test helper: compares the product's libm
+// restatements (paper_2605_17869_b200/csrc/dsift_math.cuh, compiled here as
+// host code with -ffp-contract=off) against the live host glibc.  The same
+// header is compiled into the CUDA kernels, so host-twin == glibc plus
+// device == host-twin (checked in tests/test_gpu_parity.py) gives device ==
+// glibc, the function the reference calls.
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+
+#include "../../paper_2605_17869_b200/csrc/dsift_math.cuh"
+
+namespace {
+struct Rng {
+    uint64_t s;
+    uint64_t next() {
+        uint64_t z = (s += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+    double uni() { return double(next() >> 11) * (1.0 / 9007199254740992.0); }
+};
+
+float bitsf(uint32_t u) {
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+uint32_t fbits(float f) {
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    return u;
+}
+uint64_t dbits(double d) {
+    uint64_t u;
+    std::memcpy(&u, &d, 8);
+    return u;
+}
+}  // namespace
+
+extern "C" {
+
+// mode 0: arbitrary finite float bit patterns (both signs, all exponents)
+// mode 1: pipeline-shaped gradients: differences of two [0,1] floats, and
+//         0.5f * difference (describe.cpp:84-85, orient.cpp:46-47)
+// mode 2: special values (0, +-0, inf, nan, x == 1)
+int64_t lc_atan2f_mismatch(uint64_t seed, int64_t n, int mode, float* first_bad /*[3]*/) {
+    Rng r{seed};
+    int64_t bad = 0;
+    const float specials[] = {0.0f, -0.0f, 1.0f, -1.0f, INFINITY, -INFINITY, NAN, 1e-30f, 3e38f,
+                              1e-45f, 0.5f, 2.4375f, 0.4375f, 1.1875f, 0.6875f};
+    const int ns = sizeof(specials) / sizeof(float);
+    for (int64_t i = 0; i < n; ++i) {
+        float y, x;
+        if (mode == 0) {
+            do {
+                y = bitsf(uint32_t(r.next()));
+            } while (!std::isfinite(y));
+            do {
+                x = bitsf(uint32_t(r.next()));
+            } while (!std::isfinite(x));
+        } else if (mode == 1) {
+            const float a = float(r.uni()), b = float(r.uni()), c = float(r.uni()),
+                        d = float(r.uni());
+            // scale the dynamic range like real pyramid levels (smooth areas -> tiny diffs)
+            const float s = std::ldexp(1.0f, -int(r.next() % 20));
+            y = (a - b) * s;
+            x = (c - d) * s;
+            if (r.next() & 1) {
+                y = 0.5f * y;
+                x = 0.5f * x;
+            }
+        } else {
+            y = specials[r.next() % ns];
+            x = specials[r.next() % ns];
+        }
+        const float ref = atan2f(y, x);
+        const float got = dsift_atan2f(y, x);
+        if (fbits(ref) != fbits(got) && !(std::isnan(ref) && std::isnan(got))) {
+            if (bad == 0 && first_bad) {
+                first_bad[0] = y;
+                first_bad[1] = x;
+                first_bad[2] = got;
+            }
+            ++bad;
+        }
+    }
+    return bad;
+}
+
+// exp over [lo, hi] uniformly; mode 1 = arguments shaped like the pipeline's
+// Gaussian weights: -(a^2 + b^2) / denom (orient.cpp:55, describe.cpp:97-98).
+int64_t lc_exp_mismatch(uint64_t seed, int64_t n, double lo, double hi, int mode,
+                        double* first_bad) {
+    Rng r{seed};
+    int64_t bad = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        double x;
+        if (mode == 0) {
+            x = lo + (hi - lo) * r.uni();
+        } else {
+            const double bw = 2.0 + 20.0 * r.uni();
+            const int u = int(r.next() % 161) - 80, v = int(r.next() % 161) - 80;
+            const double uu = u / bw, vv = v / bw;
+            x = -(uu * uu + vv * vv) / 8.0;
+        }
+        const double ref = std::exp(x);
+        const double got = dsift_exp(x);
+        if (dbits(ref) != dbits(got)) {
+            if (bad == 0 && first_bad) {
+                first_bad[0] = x;
+                first_bad[1] = got;
+            }
+            ++bad;
+        }
+    }
+    return bad;
+}
+
+// cos/sin of float angles in [0, 2pi): returns double mismatches; *float_bad
+// counts angles whose (float)(cx + cos*u) style sample coordinate would move
+// (here: results that differ after rounding to float).
+int64_t lc_sincos_mismatch(uint64_t seed, int64_t n, int64_t* float_bad) {
+    Rng r{seed};
+    int64_t bad = 0, fb = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        const float a = float(r.uni() * 6.283185307179586);
+        double s, c;
+        dsift_sincos(double(a), &s, &c);
+        const double rs = std::sin(double(a)), rc = std::cos(double(a));
+        if (dbits(rs) != dbits(s) || dbits(rc) != dbits(c)) {
+            ++bad;
+            if (float(rs) != float(s) || float(rc) != float(c)) ++fb;
+        }
+    }
+    if (float_bad) *float_bad = fb;
+    return bad;
+}
+
+void lc_atan2f_batch(const float* y, const float* x, int64_t n, float* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = dsift_atan2f(y[i], x[i]);
+}
+void lc_exp_batch(const double* x, int64_t n, double* out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = dsift_exp(x[i]);
+}
+void lc_sincos_batch(const double* a, int64_t n, double* s, double* c) {
+    for (int64_t i = 0; i < n; ++i) dsift_sincos(a[i], &s[i], &c[i]);
+}
+
+}  // extern "C"
