@@ -1,0 +1,160 @@
+/* include/dsift.h — C ABI of the B200-native SIFT extraction path.
+ *
+ * Drop-in boundary for detsift::extract (reference:
+ * /root/reference/proj/include/detsift/io.hpp:17-19, src/io.cpp:111-142) and
+ * for the stage-level functions the reference's tests and oracles call
+ * directly (scalespace.hpp:30-47, detect.hpp:23-33, orient.hpp:12-25,
+ * describe.hpp:19-30, core.hpp:83-91, detsum.hpp:22-48).
+ *
+ * Plain C: pointers, sizes and status codes only; no exceptions and no torch
+ * types cross this boundary.  Every entry point returns DSIFT_OK (0) or a
+ * positive DSIFT_E* code; dsift_last_error() then holds the message (for
+ * DSIFT_EINVAL it is the reference's std::invalid_argument text).
+ *
+ * Threading: one dsift_ctx per (device, host thread); all device work of a
+ * context is ordered on its CUDA stream.  Results stay on the device until
+ * copied or exported and are owned by the context until the next extract.
+ */
+#ifndef DSIFT_H
+#define DSIFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSIFT_ABI_VERSION 1
+
+enum {
+    DSIFT_OK = 0,
+    DSIFT_EINVAL = 1,    /* std::invalid_argument in the reference            */
+    DSIFT_ECAPACITY = 2, /* a device work list overflowed; nothing truncated  */
+    DSIFT_ECUDA = 3,     /* CUDA runtime error / no device / extension absent */
+    DSIFT_ENOMEM = 4,    /* device or host allocation failed                  */
+    DSIFT_ESTATE = 5     /* call order violated (e.g. no result yet)          */
+};
+
+/* detsift::SiftConfig (core.hpp:30-47).  dsp_scales is borrowed by the call. */
+typedef struct dsift_config {
+    float sigma0;
+    int32_t intervals;           /* intervals_per_octave (s)     */
+    float assumed_blur;          /* assumed_input_blur           */
+    float contrast_threshold;
+    float edge_ratio;
+    int32_t max_refine_iters;
+    int64_t upsample_pixel_limit;
+    const double* dsp_scales;
+    int32_t n_dsp_scales;
+    float descriptor_clip;
+    int32_t orientation_bins;
+    float orientation_peak_ratio;
+    int32_t num_octaves;         /* 0 = auto                      */
+} dsift_config;
+
+/* detsift::Keypoint (core.hpp:55-63), 28 bytes, identical layout. */
+typedef struct dsift_keypoint {
+    float x, y, sigma, angle, response;
+    int32_t octave, interval;
+} dsift_keypoint;
+
+typedef struct dsift_ctx dsift_ctx;
+
+/* input flags */
+#define DSIFT_INPUT_HOST 0
+#define DSIFT_INPUT_DEVICE 1
+
+/* ---- library ------------------------------------------------------------ */
+int dsift_abi_version(void);
+const char* dsift_strerror(int code);
+const char* dsift_last_error(void);
+/* Fills the reference defaults (core.hpp:31-43); dsp_scales points at a
+ * static 5-entry array owned by the library. */
+void dsift_config_default(dsift_config* cfg);
+/* SiftConfig::validate (core.cpp:17-46): DSIFT_EINVAL + reference message. */
+int dsift_config_validate(const dsift_config* cfg);
+
+/* ---- context ------------------------------------------------------------ */
+/* Creates a context on `device` (cudaSetDevice semantics).  The config is
+ * validated and copied. */
+int dsift_create(int device, const dsift_config* cfg, dsift_ctx** out);
+void dsift_destroy(dsift_ctx* ctx);
+/* Use the caller's cudaStream_t (NULL restores the context's own stream). */
+int dsift_set_stream(dsift_ctx* ctx, void* cuda_stream);
+/* Per-image capacity of the keypoint work lists (0 = automatic, from the
+ * image size).  Overflow is reported as DSIFT_ECAPACITY, never truncated. */
+int dsift_set_capacity(dsift_ctx* ctx, int64_t max_keypoints_per_image);
+
+/* ---- full pipeline: detsift::extract (io.cpp:111-142) --------------------- */
+/* `n` same-size images, row-major float32 [n][h][w], values in [0,1], on the
+ * host (DSIFT_INPUT_HOST, copied H2D inside the call) or the device.  Work is
+ * enqueued on the context stream; dsift_result_sync waits for it.  Output is
+ * per image in canonical order (core.cpp:116-170). */
+int dsift_extract_batch(dsift_ctx* ctx, const float* images, int n, int w, int h, int flags);
+int dsift_extract(dsift_ctx* ctx, const float* image, int w, int h, int flags);
+/* Waits for the last extract; *total = keypoints over all images. */
+int dsift_result_sync(dsift_ctx* ctx, int64_t* total);
+/* [begin, begin+count) of `image` inside the batch result (after sync). */
+int dsift_result_range(dsift_ctx* ctx, int image, int64_t* begin, int64_t* count);
+/* Host copies of the whole batch result (any pointer may be NULL):
+ * kps [total], desc [total][128] float32, desc_u8 [total][128] (q(v) =
+ * min(255, lround(v * 255.0))), offsets [n+1]. */
+int dsift_result_copy(dsift_ctx* ctx, dsift_keypoint* kps, float* desc, uint8_t* desc_u8,
+                      int64_t* offsets);
+/* Device pointers (valid until the next extract / destroy), no copy. */
+int dsift_result_device(dsift_ctx* ctx, const dsift_keypoint** kps, const float** desc,
+                        const uint8_t** desc_u8, const int64_t** offsets);
+/* Zero-copy DLPack export of the batch result: which = 0 keypoints (float32
+ * [total][7] view, octave/interval reinterpreted), 1 desc f32 [total][128],
+ * 2 desc u8 [total][128].  Returns a DLManagedTensor* (see dlpack.h); its
+ * deleter keeps the context buffer alive until called. */
+#define DSIFT_EXPORT_KEYPOINTS 0
+#define DSIFT_EXPORT_DESC_F32 1
+#define DSIFT_EXPORT_DESC_U8 2
+int dsift_export_dlpack(dsift_ctx* ctx, int which, void** dl_managed_tensor);
+/* SHA-256 of the DSF1 serialization of image `image` of the last result
+ * (detsum.cpp:129-132, core.cpp:153-196), computed on the host. */
+int dsift_result_sha256(dsift_ctx* ctx, int image, char hex65[65]);
+
+/* ---- stage level (scalespace.hpp / detect.hpp / orient.hpp / describe.hpp) */
+/* build_scale_space (scalespace.cpp:144-214) for one image, kept in ctx. */
+int dsift_build_scale_space(dsift_ctx* ctx, const float* image, int w, int h, int flags);
+/* Handcrafted scale space (as tests/test_detect.cpp:14-30 builds): gauss
+ * [n_oct*(s+3)] and dog [n_oct*(s+2)] host planes of dims[2*o] x dims[2*o+1]. */
+int dsift_load_scale_space(dsift_ctx* ctx, int n_oct, int upsampled, const int32_t* dims,
+                           const float* const* gauss, const float* const* dog);
+int dsift_scale_space_info(dsift_ctx* ctx, int32_t* n_oct, int32_t* upsampled, int32_t* dims);
+/* kind 0 = gauss level, 1 = DoG level; copies [h][w] float32 to host. */
+int dsift_scale_space_level(dsift_ctx* ctx, int octave, int kind, int level, float* out);
+/* find_extrema (detect.cpp:32-71): n x 5 int32 (octave, interval, row, col,
+ * is_max), in canonical (octave, interval, row, col) order. */
+int dsift_find_extrema(dsift_ctx* ctx, int32_t* out5, int64_t cap, int64_t* n);
+/* detect_keypoints (detect.cpp:158-172): refined keypoints in candidate order. */
+int dsift_detect(dsift_ctx* ctx, dsift_keypoint* out, int64_t cap, int64_t* n);
+/* orientation_histogram (orient.cpp:26-60) for n host keypoints: [n][bins]. */
+int dsift_orientation_histograms(dsift_ctx* ctx, const dsift_keypoint* kps, int64_t n,
+                                 float* out);
+/* assign_orientations (orient.cpp:77-113), flattened in keypoint order. */
+int dsift_assign_orientations(dsift_ctx* ctx, const dsift_keypoint* kps, int64_t n,
+                              dsift_keypoint* out, int64_t cap, int64_t* n_out);
+/* raw_descriptor (describe.cpp:33-127) at one support scale: [n][128]. */
+int dsift_raw_descriptors(dsift_ctx* ctx, const dsift_keypoint* kps, int64_t n,
+                          double scale_factor, float* out);
+/* dsp_descriptor (describe.cpp:148-173): [n][128] float32 (+ optional u8). */
+int dsift_dsp_descriptors(dsift_ctx* ctx, const dsift_keypoint* kps, int64_t n, float* out,
+                          uint8_t* out_u8);
+
+/* ---- synthetic input (tests/support/synth.cpp:14-66) on the device -------- */
+/* n images of value noise, image i uses seed0 + i; writes device [n][h][w]. */
+int dsift_synth_value_noise(dsift_ctx* ctx, float* dev_out, int n, int w, int h,
+                            uint64_t seed0, int octaves, int base_cells);
+
+/* ---- accounting -------------------------------------------------------------- */
+/* Number of kernel launches the context has issued since creation. */
+int64_t dsift_kernel_launches(dsift_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSIFT_H */

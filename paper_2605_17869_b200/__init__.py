@@ -1,0 +1,357 @@
+"""paper_2605_17869_b200 — B200-native SIFT extraction behind the detsift API.
+
+Python mirror of the reference's extraction surface (detsift::extract and the
+stage functions its tests call: /root/reference/proj/include/detsift/*.hpp),
+implemented over the C ABI in include/dsift.h (libdsift.so: hand-written
+sm_100a CUDA kernels + C++ orchestration).  There is no CPU fallback: if the
+library or a CUDA device is missing every entry point raises ``DsiftError``.
+
+    from paper_2605_17869_b200 import SiftConfig, extract
+    fs = extract(image_float32_hw, SiftConfig())      # FeatureSet
+    fs.keypoints  # structured array (x, y, sigma, angle, response, octave, interval)
+    fs.descriptors  # (n, 128) float32, canonical order (core.cpp:116-170)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = [
+    "SiftConfig", "FeatureSet", "KEYPOINT_DTYPE", "DsiftError", "Extractor", "extract",
+    "library_path", "load_library",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+KEYPOINT_DTYPE = np.dtype(
+    [("x", "<f4"), ("y", "<f4"), ("sigma", "<f4"), ("angle", "<f4"),
+     ("response", "<f4"), ("octave", "<i4"), ("interval", "<i4")])
+DESC_DIM = 128
+
+DSIFT_OK, DSIFT_EINVAL, DSIFT_ECAPACITY, DSIFT_ECUDA, DSIFT_ENOMEM, DSIFT_ESTATE = range(6)
+INPUT_HOST, INPUT_DEVICE = 0, 1
+
+
+class DsiftError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(msg)
+        self.code = code
+
+
+class InvalidArgument(DsiftError, ValueError):
+    """std::invalid_argument in the reference."""
+
+
+class _Config(C.Structure):
+    _fields_ = [
+        ("sigma0", C.c_float), ("intervals", C.c_int32), ("assumed_blur", C.c_float),
+        ("contrast_threshold", C.c_float), ("edge_ratio", C.c_float),
+        ("max_refine_iters", C.c_int32), ("upsample_pixel_limit", C.c_int64),
+        ("dsp_scales", C.POINTER(C.c_double)), ("n_dsp_scales", C.c_int32),
+        ("descriptor_clip", C.c_float), ("orientation_bins", C.c_int32),
+        ("orientation_peak_ratio", C.c_float), ("num_octaves", C.c_int32),
+    ]
+
+
+@dataclass
+class SiftConfig:
+    """detsift::SiftConfig (core.hpp:30-47), same defaults and field meaning."""
+    sigma0: float = 1.6
+    intervals_per_octave: int = 3
+    assumed_input_blur: float = 0.5
+    contrast_threshold: float = 0.04
+    edge_ratio: float = 10.0
+    max_refine_iters: int = 5
+    upsample_pixel_limit: int = 4_000_000
+    dsp_scales: tuple = (0.5, 1.0 / 1.4142135623730951, 1.0, 1.4142135623730951, 2.0)
+    descriptor_clip: float = 0.2
+    orientation_bins: int = 36
+    orientation_peak_ratio: float = 0.8
+    num_octaves: int = 0
+
+    def to_c(self) -> _Config:
+        arr = (C.c_double * max(1, len(self.dsp_scales)))(*self.dsp_scales)
+        c = _Config(self.sigma0, self.intervals_per_octave, self.assumed_input_blur,
+                    self.contrast_threshold, self.edge_ratio, self.max_refine_iters,
+                    self.upsample_pixel_limit, C.cast(arr, C.POINTER(C.c_double)),
+                    len(self.dsp_scales), self.descriptor_clip, self.orientation_bins,
+                    self.orientation_peak_ratio, self.num_octaves)
+        c._keep = arr
+        return c
+
+    def validate(self) -> None:
+        """SiftConfig::validate (core.cpp:17-46); raises InvalidArgument."""
+        lib = load_library()
+        _check(lib, lib.dsift_config_validate(C.byref(self.to_c())))
+
+
+@dataclass
+class FeatureSet:
+    """detsift::FeatureSet (core.hpp:66-78) + the uint8 export."""
+    keypoints: np.ndarray = field(default_factory=lambda: np.zeros(0, KEYPOINT_DTYPE))
+    descriptors: np.ndarray = field(default_factory=lambda: np.zeros((0, DESC_DIM), np.float32))
+    descriptors_u8: np.ndarray | None = None
+    dim: int = DESC_DIM
+
+    def __len__(self) -> int:
+        return len(self.keypoints)
+
+    def size(self) -> int:
+        return len(self.keypoints)
+
+    def row(self, i: int) -> np.ndarray:
+        return self.descriptors[i]
+
+
+_LIB = None
+
+
+def library_path() -> str:
+    return os.path.join(HERE, "libdsift.so")
+
+
+def load_library():
+    """Loads the in-tree libdsift.so (fails loudly; no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    path = library_path()
+    if not os.path.exists(path):
+        raise DsiftError(DSIFT_ECUDA, f"CUDA extension missing: {path} (run __graft_entry__.build())")
+    lib = C.CDLL(path)
+    vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int
+    sig = {
+        "dsift_abi_version": ([], C.c_int), "dsift_strerror": ([C.c_int], C.c_char_p),
+        "dsift_last_error": ([], C.c_char_p), "dsift_config_default": ([vp], None),
+        "dsift_config_validate": ([vp], C.c_int), "dsift_create": ([i32, vp, vp], C.c_int),
+        "dsift_destroy": ([vp], None), "dsift_set_stream": ([vp, vp], C.c_int),
+        "dsift_set_capacity": ([vp, i64], C.c_int),
+        "dsift_extract_batch": ([vp, vp, i32, i32, i32, i32], C.c_int),
+        "dsift_extract": ([vp, vp, i32, i32, i32], C.c_int),
+        "dsift_result_sync": ([vp, vp], C.c_int), "dsift_result_range": ([vp, i32, vp, vp], C.c_int),
+        "dsift_result_copy": ([vp, vp, vp, vp, vp], C.c_int),
+        "dsift_result_device": ([vp, vp, vp, vp, vp], C.c_int),
+        "dsift_export_dlpack": ([vp, i32, vp], C.c_int),
+        "dsift_result_sha256": ([vp, i32, C.c_char_p], C.c_int),
+        "dsift_build_scale_space": ([vp, vp, i32, i32, i32], C.c_int),
+        "dsift_load_scale_space": ([vp, i32, i32, vp, vp, vp], C.c_int),
+        "dsift_scale_space_info": ([vp, vp, vp, vp], C.c_int),
+        "dsift_scale_space_level": ([vp, i32, i32, i32, vp], C.c_int),
+        "dsift_find_extrema": ([vp, vp, i64, vp], C.c_int),
+        "dsift_detect": ([vp, vp, i64, vp], C.c_int),
+        "dsift_orientation_histograms": ([vp, vp, i64, vp], C.c_int),
+        "dsift_assign_orientations": ([vp, vp, i64, vp, i64, vp], C.c_int),
+        "dsift_raw_descriptors": ([vp, vp, i64, C.c_double, vp], C.c_int),
+        "dsift_dsp_descriptors": ([vp, vp, i64, vp, vp], C.c_int),
+        "dsift_synth_value_noise": ([vp, vp, i32, i32, i32, C.c_uint64, i32, i32], C.c_int),
+        "dsift_kernel_launches": ([vp], C.c_int64),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = res
+    _LIB = lib
+    return lib
+
+
+def _check(lib, rc: int) -> None:
+    if rc != DSIFT_OK:
+        msg = lib.dsift_last_error().decode()
+        if rc == DSIFT_EINVAL:
+            raise InvalidArgument(rc, msg)
+        raise DsiftError(rc, f"{lib.dsift_strerror(rc).decode()}: {msg}")
+
+
+def _f32(img) -> np.ndarray:
+    a = np.ascontiguousarray(img, dtype=np.float32)
+    if a.ndim != 2:
+        raise InvalidArgument(DSIFT_EINVAL, "image must be a 2-D [h, w] float32 array")
+    return a
+
+
+class Extractor:
+    """One dsift_ctx: a device, a stream, a config and the last result."""
+
+    def __init__(self, cfg: SiftConfig | None = None, device: int = 0):
+        self.lib = load_library()
+        self.cfg = cfg or SiftConfig()
+        self._ccfg = self.cfg.to_c()
+        ctx = C.c_void_p()
+        _check(self.lib, self.lib.dsift_create(device, C.byref(self._ccfg), C.byref(ctx)))
+        self.ctx = ctx
+        self.device = device
+        self.batch = 0
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.dsift_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # ---- hot path ----------------------------------------------------------
+    def set_stream(self, cuda_stream_handle: int | None) -> None:
+        _check(self.lib, self.lib.dsift_set_stream(self.ctx, C.c_void_p(cuda_stream_handle or 0)))
+
+    def set_capacity(self, per_image: int) -> None:
+        _check(self.lib, self.lib.dsift_set_capacity(self.ctx, per_image))
+
+    def submit(self, images, n: int | None = None, w: int | None = None, h: int | None = None,
+               device_ptr: int | None = None) -> None:
+        """Enqueue a batch: host array [n, h, w] / [h, w], or a device pointer."""
+        if device_ptr is not None:
+            _check(self.lib, self.lib.dsift_extract_batch(self.ctx, C.c_void_p(device_ptr), n, w, h,
+                                                          INPUT_DEVICE))
+            self.batch = n
+            return
+        a = np.ascontiguousarray(images, dtype=np.float32)
+        if a.ndim == 2:
+            a = a[None]
+        if a.ndim != 3:
+            raise InvalidArgument(DSIFT_EINVAL, "images must be [n, h, w] float32")
+        self._pin = a
+        _check(self.lib, self.lib.dsift_extract_batch(self.ctx, a.ctypes.data, a.shape[0], a.shape[2],
+                                                      a.shape[1], INPUT_HOST))
+        self.batch = a.shape[0]
+
+    def sync(self) -> int:
+        total = C.c_int64()
+        _check(self.lib, self.lib.dsift_result_sync(self.ctx, C.byref(total)))
+        return total.value
+
+    def results(self, with_u8: bool = True) -> list[FeatureSet]:
+        total = self.sync()
+        kps = np.zeros(total, KEYPOINT_DTYPE)
+        desc = np.zeros((total, DESC_DIM), np.float32)
+        u8 = np.zeros((total, DESC_DIM), np.uint8) if with_u8 else None
+        offs = np.zeros(self.batch + 1, np.int64)
+        _check(self.lib, self.lib.dsift_result_copy(self.ctx, kps.ctypes.data, desc.ctypes.data,
+                                                    u8.ctypes.data if with_u8 else None, offs.ctypes.data))
+        out = []
+        for b in range(self.batch):
+            s, e = int(offs[b]), int(offs[b + 1])
+            out.append(FeatureSet(kps[s:e], desc[s:e], u8[s:e] if with_u8 else None))
+        return out
+
+    def extract(self, img) -> FeatureSet:
+        """detsift::extract (io.cpp:111-142) for one image."""
+        self.submit(_f32(img))
+        return self.results()[0]
+
+    def extract_batch(self, imgs) -> list[FeatureSet]:
+        self.submit(imgs)
+        return self.results()
+
+    def sha256(self, image: int = 0) -> str:
+        buf = C.create_string_buffer(65)
+        _check(self.lib, self.lib.dsift_result_sha256(self.ctx, image, buf))
+        return buf.value.decode()
+
+    def kernel_launches(self) -> int:
+        return int(self.lib.dsift_kernel_launches(self.ctx))
+
+    def synth_value_noise(self, dev_ptr: int, n: int, w: int, h: int, seed0: int, octaves: int = 5,
+                          cells: int = 8) -> None:
+        _check(self.lib, self.lib.dsift_synth_value_noise(self.ctx, C.c_void_p(dev_ptr), n, w, h,
+                                                          C.c_uint64(seed0), octaves, cells))
+
+    # ---- stage level (scalespace.hpp / detect.hpp / orient.hpp / describe.hpp) ----
+    def build_scale_space(self, img) -> dict:
+        a = _f32(img)
+        _check(self.lib, self.lib.dsift_build_scale_space(self.ctx, a.ctypes.data, a.shape[1], a.shape[0],
+                                                          INPUT_HOST))
+        return self.scale_space_info()
+
+    def load_scale_space(self, gauss, dog, upsampled: bool = False) -> dict:
+        n_oct = len(gauss)
+        dims = np.array([v for o in range(n_oct) for v in (gauss[o][0].shape[1], gauss[o][0].shape[0])], np.int32)
+        g = [np.ascontiguousarray(x, np.float32) for o in range(n_oct) for x in gauss[o]]
+        d = [np.ascontiguousarray(x, np.float32) for o in range(n_oct) for x in dog[o]]
+        gp = (C.c_void_p * len(g))(*[x.ctypes.data for x in g])
+        dp = (C.c_void_p * len(d))(*[x.ctypes.data for x in d])
+        _check(self.lib, self.lib.dsift_load_scale_space(self.ctx, n_oct, int(upsampled), dims.ctypes.data, gp, dp))
+        return self.scale_space_info()
+
+    def scale_space_info(self) -> dict:
+        n, up = C.c_int32(), C.c_int32()
+        dims = np.zeros(128, np.int32)
+        _check(self.lib, self.lib.dsift_scale_space_info(self.ctx, C.byref(n), C.byref(up), dims.ctypes.data))
+        return {"n_oct": n.value, "upsampled": bool(up.value),
+                "dims": [(int(dims[2 * o]), int(dims[2 * o + 1])) for o in range(n.value)]}
+
+    def level(self, octave: int, kind: str, level: int) -> np.ndarray:
+        info = self.scale_space_info()
+        w, h = info["dims"][octave]
+        out = np.empty((h, w), np.float32)
+        _check(self.lib, self.lib.dsift_scale_space_level(self.ctx, octave, 0 if kind == "gauss" else 1, level,
+                                                          out.ctypes.data))
+        return out
+
+    def find_extrema(self) -> np.ndarray:
+        n = C.c_int64()
+        _check(self.lib, self.lib.dsift_find_extrema(self.ctx, None, 0, C.byref(n)))
+        out = np.zeros((max(1, n.value), 5), np.int32)
+        _check(self.lib, self.lib.dsift_find_extrema(self.ctx, out.ctypes.data, n.value, C.byref(n)))
+        return out[:n.value]
+
+    def detect(self) -> np.ndarray:
+        n = C.c_int64()
+        _check(self.lib, self.lib.dsift_detect(self.ctx, None, 0, C.byref(n)))
+        out = np.zeros(max(1, n.value), KEYPOINT_DTYPE)
+        _check(self.lib, self.lib.dsift_detect(self.ctx, out.ctypes.data, n.value, C.byref(n)))
+        return out[:n.value]
+
+    def orientation_histograms(self, kps) -> np.ndarray:
+        k = np.ascontiguousarray(kps, KEYPOINT_DTYPE)
+        out = np.zeros((len(k), self.cfg.orientation_bins), np.float32)
+        _check(self.lib, self.lib.dsift_orientation_histograms(self.ctx, k.ctypes.data, len(k), out.ctypes.data))
+        return out
+
+    def assign_orientations(self, kps) -> np.ndarray:
+        k = np.ascontiguousarray(kps, KEYPOINT_DTYPE)
+        cap = max(1, len(k) * self.cfg.orientation_bins)
+        out = np.zeros(cap, KEYPOINT_DTYPE)
+        n = C.c_int64()
+        _check(self.lib, self.lib.dsift_assign_orientations(self.ctx, k.ctypes.data, len(k), out.ctypes.data, cap,
+                                                            C.byref(n)))
+        return out[:n.value]
+
+    def raw_descriptors(self, kps, scale_factor: float) -> np.ndarray:
+        k = np.ascontiguousarray(kps, KEYPOINT_DTYPE)
+        out = np.zeros((len(k), DESC_DIM), np.float32)
+        _check(self.lib, self.lib.dsift_raw_descriptors(self.ctx, k.ctypes.data, len(k), scale_factor,
+                                                        out.ctypes.data))
+        return out
+
+    def dsp_descriptors(self, kps, with_u8: bool = False):
+        k = np.ascontiguousarray(kps, KEYPOINT_DTYPE)
+        out = np.zeros((len(k), DESC_DIM), np.float32)
+        u8 = np.zeros((len(k), DESC_DIM), np.uint8)
+        _check(self.lib, self.lib.dsift_dsp_descriptors(self.ctx, k.ctypes.data, len(k), out.ctypes.data,
+                                                        u8.ctypes.data))
+        return (out, u8) if with_u8 else out
+
+
+def extract(img, cfg: SiftConfig | None = None, device: int = 0) -> FeatureSet:
+    """FeatureSet detsift::extract(const GrayImage&, const SiftConfig&) on a B200."""
+    with Extractor(cfg, device) as ex:
+        return ex.extract(img)
+
+
+def quantize_u8(desc: np.ndarray) -> np.ndarray:
+    """The uint8 export q(v) = min(255, lround(v * 255.0)) applied on the host."""
+    v = np.asarray(desc, np.float64) * 255.0
+    q = np.floor(np.abs(v) + 0.5) * np.sign(v)
+    return np.clip(q, 0, 255).astype(np.uint8)

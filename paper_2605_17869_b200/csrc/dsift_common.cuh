@@ -1,0 +1,74 @@
+// dsift_common.cuh — device-side data layout shared by the kernels and the
+// host orchestration (dsift_host.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/dsift.h"
+
+namespace dsift {
+
+constexpr int kMaxOctaves = 24;
+constexpr int kMaxLevels = 16;      // s + 3 <= kMaxLevels
+constexpr int kMaxRadius = 64;      // largest Gaussian tap radius supported
+constexpr int kDescCells = 4;       // describe.hpp:11
+constexpr int kDescOrients = 8;     // describe.hpp:12
+constexpr int kDescDim = 128;       // describe.hpp:13
+constexpr int kMaxDsp = 16;         // dsp_scales entries
+constexpr int kMaxOriBins = 64;     // orientation_bins supported on device
+constexpr double kTwoPi = 6.283185307179586476925286766559;  // orient.cpp:37
+
+// Pyramid layout in HBM: for octave o, Gaussian levels are a dense array
+// [batch][s+3][h_o][pitch_o] and DoG levels [batch][s+2][h_o][pitch_o]
+// (pitch_o = w_o rounded up to 32 floats = 128 B so every row starts on a
+// cache-line boundary).
+struct OctaveDesc {
+    int w, h, pitch;
+    int tiles_x, tiles_y;      // extrema tiles
+    long long level_stride;    // pitch * h
+    float* gauss;              // [batch][s+3] levels
+    float* dog;                // [batch][s+2] levels
+};
+
+struct PyramidDesc {
+    int n_oct, s, batch, upsampled;
+    float sigma0;
+    OctaveDesc oct[kMaxOctaves];
+    double level_sigma[kMaxLevels];   // sigma0 * 2^(i/s)   (scalespace.cpp:11-13)
+    __host__ __device__ long long gauss_img_stride(int o) const { return (long long)(s + 3) * oct[o].level_stride; }
+    __host__ __device__ long long dog_img_stride(int o) const { return (long long)(s + 2) * oct[o].level_stride; }
+};
+
+// Keypoint as it travels between device stages (32 B).  `image` is the batch
+// index; `src` packs the originating candidate (octave, interval, row, col)
+// so stage-level APIs can restore the reference's candidate order.
+struct DevKeypoint {
+    float x, y, sigma, angle, response;
+    int32_t octave, interval;
+    int32_t image;
+};
+
+struct DevCandidate {   // raw extremum (detect.hpp:12-18)
+    int32_t image, octave, interval, row, col, is_max;
+};
+
+// Per-launch error word bits (OR-ed on device, checked at sync).
+enum : unsigned {
+    kErrKeypointCapacity = 1u,
+    kErrOrientedCapacity = 2u,
+    kErrCandidateCapacity = 4u,
+    kErrDescriptorLattice = 8u,
+};
+
+// Decoupled look-back scan state (per ticket): bit 63..62 = status.
+constexpr unsigned long long kLbAggregate = 1ull << 62;
+constexpr unsigned long long kLbPrefix = 2ull << 62;
+constexpr unsigned long long kLbValueMask = (1ull << 62) - 1;
+
+struct ScanState {
+    unsigned long long* states;   // [n_tiles]
+    unsigned int* ticket;         // dynamic tile ticket
+    unsigned long long* total;    // inclusive total (written by the last tile)
+};
+
+}  // namespace dsift

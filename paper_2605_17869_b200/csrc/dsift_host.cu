@@ -1,0 +1,1114 @@
+// dsift_host.cu — host orchestration and the C ABI (include/dsift.h).
+//
+// Replaces detsift::extract (io.cpp:111-142) and its parallel_for fan-out
+// (parallel.hpp:21-54): a batch of same-size images is pushed through
+// K1 (pyramid+DoG, per level, grid.z = image) -> K2/K3 (extrema+refine, one
+// launch for all octaves) -> K4 (orientation + fan-out) -> K7 (canonical
+// sort) -> K5/K6 (descriptors in canonical order), all on one stream, with a
+// single host synchronisation when the caller asks for the result.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dlpack_min.h"
+#include "dsift_common.cuh"
+#include "dsift_kernels.cuh"
+
+namespace dsift {
+
+
+// ---- errors -------------------------------------------------------------------
+thread_local std::string g_err;
+
+struct Error {
+    int code;
+    std::string msg;
+};
+
+static void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw Error{e == cudaErrorMemoryAllocation ? DSIFT_ENOMEM : DSIFT_ECUDA,
+                    std::string(what) + ": " + cudaGetErrorString(e)};
+}
+
+static void invalid(const std::string& m) { throw Error{DSIFT_EINVAL, m}; }
+
+template <typename F>
+static int guard(F&& f) {
+    try {
+        f();
+        return DSIFT_OK;
+    } catch (const Error& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return DSIFT_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return DSIFT_ECUDA;
+    }
+}
+
+// ---- config (core.hpp:30-47, core.cpp:17-46) -----------------------------------
+static const double kDefaultDsp[5] = {0.5, 1.0 / 1.4142135623730951, 1.0, 1.4142135623730951, 2.0};
+
+struct Cfg {
+    dsift_config c;
+    std::vector<double> dsp;
+};
+
+static void validate(const dsift_config& c) {
+    if (!(c.sigma0 > 0.0f) || !(c.assumed_blur >= 0.0f) || !(c.sigma0 > c.assumed_blur))
+        invalid("config: require sigma0 > assumed_input_blur >= 0");
+    if (c.intervals < 1) invalid("config: intervals_per_octave must be >= 1");
+    if (!(c.contrast_threshold > 0.0f)) invalid("config: contrast_threshold must be > 0");
+    if (!(c.edge_ratio > 1.0f)) invalid("config: edge_ratio must be > 1");
+    if (c.max_refine_iters < 1) invalid("config: max_refine_iters must be >= 1");
+    if (c.upsample_pixel_limit < 0) invalid("config: upsample_pixel_limit must be >= 0");
+    if (c.n_dsp_scales <= 0 || !c.dsp_scales) invalid("config: dsp_scales must be nonempty");
+    for (int i = 0; i < c.n_dsp_scales; ++i) {
+        if (!(c.dsp_scales[i] > 0.0)) invalid("config: dsp_scales must all be > 0");
+        if (i > 0 && !(c.dsp_scales[i] > c.dsp_scales[i - 1]))
+            invalid("config: dsp_scales must be strictly increasing");
+    }
+    if (!(c.descriptor_clip > 0.0f)) invalid("config: descriptor_clip must be > 0");
+    if (c.orientation_bins < 2) invalid("config: orientation_bins must be >= 2");
+    if (!(c.orientation_peak_ratio > 0.0f) || c.orientation_peak_ratio > 1.0f)
+        invalid("config: orientation_peak_ratio must be in (0,1]");
+    if (c.num_octaves < 0) invalid("config: num_octaves must be >= 0 (0 = auto)");
+    // device-implementation limits (explicit, never silent)
+    if (c.intervals + 3 > kMaxLevels) invalid("config: intervals_per_octave too large for this build");
+    if (c.n_dsp_scales > kMaxDsp) invalid("config: too many dsp_scales for this build");
+    if (c.orientation_bins > kMaxOriBins) invalid("config: orientation_bins too large for this build");
+}
+
+// ---- scale-space plan (scalespace.cpp:11-36, 144-214) --------------------------------
+static std::vector<float> gaussian_taps(double sigma) {
+    if (!(sigma > 0.0)) invalid("gaussian_kernel: sigma must be > 0");
+    const int radius = (int)std::ceil(4.0 * sigma);
+    std::vector<double> raw(2 * radius + 1);
+    double sum = 0.0;
+    for (int k = -radius; k <= radius; ++k) {
+        raw[k + radius] = std::exp(-double(k) * k / (2.0 * sigma * sigma));
+        sum += raw[k + radius];
+    }
+    std::vector<float> out(raw.size());
+    for (size_t i = 0; i < raw.size(); ++i) out[i] = (float)(raw[i] / sum);
+    return out;
+}
+
+struct Plan {
+    int in_w = 0, in_h = 0, base_w = 0, base_h = 0;
+    bool up = false;
+    int s = 3, n_oct = 0;
+    std::vector<int> ow, oh, pitch;
+    std::vector<float> bridge;
+    std::vector<std::vector<float>> inc;   // s+2 incremental kernels
+    double level_sigma[kMaxLevels] = {};
+    bool handcrafted = false;
+};
+
+static int round_pitch(int w) { return (w + 31) & ~31; }
+
+static Plan make_plan(const Cfg& cfg, int w, int h) {
+    const dsift_config& c = cfg.c;
+    if (w <= 0 || h <= 0) invalid("build_scale_space: empty image");
+    Plan p;
+    p.in_w = w;
+    p.in_h = h;
+    p.s = c.intervals;
+    p.up = (int64_t)w * h <= c.upsample_pixel_limit;
+    p.base_w = p.up ? 2 * w : w;
+    p.base_h = p.up ? 2 * h : h;
+    const double assumed = p.up ? 2.0 * c.assumed_blur : c.assumed_blur;
+    if (!((double)c.sigma0 > assumed)) invalid("build_scale_space: effective input blur exceeds sigma0");
+    if (std::min(p.base_w, p.base_h) < 8)
+        invalid("build_scale_space: image smaller than 8x8 after upsampling policy");
+    const int s = c.intervals;
+    int auto_oct = -2;
+    for (int d = std::min(p.base_w, p.base_h); d > 1; d /= 2) ++auto_oct;
+    auto_oct = std::max(1, auto_oct);
+    const double bridge = std::sqrt(double(c.sigma0) * c.sigma0 - assumed * assumed);
+    std::vector<double> inc;
+    for (int i = 1; i < s + 3; ++i)
+        inc.push_back(c.sigma0 * std::pow(2.0, double(i - 1) / s) * std::sqrt(std::pow(2.0, 2.0 / s) - 1.0));
+    int max_radius = (int)std::ceil(4.0 * bridge);
+    for (double sg : inc) max_radius = std::max(max_radius, (int)std::ceil(4.0 * sg));
+    if (std::max(p.base_w, p.base_h) < max_radius)
+        invalid("build_scale_space: image too small for the blur ladder");
+    if (max_radius > kMaxRadius) invalid("config: Gaussian radius exceeds this build's limit");
+    int feasible = 1;
+    for (int ww = p.base_w / 2, hh = p.base_h / 2; std::min(ww, hh) >= 8 && std::max(ww, hh) >= max_radius;
+         ww /= 2, hh /= 2)
+        ++feasible;
+    int oct = c.num_octaves > 0 ? std::min(c.num_octaves, auto_oct) : auto_oct;
+    oct = std::min(oct, feasible);
+    if (oct > kMaxOctaves) oct = kMaxOctaves;
+    p.n_oct = oct;
+    int ww = p.base_w, hh = p.base_h;
+    for (int o = 0; o < oct; ++o) {
+        p.ow.push_back(ww);
+        p.oh.push_back(hh);
+        p.pitch.push_back(round_pitch(ww));
+        ww /= 2;
+        hh /= 2;
+    }
+    p.bridge = gaussian_taps(bridge);
+    for (double sg : inc) p.inc.push_back(gaussian_taps(sg));
+    for (int i = 0; i < s + 3; ++i) p.level_sigma[i] = c.sigma0 * std::pow(2.0, double(i) / s);
+    return p;
+}
+
+// ---- device memory ---------------------------------------------------------------
+struct DevBuf {
+    std::shared_ptr<void> ptr;
+    size_t bytes = 0;
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr.get()); }
+    void ensure(size_t need) {
+        if (need <= bytes && ptr && ptr.use_count() == 1) return;
+        if (need < bytes) need = bytes;   // keep the larger size when forking an exported buffer
+        ptr.reset();
+        void* p = nullptr;
+        cuda_check(cudaMalloc(&p, std::max<size_t>(need, 256)), "cudaMalloc");
+        ptr = std::shared_ptr<void>(p, [](void* q) { cudaFree(q); });
+        bytes = std::max<size_t>(need, 256);
+    }
+};
+
+struct Counters {          // one small device block, cleared per batch
+    unsigned long long n_det;
+    unsigned long long n_ori;
+    unsigned err;
+    unsigned det_ticket;
+    unsigned ori_ticket;
+    unsigned pad;
+};
+
+}  // namespace dsift
+
+using namespace dsift;
+
+struct dsift_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    Cfg cfg;
+    long long cap_override = 0;
+    Plan plan;
+    int batch = 0;            // images in the current pyramid / result
+    PyramidDesc pyr{};
+    DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
+        pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out;
+    long long cap_det = 0, cap_ori = 0;
+    long long launches = 0;
+    bool result_pending = false, result_ready = false;
+    int64_t total = 0;
+    std::vector<int64_t> h_offsets;
+    int sm_count = 148;
+    cudaEvent_t done = nullptr;
+};
+
+namespace dsift {
+
+static void set_device(dsift_ctx* c) { cuda_check(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+static void build_pyramid_desc(dsift_ctx* c) {
+    const Plan& p = c->plan;
+    PyramidDesc d{};
+    d.n_oct = p.n_oct;
+    d.s = p.s;
+    d.batch = c->batch;
+    d.upsampled = p.up ? 1 : 0;
+    d.sigma0 = c->cfg.c.sigma0;
+    for (int i = 0; i < p.s + 3; ++i) d.level_sigma[i] = p.level_sigma[i];
+    size_t off = 0;
+    for (int o = 0; o < p.n_oct; ++o) {
+        OctaveDesc& od = d.oct[o];
+        od.w = p.ow[o];
+        od.h = p.oh[o];
+        od.pitch = p.pitch[o];
+        od.level_stride = (long long)od.pitch * od.h;
+        od.tiles_x = od.w >= 3 ? (od.w - 2 + 31) / 32 : 0;
+        od.tiles_y = od.h >= 3 ? (od.h - 2 + 31) / 32 : 0;
+        if (od.tiles_x == 0 || od.tiles_y == 0) od.tiles_x = od.tiles_y = 0;
+        const size_t g = sizeof(float) * (size_t)c->batch * (p.s + 3) * od.level_stride;
+        const size_t dg = sizeof(float) * (size_t)c->batch * (p.s + 2) * od.level_stride;
+        od.gauss = reinterpret_cast<float*>(off);
+        off += (g + 255) & ~size_t(255);
+        od.dog = reinterpret_cast<float*>(off);
+        off += (dg + 255) & ~size_t(255);
+    }
+    c->pyramid.ensure(off);
+    char* base = c->pyramid.as<char>();
+    for (int o = 0; o < p.n_oct; ++o) {
+        d.oct[o].gauss = reinterpret_cast<float*>(base + reinterpret_cast<size_t>(d.oct[o].gauss));
+        d.oct[o].dog = reinterpret_cast<float*>(base + reinterpret_cast<size_t>(d.oct[o].dog));
+    }
+    c->pyr = d;
+}
+
+static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
+    const Plan& p = c->plan;
+    const PyramidDesc& d = c->pyr;
+    const int s = p.s;
+    for (int o = 0; o < p.n_oct; ++o) {
+        const OctaveDesc& od = d.oct[o];
+        const long long gstride = d.gauss_img_stride(o), dstride = d.dog_img_stride(o);
+        auto fill_taps = [](BlurArgs& a, const std::vector<float>& t) {
+            for (size_t i = 0; i < t.size(); ++i) a.taps[i] = (double)t[i];
+        };
+        int first_level;
+        if (o == 0) {
+            BlurArgs a{};
+            a.src = dev_images;
+            a.src_img_stride = (long long)p.in_w * p.in_h;
+            a.src_pitch = p.in_w;
+            a.src_w = p.in_w;
+            a.src_h = p.in_h;
+            a.dst = od.gauss;
+            a.dst_img_stride = gstride;
+            a.w = od.w;
+            a.h = od.h;
+            a.pitch = od.pitch;
+            fill_taps(a, p.bridge);
+            cuda_check(launch_blur(a, p.up ? kModeUpsample : kModeRaw, (int)p.bridge.size() / 2, c->batch,
+                                   c->stream), "bridge blur");
+            ++c->launches;
+            first_level = 1;
+        } else {
+            const OctaveDesc& pd = d.oct[o - 1];
+            BlurArgs a{};
+            a.src = pd.gauss + (long long)s * pd.level_stride;
+            a.src_img_stride = d.gauss_img_stride(o - 1);
+            a.src_pitch = pd.pitch;
+            a.src_w = pd.w;
+            a.src_h = pd.h;
+            a.seed = od.gauss;
+            a.seed_img_stride = gstride;
+            a.dst = od.gauss + od.level_stride;
+            a.dst_img_stride = gstride;
+            a.dog = od.dog;
+            a.dog_img_stride = dstride;
+            a.w = od.w;
+            a.h = od.h;
+            a.pitch = od.pitch;
+            fill_taps(a, p.inc[0]);
+            cuda_check(launch_blur(a, kModeDecimate, (int)p.inc[0].size() / 2, c->batch, c->stream),
+                       "decimate blur");
+            ++c->launches;
+            first_level = 2;
+        }
+        for (int i = first_level; i < s + 3; ++i) {
+            BlurArgs a{};
+            a.src = od.gauss + (long long)(i - 1) * od.level_stride;
+            a.src_img_stride = gstride;
+            a.src_pitch = od.pitch;
+            a.src_w = od.w;
+            a.src_h = od.h;
+            a.dst = od.gauss + (long long)i * od.level_stride;
+            a.dst_img_stride = gstride;
+            a.dog = od.dog + (long long)(i - 1) * od.level_stride;
+            a.dog_img_stride = dstride;
+            a.w = od.w;
+            a.h = od.h;
+            a.pitch = od.pitch;
+            fill_taps(a, p.inc[i - 1]);
+            cuda_check(launch_blur(a, kModeLevel, (int)p.inc[i - 1].size() / 2, c->batch, c->stream),
+                       "level blur");
+            ++c->launches;
+        }
+        if (o == 0) {
+            // octave 0 has no DoG[0] from the bridge pass: it came with level 1 above.
+        }
+    }
+}
+
+static long long auto_cap(dsift_ctx* c, double factor) {
+    if (c->cap_override > 0) return c->cap_override;
+    const long long px = (long long)c->plan.in_w * c->plan.in_h;
+    return std::max<long long>(4096, (long long)(px * factor));
+}
+
+static Counters* counters(dsift_ctx* c) { return c->counters.as<Counters>(); }
+
+static unsigned detect_tiles(const PyramidDesc& d, int* base, int* per_image) {
+    int acc = 0;
+    for (int o = 0; o < d.n_oct; ++o) {
+        base[o] = acc;
+        acc += d.oct[o].tiles_x * d.oct[o].tiles_y;
+    }
+    base[d.n_oct] = acc;
+    *per_image = acc;
+    return (unsigned)acc * (unsigned)d.batch;
+}
+
+static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
+    const dsift_config& cf = c->cfg.c;
+    DetectArgs a{};
+    a.pyr = c->pyr;
+    a.n_tiles = detect_tiles(c->pyr, a.oct_tile_base, &a.tiles_per_image);
+    a.pre_gate = 0.5f * cf.contrast_threshold / cf.intervals;
+    a.contrast_gate = double(cf.contrast_threshold) / cf.intervals;
+    a.edge_r = cf.edge_ratio;
+    a.max_iters = cf.max_refine_iters;
+    a.raw_mode = raw_mode;
+    c->det_kps.ensure(sizeof(DevKeypoint) * (size_t)cap);
+    a.out = c->det_kps.as<DevKeypoint>();
+    a.cap = cap;
+    Counters* ctr = counters(c);
+    a.err = &ctr->err;
+    c->det_states.ensure(sizeof(unsigned long long) * (size_t)std::max(1u, a.n_tiles));
+    cuda_check(cudaMemsetAsync(c->det_states.as<void>(), 0, sizeof(unsigned long long) * std::max(1u, a.n_tiles),
+                               c->stream), "memset");
+    a.scan.states = c->det_states.as<unsigned long long>();
+    a.scan.ticket = &ctr->det_ticket;
+    a.scan.total = &ctr->n_det;
+    if (raw_mode) {
+        c->det_cand.ensure(sizeof(DevCandidate) * (size_t)cap);
+        a.cand_out = c->det_cand.as<DevCandidate>();
+    } else {
+        a.cand_out = nullptr;
+    }
+    cuda_check(launch_detect(a, c->stream), "detect");
+    ++c->launches;
+}
+
+static void run_detect_with_candidates(dsift_ctx* c, long long cap) {
+    // refine mode + originating candidates (stage API only)
+    const dsift_config& cf = c->cfg.c;
+    DetectArgs a{};
+    a.pyr = c->pyr;
+    a.n_tiles = detect_tiles(c->pyr, a.oct_tile_base, &a.tiles_per_image);
+    a.pre_gate = 0.5f * cf.contrast_threshold / cf.intervals;
+    a.contrast_gate = double(cf.contrast_threshold) / cf.intervals;
+    a.edge_r = cf.edge_ratio;
+    a.max_iters = cf.max_refine_iters;
+    a.raw_mode = 0;
+    c->det_kps.ensure(sizeof(DevKeypoint) * (size_t)cap);
+    c->det_cand.ensure(sizeof(DevCandidate) * (size_t)cap);
+    a.out = c->det_kps.as<DevKeypoint>();
+    a.cand_out = c->det_cand.as<DevCandidate>();
+    a.cap = cap;
+    Counters* ctr = counters(c);
+    a.err = &ctr->err;
+    c->det_states.ensure(sizeof(unsigned long long) * (size_t)std::max(1u, a.n_tiles));
+    cuda_check(cudaMemsetAsync(c->det_states.as<void>(), 0, sizeof(unsigned long long) * std::max(1u, a.n_tiles),
+                               c->stream), "memset");
+    a.scan.states = c->det_states.as<unsigned long long>();
+    a.scan.ticket = &ctr->det_ticket;
+    a.scan.total = &ctr->n_det;
+    cuda_check(launch_detect(a, c->stream), "detect");
+    ++c->launches;
+}
+
+static int orient_depth(const dsift_config& cf, const std::vector<dsift_keypoint>* kps, const Plan& p) {
+    // window <= (2R+1)^2 with R = lround(4.5 sigma_rel); sigma_rel <= sigma0 * 2^((s+0.5)/s)
+    double smax = cf.sigma0 * std::pow(2.0, (cf.intervals + 0.5) / cf.intervals) * 1.001;
+    if (kps)
+        for (const auto& k : *kps) {
+            const double to_input = std::ldexp(1.0, k.octave) * (p.up ? 0.5 : 1.0);
+            smax = std::max(smax, k.sigma / to_input);
+        }
+    const long long r = std::llround(4.5 * smax) + 1;
+    const long long n = (2 * r + 1) * (2 * r + 1);
+    int depth = 1;
+    while ((1ll << depth) <= n) ++depth;
+    return depth + 1;
+}
+
+static void run_orient(dsift_ctx* c, const DevKeypoint* kps, long long n_host, long long cap_kp,
+                       DevKeypoint* out, long long cap_out, float* hist_out, int depth) {
+    const dsift_config& cf = c->cfg.c;
+    OrientArgs a{};
+    a.pyr = c->pyr;
+    a.kps = kps;
+    Counters* ctr = counters(c);
+    a.n_dev = &ctr->n_det;
+    a.n_host = n_host;
+    a.bins = cf.orientation_bins;
+    a.peak_ratio = cf.orientation_peak_ratio;
+    a.depth = depth;
+    a.out = out;
+    a.cap = cap_out;
+    a.err = &ctr->err;
+    a.hist_out = hist_out;
+    const long long nk = n_host >= 0 ? n_host : cap_kp;
+    a.n_tiles = (unsigned)((nk + orient_tile_size() - 1) / orient_tile_size());
+    c->ori_states.ensure(sizeof(unsigned long long) * (size_t)std::max(1u, a.n_tiles));
+    cuda_check(cudaMemsetAsync(c->ori_states.as<void>(), 0, sizeof(unsigned long long) * std::max(1u, a.n_tiles),
+                               c->stream), "memset");
+    a.scan.states = c->ori_states.as<unsigned long long>();
+    a.scan.ticket = &ctr->ori_ticket;
+    a.scan.total = &ctr->n_ori;
+    cuda_check(launch_orient(a, c->stream), "orient");
+    ++c->launches;
+}
+
+static int describe_axis(const dsift_config& cf, const std::vector<double>& dsp, double smax) {
+    double fmax = 0.0;
+    for (double f : dsp) fmax = std::max(fmax, f);
+    const double bw = 3.0 * fmax * smax;
+    const long long r = std::llround(bw * 5.0 * 0.5 * 1.4142135623730951) + 2;
+    (void)cf;
+    return (int)(2 * r + 3);
+}
+
+static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host, float* desc,
+                         unsigned char* desc_u8, int raw_mode, double raw_scale, double smax,
+                         const unsigned long long* n_dev) {
+    const dsift_config& cf = c->cfg.c;
+    DescArgs a{};
+    a.pyr = c->pyr;
+    a.kps = kps;
+    a.n_dev = n_dev;
+    a.n_host = n_host;
+    a.n_dsp = (int)c->cfg.dsp.size();
+    for (int i = 0; i < a.n_dsp; ++i) a.dsp[i] = c->cfg.dsp[i];
+    a.clip = cf.descriptor_clip;
+    a.raw_mode = raw_mode;
+    a.raw_scale = raw_scale;
+    std::vector<double> fs = raw_mode ? std::vector<double>{raw_scale} : c->cfg.dsp;
+    a.max_axis = describe_axis(cf, fs, smax);
+    {
+        double fmax = 0.0;
+        for (double f : fs) fmax = std::max(fmax, f);
+        const double bw = 3.0 * fmax * smax;
+        if ((2.0 * bw + 2.0) * (2.0 * bw + 2.0) >= 65535.0)
+            invalid("descriptor: support window exceeds the per-bin tree capacity of this build");
+    }
+    a.chunk_rows = 16;
+    a.desc = desc;
+    a.desc_u8 = desc_u8;
+    a.err = &counters(c)->err;
+    const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, raw_mode ? 1 : a.n_dsp);
+    if (smem > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
+    const int per_sm = std::max(1, describe_blocks_per_sm(smem));
+    int grid = c->sm_count * per_sm;
+    if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
+    cuda_check(launch_describe(a, grid, c->stream), "describe");
+    ++c->launches;
+}
+
+static void ensure_counters(dsift_ctx* c) {
+    c->counters.ensure(sizeof(Counters));
+}
+
+static void reset_counters(dsift_ctx* c) {
+    cuda_check(cudaMemsetAsync(c->counters.as<void>(), 0, sizeof(Counters), c->stream), "memset");
+}
+
+static const float* stage_input(dsift_ctx* c, const float* images, int n, int w, int h, int flags) {
+    if (flags & DSIFT_INPUT_DEVICE) return images;
+    const size_t bytes = sizeof(float) * (size_t)n * w * h;
+    c->input.ensure(bytes);
+    cuda_check(cudaMemcpyAsync(c->input.as<void>(), images, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+    return c->input.as<float>();
+}
+
+static void extract_batch(dsift_ctx* c, const float* images, int n, int w, int h, int flags) {
+    if (n <= 0) invalid("extract: batch must contain at least one image");
+    if (!images) invalid("extract: null image pointer");
+    set_device(c);
+    c->plan = make_plan(c->cfg, w, h);
+    c->batch = n;
+    build_pyramid_desc(c);
+    ensure_counters(c);
+    reset_counters(c);
+    const float* dev_in = stage_input(c, images, n, w, h, flags);
+    launch_pyramid(c, dev_in);
+
+    c->cap_det = (long long)n * auto_cap(c, 1.0 / 24.0);
+    c->cap_ori = (long long)n * auto_cap(c, 1.0 / 16.0);
+    run_detect(c, 0, c->cap_det);
+    c->ori_kps.ensure(sizeof(DevKeypoint) * (size_t)c->cap_ori);
+    run_orient(c, c->det_kps.as<DevKeypoint>(), -1, c->cap_det, c->ori_kps.as<DevKeypoint>(), c->cap_ori,
+               nullptr, orient_depth(c->cfg.c, nullptr, c->plan));
+
+    // canonical order
+    const long long cap = c->cap_ori;
+    c->sort_keys.ensure(sizeof(unsigned long long) * 2 * (size_t)cap);
+    c->sort_idx.ensure(sizeof(int) * 2 * (size_t)cap);
+    const size_t tb = sort_temp_bytes(cap);
+    c->sort_temp.ensure(tb);
+    SortBuffers sb;
+    sb.keys_a = c->sort_keys.as<unsigned long long>();
+    sb.keys_b = sb.keys_a + cap;
+    sb.idx_a = c->sort_idx.as<int>();
+    sb.idx_b = sb.idx_a + cap;
+    sb.temp = c->sort_temp.as<void>();
+    sb.temp_bytes = tb;
+    c->sorted_kps.ensure(sizeof(DevKeypoint) * (size_t)cap);
+    c->pub_kps.ensure(sizeof(dsift_keypoint) * (size_t)cap);
+    c->offsets.ensure(sizeof(long long) * (size_t)(n + 1));
+    Counters* ctr = counters(c);
+    cuda_check(launch_canonical_sort(c->ori_kps.as<DevKeypoint>(), &ctr->n_ori, cap, sb,
+                                     c->sorted_kps.as<DevKeypoint>(), c->pub_kps.as<dsift_keypoint>(), n,
+                                     c->offsets.as<long long>(), c->stream, &c->launches),
+               "sort");
+    c->desc.ensure(sizeof(float) * kDescDim * (size_t)cap);
+    c->desc_u8.ensure((size_t)kDescDim * (size_t)cap);
+    const double smax = c->cfg.c.sigma0 * std::pow(2.0, (c->cfg.c.intervals + 0.5) / c->cfg.c.intervals) * 1.001;
+    run_describe(c, c->sorted_kps.as<DevKeypoint>(), -1, c->desc.as<float>(), c->desc_u8.as<unsigned char>(), 0,
+                 0.0, smax, &ctr->n_ori);
+    cuda_check(cudaEventRecord(c->done, c->stream), "event");
+    c->result_pending = true;
+    c->result_ready = false;
+}
+
+static void result_sync(dsift_ctx* c) {
+    if (!c->result_pending && !c->result_ready) throw Error{DSIFT_ESTATE, "result: no extract issued"};
+    if (c->result_ready) return;
+    set_device(c);
+    cuda_check(cudaEventSynchronize(c->done), "sync");
+    cuda_check(cudaGetLastError(), "async kernel error");
+    Counters h{};
+    cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(Counters), cudaMemcpyDeviceToHost), "D2H");
+    c->result_pending = false;
+    if (h.err) {
+        std::string m = "device work list overflow:";
+        if (h.err & kErrKeypointCapacity) m += " keypoints";
+        if (h.err & kErrOrientedCapacity) m += " oriented keypoints";
+        if (h.err & kErrCandidateCapacity) m += " candidates";
+        if (h.err & kErrDescriptorLattice) m += " descriptor lattice";
+        m += " (raise dsift_set_capacity)";
+        throw Error{DSIFT_ECAPACITY, m};
+    }
+    c->total = (int64_t)h.n_ori;
+    c->h_offsets.assign(c->batch + 1, 0);
+    cuda_check(cudaMemcpy(c->h_offsets.data(), c->offsets.as<void>(), sizeof(long long) * (c->batch + 1),
+                          cudaMemcpyDeviceToHost), "D2H");
+    c->result_ready = true;
+}
+
+// ---- SHA-256 / DSF1 (sha256.cpp, core.cpp:153-196), host side -------------------------
+static void sha256(const uint8_t* data, size_t n, char* hex) {
+    static const uint32_t K[64] = {
+        0x428a2f98, 0x71374491, 0xb5c0fbcf, 0xe9b5dba5, 0x3956c25b, 0x59f111f1, 0x923f82a4, 0xab1c5ed5,
+        0xd807aa98, 0x12835b01, 0x243185be, 0x550c7dc3, 0x72be5d74, 0x80deb1fe, 0x9bdc06a7, 0xc19bf174,
+        0xe49b69c1, 0xefbe4786, 0x0fc19dc6, 0x240ca1cc, 0x2de92c6f, 0x4a7484aa, 0x5cb0a9dc, 0x76f988da,
+        0x983e5152, 0xa831c66d, 0xb00327c8, 0xbf597fc7, 0xc6e00bf3, 0xd5a79147, 0x06ca6351, 0x14292967,
+        0x27b70a85, 0x2e1b2138, 0x4d2c6dfc, 0x53380d13, 0x650a7354, 0x766a0abb, 0x81c2c92e, 0x92722c85,
+        0xa2bfe8a1, 0xa81a664b, 0xc24b8b70, 0xc76c51a3, 0xd192e819, 0xd6990624, 0xf40e3585, 0x106aa070,
+        0x19a4c116, 0x1e376c08, 0x2748774c, 0x34b0bcb5, 0x391c0cb3, 0x4ed8aa4a, 0x5b9cca4f, 0x682e6ff3,
+        0x748f82ee, 0x78a5636f, 0x84c87814, 0x8cc70208, 0x90befffa, 0xa4506ceb, 0xbef9a3f7, 0xc67178f2};
+    uint32_t st[8] = {0x6a09e667, 0xbb67ae85, 0x3c6ef372, 0xa54ff53a, 0x510e527f, 0x9b05688c, 0x1f83d9ab, 0x5be0cd19};
+    auto rot = [](uint32_t x, int r) { return (x >> r) | (x << (32 - r)); };
+    auto block = [&](const uint8_t* p) {
+        uint32_t w[64];
+        for (int i = 0; i < 16; ++i)
+            w[i] = (uint32_t)p[4 * i] << 24 | (uint32_t)p[4 * i + 1] << 16 | (uint32_t)p[4 * i + 2] << 8 | p[4 * i + 3];
+        for (int i = 16; i < 64; ++i)
+            w[i] = w[i - 16] + (rot(w[i - 15], 7) ^ rot(w[i - 15], 18) ^ (w[i - 15] >> 3)) + w[i - 7] +
+                   (rot(w[i - 2], 17) ^ rot(w[i - 2], 19) ^ (w[i - 2] >> 10));
+        uint32_t a = st[0], b = st[1], c = st[2], d = st[3], e = st[4], f = st[5], g = st[6], h = st[7];
+        for (int i = 0; i < 64; ++i) {
+            const uint32_t t1 = h + (rot(e, 6) ^ rot(e, 11) ^ rot(e, 25)) + ((e & f) ^ (~e & g)) + K[i] + w[i];
+            const uint32_t t2 = (rot(a, 2) ^ rot(a, 13) ^ rot(a, 22)) + ((a & b) ^ (a & c) ^ (b & c));
+            h = g; g = f; f = e; e = d + t1; d = c; c = b; b = a; a = t1 + t2;
+        }
+        st[0] += a; st[1] += b; st[2] += c; st[3] += d; st[4] += e; st[5] += f; st[6] += g; st[7] += h;
+    };
+    size_t i = 0;
+    for (; i + 64 <= n; i += 64) block(data + i);
+    uint8_t tail[128] = {0};
+    const size_t rem = n - i;
+    std::memcpy(tail, data + i, rem);
+    tail[rem] = 0x80;
+    const size_t tl = rem + 9 <= 64 ? 64 : 128;
+    const uint64_t bits = (uint64_t)n * 8u;
+    for (int k = 0; k < 8; ++k) tail[tl - 1 - k] = (uint8_t)(bits >> (8 * k));
+    block(tail);
+    if (tl == 128) block(tail + 64);
+    for (int k = 0; k < 8; ++k) std::snprintf(hex + 8 * k, 9, "%08x", st[k]);
+    hex[64] = 0;
+}
+
+}  // namespace dsift
+
+// ================================ C ABI =========================================
+extern "C" {
+
+int dsift_abi_version(void) { return DSIFT_ABI_VERSION; }
+
+const char* dsift_strerror(int code) {
+    switch (code) {
+        case DSIFT_OK: return "ok";
+        case DSIFT_EINVAL: return "invalid argument";
+        case DSIFT_ECAPACITY: return "device capacity exceeded";
+        case DSIFT_ECUDA: return "CUDA error";
+        case DSIFT_ENOMEM: return "out of memory";
+        case DSIFT_ESTATE: return "invalid call order";
+        default: return "unknown error";
+    }
+}
+
+const char* dsift_last_error(void) { return g_err.c_str(); }
+
+void dsift_config_default(dsift_config* c) {
+    c->sigma0 = 1.6f;
+    c->intervals = 3;
+    c->assumed_blur = 0.5f;
+    c->contrast_threshold = 0.04f;
+    c->edge_ratio = 10.0f;
+    c->max_refine_iters = 5;
+    c->upsample_pixel_limit = 4000000;
+    c->dsp_scales = kDefaultDsp;
+    c->n_dsp_scales = 5;
+    c->descriptor_clip = 0.2f;
+    c->orientation_bins = 36;
+    c->orientation_peak_ratio = 0.8f;
+    c->num_octaves = 0;
+}
+
+int dsift_config_validate(const dsift_config* c) {
+    return guard([&] {
+        if (!c) invalid("config: null");
+        validate(*c);
+    });
+}
+
+int dsift_create(int device, const dsift_config* cfg, dsift_ctx** out) {
+    return guard([&] {
+        if (!out) invalid("create: null output");
+        dsift_config c;
+        if (cfg) c = *cfg; else dsift_config_default(&c);
+        validate(c);
+        auto ctx = std::make_unique<dsift_ctx>();
+        ctx->device = device;
+        ctx->cfg.c = c;
+        ctx->cfg.dsp.assign(c.dsp_scales, c.dsp_scales + c.n_dsp_scales);
+        ctx->cfg.c.dsp_scales = ctx->cfg.dsp.data();
+        int ndev = 0;
+        cuda_check(cudaGetDeviceCount(&ndev), "cudaGetDeviceCount");
+        if (device < 0 || device >= ndev) throw Error{DSIFT_ECUDA, "create: no such CUDA device"};
+        set_device(ctx.get());
+        cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+        ctx->stream = ctx->own_stream;
+        cuda_check(cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming), "event");
+        cuda_check(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
+        ensure_counters(ctx.get());
+        *out = ctx.release();
+    });
+}
+
+void dsift_destroy(dsift_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->done) cudaEventDestroy(c->done);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+int dsift_set_stream(dsift_ctx* c, void* s) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        c->stream = s ? static_cast<cudaStream_t>(s) : c->own_stream;
+    });
+}
+
+int dsift_set_capacity(dsift_ctx* c, int64_t cap) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (cap < 0) invalid("capacity must be >= 0");
+        c->cap_override = cap;
+    });
+}
+
+int dsift_extract_batch(dsift_ctx* c, const float* images, int n, int w, int h, int flags) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        extract_batch(c, images, n, w, h, flags);
+    });
+}
+
+int dsift_extract(dsift_ctx* c, const float* image, int w, int h, int flags) {
+    return dsift_extract_batch(c, image, 1, w, h, flags);
+}
+
+int dsift_result_sync(dsift_ctx* c, int64_t* total) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        result_sync(c);
+        if (total) *total = c->total;
+    });
+}
+
+int dsift_result_range(dsift_ctx* c, int image, int64_t* begin, int64_t* count) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        result_sync(c);
+        if (image < 0 || image >= c->batch) invalid("result: image index out of range");
+        if (begin) *begin = c->h_offsets[image];
+        if (count) *count = c->h_offsets[image + 1] - c->h_offsets[image];
+    });
+}
+
+int dsift_result_copy(dsift_ctx* c, dsift_keypoint* kps, float* desc, uint8_t* desc_u8, int64_t* offsets) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        result_sync(c);
+        const size_t n = (size_t)c->total;
+        if (kps && n)
+            cuda_check(cudaMemcpy(kps, c->pub_kps.as<void>(), n * sizeof(dsift_keypoint), cudaMemcpyDeviceToHost), "D2H");
+        if (desc && n)
+            cuda_check(cudaMemcpy(desc, c->desc.as<void>(), n * kDescDim * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+        if (desc_u8 && n)
+            cuda_check(cudaMemcpy(desc_u8, c->desc_u8.as<void>(), n * kDescDim, cudaMemcpyDeviceToHost), "D2H");
+        if (offsets) std::memcpy(offsets, c->h_offsets.data(), sizeof(int64_t) * (c->batch + 1));
+    });
+}
+
+int dsift_result_device(dsift_ctx* c, const dsift_keypoint** kps, const float** desc, const uint8_t** desc_u8,
+                        const int64_t** offsets) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (!c->result_pending && !c->result_ready) throw Error{DSIFT_ESTATE, "result: no extract issued"};
+        if (kps) *kps = c->pub_kps.as<dsift_keypoint>();
+        if (desc) *desc = c->desc.as<float>();
+        if (desc_u8) *desc_u8 = c->desc_u8.as<uint8_t>();
+        if (offsets) *offsets = reinterpret_cast<const int64_t*>(c->offsets.as<long long>());
+    });
+}
+
+struct DlHolder {
+    std::shared_ptr<void> keep;
+    int64_t shape[2];
+    DLManagedTensor t;
+};
+
+int dsift_export_dlpack(dsift_ctx* c, int which, void** out) {
+    return guard([&] {
+        if (!c || !out) invalid("null argument");
+        result_sync(c);
+        auto* h = new DlHolder();
+        DLTensor& t = h->t.dl_tensor;
+        t.device = {kDLCUDA, c->device};
+        t.ndim = 2;
+        t.strides = nullptr;
+        t.byte_offset = 0;
+        h->shape[0] = c->total;
+        if (which == DSIFT_EXPORT_KEYPOINTS) {
+            h->keep = c->pub_kps.ptr;
+            h->shape[1] = 7;
+            t.dtype = {kDLFloat, 32, 1};
+        } else if (which == DSIFT_EXPORT_DESC_F32) {
+            h->keep = c->desc.ptr;
+            h->shape[1] = kDescDim;
+            t.dtype = {kDLFloat, 32, 1};
+        } else if (which == DSIFT_EXPORT_DESC_U8) {
+            h->keep = c->desc_u8.ptr;
+            h->shape[1] = kDescDim;
+            t.dtype = {kDLUInt, 8, 1};
+        } else {
+            delete h;
+            invalid("export: unknown tensor");
+        }
+        t.data = h->keep.get();
+        t.shape = h->shape;
+        h->t.manager_ctx = h;
+        h->t.deleter = [](DLManagedTensor* self) { delete static_cast<DlHolder*>(self->manager_ctx); };
+        *out = &h->t;
+    });
+}
+
+int dsift_result_sha256(dsift_ctx* c, int image, char hex65[65]) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        result_sync(c);
+        if (image < 0 || image >= c->batch) invalid("result: image index out of range");
+        const int64_t b = c->h_offsets[image], n = c->h_offsets[image + 1] - b;
+        std::vector<uint8_t> buf(16 + (size_t)n * (28 + kDescDim * 4));
+        const uint32_t hdr[3] = {1u, (uint32_t)n, (uint32_t)kDescDim};
+        std::memcpy(buf.data(), "DSF1", 4);
+        std::memcpy(buf.data() + 4, hdr, 12);
+        if (n) {
+            cuda_check(cudaMemcpy(buf.data() + 16, c->pub_kps.as<dsift_keypoint>() + b, (size_t)n * 28,
+                                  cudaMemcpyDeviceToHost), "D2H");
+            cuda_check(cudaMemcpy(buf.data() + 16 + (size_t)n * 28, c->desc.as<float>() + b * kDescDim,
+                                  (size_t)n * kDescDim * 4, cudaMemcpyDeviceToHost), "D2H");
+        }
+        sha256(buf.data(), buf.size(), hex65);
+    });
+}
+
+// ---- stage level -------------------------------------------------------------------
+int dsift_build_scale_space(dsift_ctx* c, const float* image, int w, int h, int flags) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (!image) invalid("build_scale_space: null image");
+        set_device(c);
+        c->plan = make_plan(c->cfg, w, h);
+        c->batch = 1;
+        build_pyramid_desc(c);
+        ensure_counters(c);
+        const float* dev_in = stage_input(c, image, 1, w, h, flags);
+        launch_pyramid(c, dev_in);
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        c->result_pending = c->result_ready = false;
+    });
+}
+
+int dsift_load_scale_space(dsift_ctx* c, int n_oct, int upsampled, const int32_t* dims, const float* const* gauss,
+                           const float* const* dog) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (n_oct <= 0 || n_oct > kMaxOctaves) invalid("load_scale_space: bad octave count");
+        set_device(c);
+        Plan p;
+        p.s = c->cfg.c.intervals;
+        p.up = upsampled != 0;
+        p.n_oct = n_oct;
+        p.handcrafted = true;
+        for (int o = 0; o < n_oct; ++o) {
+            p.ow.push_back(dims[2 * o]);
+            p.oh.push_back(dims[2 * o + 1]);
+            p.pitch.push_back(round_pitch(dims[2 * o]));
+        }
+        p.in_w = dims[0];
+        p.in_h = dims[1];
+        for (int i = 0; i < p.s + 3; ++i) p.level_sigma[i] = c->cfg.c.sigma0 * std::pow(2.0, double(i) / p.s);
+        c->plan = p;
+        c->batch = 1;
+        build_pyramid_desc(c);
+        ensure_counters(c);
+        const int s = p.s;
+        for (int o = 0; o < n_oct; ++o) {
+            const OctaveDesc& od = c->pyr.oct[o];
+            for (int i = 0; i < s + 3; ++i)
+                cuda_check(cudaMemcpy2D(od.gauss + i * od.level_stride, sizeof(float) * od.pitch, gauss[o * (s + 3) + i],
+                                        sizeof(float) * od.w, sizeof(float) * od.w, od.h, cudaMemcpyHostToDevice), "H2D");
+            for (int i = 0; i < s + 2; ++i)
+                cuda_check(cudaMemcpy2D(od.dog + i * od.level_stride, sizeof(float) * od.pitch, dog[o * (s + 2) + i],
+                                        sizeof(float) * od.w, sizeof(float) * od.w, od.h, cudaMemcpyHostToDevice), "H2D");
+        }
+        c->result_pending = c->result_ready = false;
+    });
+}
+
+int dsift_scale_space_info(dsift_ctx* c, int32_t* n_oct, int32_t* upsampled, int32_t* dims) {
+    return guard([&] {
+        if (!c || c->plan.n_oct == 0) throw Error{DSIFT_ESTATE, "scale space: none built"};
+        if (n_oct) *n_oct = c->plan.n_oct;
+        if (upsampled) *upsampled = c->plan.up ? 1 : 0;
+        if (dims)
+            for (int o = 0; o < c->plan.n_oct; ++o) {
+                dims[2 * o] = c->plan.ow[o];
+                dims[2 * o + 1] = c->plan.oh[o];
+            }
+    });
+}
+
+int dsift_scale_space_level(dsift_ctx* c, int octave, int kind, int level, float* out) {
+    return guard([&] {
+        if (!c || c->plan.n_oct == 0) throw Error{DSIFT_ESTATE, "scale space: none built"};
+        if (octave < 0 || octave >= c->plan.n_oct) invalid("scale space: octave out of range");
+        const int nl = kind == 0 ? c->plan.s + 3 : c->plan.s + 2;
+        if (level < 0 || level >= nl) invalid("scale space: level out of range");
+        set_device(c);
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        const OctaveDesc& od = c->pyr.oct[octave];
+        const float* src = (kind == 0 ? od.gauss : od.dog) + (long long)level * od.level_stride;
+        cuda_check(cudaMemcpy2D(out, sizeof(float) * od.w, src, sizeof(float) * od.pitch, sizeof(float) * od.w, od.h,
+                                cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+static void require_space(dsift_ctx* c) {
+    if (c->plan.n_oct == 0) throw Error{DSIFT_ESTATE, "scale space: none built"};
+    if (c->batch != 1) throw Error{DSIFT_ESTATE, "stage API needs a single-image scale space"};
+}
+
+int dsift_find_extrema(dsift_ctx* c, int32_t* out5, int64_t cap, int64_t* n) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        require_space(c);
+        set_device(c);
+        long long dcap = 0;
+        for (int o = 0; o < c->plan.n_oct; ++o) dcap += (long long)c->plan.ow[o] * c->plan.oh[o] * c->plan.s / 2 + 16;
+        reset_counters(c);
+        run_detect(c, 1, dcap);
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        Counters h{};
+        cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+        std::vector<DevCandidate> v((size_t)h.n_det);
+        if (!v.empty())
+            cuda_check(cudaMemcpy(v.data(), c->det_cand.as<void>(), v.size() * sizeof(DevCandidate),
+                                  cudaMemcpyDeviceToHost), "D2H");
+        std::sort(v.begin(), v.end(), [](const DevCandidate& a, const DevCandidate& b) {
+            if (a.octave != b.octave) return a.octave < b.octave;
+            if (a.interval != b.interval) return a.interval < b.interval;
+            if (a.row != b.row) return a.row < b.row;
+            return a.col < b.col;
+        });
+        *n = (int64_t)v.size();
+        for (size_t k = 0; k < v.size() && (int64_t)k < cap; ++k) {
+            out5[5 * k + 0] = v[k].octave;
+            out5[5 * k + 1] = v[k].interval;
+            out5[5 * k + 2] = v[k].row;
+            out5[5 * k + 3] = v[k].col;
+            out5[5 * k + 4] = v[k].is_max;
+        }
+    });
+}
+
+int dsift_detect(dsift_ctx* c, dsift_keypoint* out, int64_t cap, int64_t* n) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        require_space(c);
+        set_device(c);
+        long long dcap = 0;
+        for (int o = 0; o < c->plan.n_oct; ++o) dcap += (long long)c->plan.ow[o] * c->plan.oh[o] * c->plan.s / 2 + 16;
+        reset_counters(c);
+        run_detect_with_candidates(c, dcap);
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        Counters h{};
+        cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+        const size_t m = (size_t)h.n_det;
+        std::vector<DevKeypoint> kp(m);
+        std::vector<DevCandidate> cd(m);
+        if (m) {
+            cuda_check(cudaMemcpy(kp.data(), c->det_kps.as<void>(), m * sizeof(DevKeypoint), cudaMemcpyDeviceToHost), "D2H");
+            cuda_check(cudaMemcpy(cd.data(), c->det_cand.as<void>(), m * sizeof(DevCandidate), cudaMemcpyDeviceToHost), "D2H");
+        }
+        std::vector<size_t> order(m);
+        for (size_t i = 0; i < m; ++i) order[i] = i;
+        std::stable_sort(order.begin(), order.end(), [&](size_t i, size_t j) {
+            const DevCandidate &a = cd[i], &b = cd[j];
+            if (a.octave != b.octave) return a.octave < b.octave;
+            if (a.interval != b.interval) return a.interval < b.interval;
+            if (a.row != b.row) return a.row < b.row;
+            return a.col < b.col;
+        });
+        *n = (int64_t)m;
+        for (size_t k = 0; k < m && (int64_t)k < cap; ++k) {
+            const DevKeypoint& s = kp[order[k]];
+            out[k] = dsift_keypoint{s.x, s.y, s.sigma, s.angle, s.response, s.octave, s.interval};
+        }
+    });
+}
+
+static DevKeypoint* upload_kps(dsift_ctx* c, const dsift_keypoint* kps, int64_t n) {
+    std::vector<DevKeypoint> v((size_t)n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (kps[i].octave < 0 || kps[i].octave >= c->plan.n_oct) invalid("keypoint octave out of range");
+        v[i] = DevKeypoint{kps[i].x, kps[i].y, kps[i].sigma, kps[i].angle, kps[i].response, kps[i].octave,
+                           kps[i].interval, 0};
+    }
+    c->stage_kps.ensure(sizeof(DevKeypoint) * (size_t)std::max<int64_t>(n, 1));
+    if (n) cuda_check(cudaMemcpy(c->stage_kps.as<void>(), v.data(), v.size() * sizeof(DevKeypoint),
+                                 cudaMemcpyHostToDevice), "H2D");
+    return c->stage_kps.as<DevKeypoint>();
+}
+
+static double stage_smax(dsift_ctx* c, const dsift_keypoint* kps, int64_t n) {
+    double smax = c->cfg.c.sigma0 * std::pow(2.0, (c->cfg.c.intervals + 0.5) / c->cfg.c.intervals) * 1.001;
+    for (int64_t i = 0; i < n; ++i) {
+        const double to_input = std::ldexp(1.0, kps[i].octave) * (c->plan.up ? 0.5 : 1.0);
+        smax = std::max(smax, kps[i].sigma / to_input * 1.001);
+    }
+    return smax;
+}
+
+int dsift_orientation_histograms(dsift_ctx* c, const dsift_keypoint* kps, int64_t n, float* out) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        require_space(c);
+        set_device(c);
+        if (n <= 0) return;
+        DevKeypoint* dk = upload_kps(c, kps, n);
+        std::vector<dsift_keypoint> hk(kps, kps + n);
+        const int bins = c->cfg.c.orientation_bins;
+        c->stage_out.ensure(sizeof(float) * (size_t)n * bins + sizeof(DevKeypoint) * (size_t)n * bins);
+        float* hist = c->stage_out.as<float>();
+        DevKeypoint* tmp = reinterpret_cast<DevKeypoint*>(hist + (size_t)n * bins);
+        reset_counters(c);
+        run_orient(c, dk, n, n, tmp, n * bins, hist, orient_depth(c->cfg.c, &hk, c->plan));
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        cuda_check(cudaMemcpy(out, hist, sizeof(float) * (size_t)n * bins, cudaMemcpyDeviceToHost), "D2H");
+    });
+}
+
+int dsift_assign_orientations(dsift_ctx* c, const dsift_keypoint* kps, int64_t n, dsift_keypoint* out, int64_t cap,
+                              int64_t* n_out) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        require_space(c);
+        set_device(c);
+        *n_out = 0;
+        if (n <= 0) return;
+        DevKeypoint* dk = upload_kps(c, kps, n);
+        std::vector<dsift_keypoint> hk(kps, kps + n);
+        const int bins = c->cfg.c.orientation_bins;
+        c->stage_out.ensure(sizeof(DevKeypoint) * (size_t)n * bins);
+        DevKeypoint* tmp = c->stage_out.as<DevKeypoint>();
+        reset_counters(c);
+        run_orient(c, dk, n, n, tmp, n * bins, nullptr, orient_depth(c->cfg.c, &hk, c->plan));
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        Counters h{};
+        cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+        std::vector<DevKeypoint> v((size_t)h.n_ori);
+        if (!v.empty())
+            cuda_check(cudaMemcpy(v.data(), tmp, v.size() * sizeof(DevKeypoint), cudaMemcpyDeviceToHost), "D2H");
+        *n_out = (int64_t)v.size();
+        for (size_t k = 0; k < v.size() && (int64_t)k < cap; ++k)
+            out[k] = dsift_keypoint{v[k].x, v[k].y, v[k].sigma, v[k].angle, v[k].response, v[k].octave, v[k].interval};
+    });
+}
+
+static void stage_describe(dsift_ctx* c, const dsift_keypoint* kps, int64_t n, float* out, uint8_t* out_u8,
+                           int raw_mode, double f) {
+    if (!c) invalid("null context");
+    require_space(c);
+    set_device(c);
+    if (raw_mode && !(f > 0.0)) invalid("raw_descriptor: scale_factor must be > 0");
+    if (n <= 0) return;
+    DevKeypoint* dk = upload_kps(c, kps, n);
+    c->stage_out.ensure(sizeof(float) * kDescDim * (size_t)n + (size_t)kDescDim * n);
+    float* d = c->stage_out.as<float>();
+    unsigned char* d8 = reinterpret_cast<unsigned char*>(d + (size_t)kDescDim * n);
+    reset_counters(c);
+    run_describe(c, dk, n, d, raw_mode ? nullptr : d8, raw_mode, f, stage_smax(c, kps, n), nullptr);
+    cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    Counters h{};
+    cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+    if (h.err & kErrDescriptorLattice) throw Error{DSIFT_ECAPACITY, "descriptor lattice exceeds table capacity"};
+    cuda_check(cudaMemcpy(out, d, sizeof(float) * kDescDim * (size_t)n, cudaMemcpyDeviceToHost), "D2H");
+    if (out_u8 && !raw_mode)
+        cuda_check(cudaMemcpy(out_u8, d8, (size_t)kDescDim * n, cudaMemcpyDeviceToHost), "D2H");
+}
+
+int dsift_raw_descriptors(dsift_ctx* c, const dsift_keypoint* kps, int64_t n, double f, float* out) {
+    return guard([&] { stage_describe(c, kps, n, out, nullptr, 1, f); });
+}
+
+int dsift_dsp_descriptors(dsift_ctx* c, const dsift_keypoint* kps, int64_t n, float* out, uint8_t* out_u8) {
+    return guard([&] { stage_describe(c, kps, n, out, out_u8, 0, 0.0); });
+}
+
+int dsift_synth_value_noise(dsift_ctx* c, float* dev_out, int n, int w, int h, uint64_t seed0, int octaves,
+                            int cells) {
+    return guard([&] {
+        if (!c || !dev_out) invalid("null argument");
+        if (n <= 0 || w <= 0 || h <= 0) invalid("synth: bad size");
+        set_device(c);
+        const int nparts = 64;
+        c->scratch.ensure(sizeof(double) * 2 * (size_t)n * nparts);
+        cuda_check(launch_value_noise(dev_out, n, w, h, seed0, octaves, cells, c->scratch.as<double>(), nparts,
+                                      c->stream), "synth");
+        c->launches += 2;
+    });
+}
+
+int64_t dsift_kernel_launches(dsift_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

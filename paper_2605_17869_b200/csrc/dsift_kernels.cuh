@@ -1,0 +1,97 @@
+// dsift_kernels.cuh — launch-argument structs and launcher entry points of
+// the device stages (one definition shared by k_*.cu and dsift_host.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "dsift_common.cuh"
+
+namespace dsift {
+
+enum BlurMode : int { kModeLevel = 0, kModeRaw = 1, kModeUpsample = 2, kModeDecimate = 3 };
+
+struct BlurArgs {
+    const float* src;
+    long long src_img_stride;
+    int src_pitch, src_w, src_h;
+    float* dst;
+    long long dst_img_stride;
+    float* dog;
+    long long dog_img_stride;
+    float* seed;
+    long long seed_img_stride;
+    int w, h, pitch;
+    double taps[2 * kMaxRadius + 1];
+};
+cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStream_t st);
+
+struct DetectArgs {
+    PyramidDesc pyr;
+    int tiles_per_image;
+    int oct_tile_base[kMaxOctaves + 1];
+    unsigned n_tiles;
+    float pre_gate;
+    double contrast_gate;
+    double edge_r;
+    int max_iters;
+    int raw_mode;
+    DevKeypoint* out;
+    DevCandidate* cand_out;
+    long long cap;
+    unsigned* err;
+    ScanState scan;
+};
+cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st);
+
+struct OrientArgs {
+    PyramidDesc pyr;
+    const DevKeypoint* kps;
+    const unsigned long long* n_dev;
+    long long n_host;
+    int bins;
+    float peak_ratio;
+    int depth;
+    DevKeypoint* out;
+    long long cap;
+    unsigned* err;
+    float* hist_out;
+    ScanState scan;
+    unsigned n_tiles;
+};
+cudaError_t launch_orient(const OrientArgs& a, cudaStream_t st);
+int orient_tile_size();
+
+struct DescArgs {
+    PyramidDesc pyr;
+    const DevKeypoint* kps;
+    const unsigned long long* n_dev;
+    long long n_host;
+    double dsp[kMaxDsp];
+    int n_dsp;
+    float clip;
+    int raw_mode;
+    double raw_scale;
+    int max_axis;
+    int chunk_rows;
+    float* desc;
+    unsigned char* desc_u8;
+    unsigned* err;
+};
+cudaError_t launch_describe(const DescArgs& a, int grid, cudaStream_t st);
+size_t describe_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
+
+struct SortBuffers {
+    unsigned long long *keys_a, *keys_b;
+    int *idx_a, *idx_b;
+    void* temp;
+    size_t temp_bytes;
+};
+size_t sort_temp_bytes(long long cap);
+cudaError_t launch_canonical_sort(const DevKeypoint* in, const unsigned long long* n_dev, long long cap,
+                                  const SortBuffers& sb, DevKeypoint* out, dsift_keypoint* out_pub,
+                                  int batch, long long* offsets, cudaStream_t st, long long* launches);
+cudaError_t launch_value_noise(float* out, int n, int w, int h, unsigned long long seed0, int octaves,
+                               int cells, double* scratch, int nparts, cudaStream_t st);
+
+int describe_blocks_per_sm(size_t smem);
+
+}  // namespace dsift

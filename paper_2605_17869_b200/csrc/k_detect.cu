@@ -1,0 +1,212 @@
+// k_detect.cu — K2+K3: scale-space extrema, Taylor refinement, contrast and
+// edge rejection, deterministic compaction (reference: detect.cpp:11-172).
+//
+// One launch covers every (image, octave, 32x32 tile) of the batch.  A tile
+// stages all s+2 DoG levels (+1-pixel halo) in shared memory once, tests the
+// strict 26-neighbour extremum on levels 1..s with the float pre-gate
+// |v| > 0.5f*ct/s (detect.cpp:35-36), refines each candidate in place with the
+// reference's FP64 Cramer solve (no FMA contraction: this file is compiled
+// with -fmad=false) and emits accepted keypoints through a warp-shuffle block
+// scan plus a decoupled look-back over ticket-ordered tiles.  Output order is
+// (image, octave, tile, thread, level, row) — fixed by construction, no
+// atomics on order; canonical order is restored later by the sort (K7).
+#include <cuda_runtime.h>
+
+#include "dsift_common.cuh"
+#include "dsift_kernels.cuh"
+#include "dsift_scan.cuh"
+
+namespace dsift {
+
+constexpr int kDetTile = 32;
+constexpr int kDetThreads = 256;
+constexpr int kDetHalo = kDetTile + 2;
+
+// refine_extremum (detect.cpp:73-156), bit-exact FP64 restatement.
+__device__ bool refine_candidate(const DetectArgs& a, int b, int o, int x, int y, int i,
+                                 DevKeypoint* kp) {
+    const OctaveDesc& od = a.pyr.oct[o];
+    const int s = a.pyr.s, w = od.w, h = od.h, pitch = od.pitch;
+    const float* __restrict__ dogb = od.dog + (long long)b * a.pyr.dog_img_stride(o);
+    const long long ls = od.level_stride;
+#define DAT(L, X, Y) ((double)__ldg(dogb + (long long)(L) * ls + (long long)(Y) * pitch + (X)))
+    double dx = 0, dy = 0, ds = 0, gx = 0, gy = 0, gs = 0, dxx = 0, dyy = 0, dxy = 0;
+    bool converged = false;
+    for (int it = 0; it < a.max_iters; ++it) {
+        const double v = DAT(i, x, y);
+        gx = 0.5 * (DAT(i, x + 1, y) - DAT(i, x - 1, y));
+        gy = 0.5 * (DAT(i, x, y + 1) - DAT(i, x, y - 1));
+        gs = 0.5 * (DAT(i + 1, x, y) - DAT(i - 1, x, y));
+        dxx = DAT(i, x + 1, y) + DAT(i, x - 1, y) - 2.0 * v;
+        dyy = DAT(i, x, y + 1) + DAT(i, x, y - 1) - 2.0 * v;
+        const double dss = DAT(i + 1, x, y) + DAT(i - 1, x, y) - 2.0 * v;
+        dxy = 0.25 * (DAT(i, x + 1, y + 1) - DAT(i, x - 1, y + 1) - DAT(i, x + 1, y - 1) +
+                      DAT(i, x - 1, y - 1));
+        const double dxs = 0.25 * (DAT(i + 1, x + 1, y) - DAT(i + 1, x - 1, y) -
+                                   DAT(i - 1, x + 1, y) + DAT(i - 1, x - 1, y));
+        const double dys = 0.25 * (DAT(i + 1, x, y + 1) - DAT(i + 1, x, y - 1) -
+                                   DAT(i - 1, x, y + 1) + DAT(i - 1, x, y - 1));
+        const double det = dxx * (dyy * dss - dys * dys) - dxy * (dxy * dss - dys * dxs) +
+                           dxs * (dxy * dys - dyy * dxs);
+        if (fabs(det) < 1e-12) return false;
+        const double det_x = -gx * (dyy * dss - dys * dys) - dxy * (-gy * dss - dys * -gs) +
+                             dxs * (-gy * dys - dyy * -gs);
+        const double det_y = dxx * (-gy * dss - dys * -gs) - (-gx) * (dxy * dss - dys * dxs) +
+                             dxs * (dxy * -gs - (-gy) * dxs);
+        const double det_s = dxx * (dyy * -gs - (-gy) * dys) - dxy * (dxy * -gs - (-gy) * dxs) +
+                             (-gx) * (dxy * dys - dyy * dxs);
+        dx = det_x / det;
+        dy = det_y / det;
+        ds = det_s / det;
+        if (fabs(dx) <= 0.5 && fabs(dy) <= 0.5 && fabs(ds) <= 0.5) {
+            converged = true;
+            break;
+        }
+        if (dx > 0.5) ++x; else if (dx < -0.5) --x;
+        if (dy > 0.5) ++y; else if (dy < -0.5) --y;
+        if (ds > 0.5) ++i; else if (ds < -0.5) --i;
+        if (x < 1 || x >= w - 1 || y < 1 || y >= h - 1 || i < 1 || i > s) return false;
+    }
+    if (!converged) return false;
+    const double value = DAT(i, x, y) + 0.5 * (gx * dx + gy * dy + gs * ds);
+#undef DAT
+    if (fabs(value) < a.contrast_gate) return false;
+    const double tr = dxx + dyy;
+    const double det2 = dxx * dyy - dxy * dxy;
+    const double r = a.edge_r;
+    if (det2 <= 0.0 || tr * tr * r >= det2 * (r + 1.0) * (r + 1.0)) return false;
+    const double to_input = ldexp(1.0, o) * (a.pyr.upsampled ? 0.5 : 1.0);
+    kp->x = (float)((x + dx) * to_input);
+    kp->y = (float)((y + dy) * to_input);
+    kp->sigma = (float)(a.pyr.sigma0 * pow(2.0, o + (i + ds) / s) * (a.pyr.upsampled ? 0.5 : 1.0));
+    kp->angle = 0.0f;
+    kp->response = (float)fabs(value);
+    kp->octave = o;
+    kp->interval = i;
+    kp->image = b;
+    return true;
+}
+
+__global__ void __launch_bounds__(kDetThreads)
+detect_kernel(const __grid_constant__ DetectArgs a) {
+    extern __shared__ float lv_s[];   // [s+2][34][34]
+    __shared__ unsigned ticket_s;
+    __shared__ unsigned long long off_s;
+    __shared__ int warp_tot[kDetThreads / 32];
+
+    const unsigned t = scan_ticket(a.scan, &ticket_s);
+    const int b = (int)(t / a.tiles_per_image);
+    const int rr = (int)(t % a.tiles_per_image);
+    int o = 0;
+    while (o + 1 < a.pyr.n_oct && a.oct_tile_base[o + 1] <= rr) ++o;
+    const OctaveDesc& od = a.pyr.oct[o];
+    const int tile = rr - a.oct_tile_base[o];
+    const int xs = 1 + (tile % od.tiles_x) * kDetTile;
+    const int ys = 1 + (tile / od.tiles_x) * kDetTile;
+    const int s = a.pyr.s, w = od.w, h = od.h;
+    const int nlev = s + 2;
+
+    const float* __restrict__ dogb = od.dog + (long long)b * a.pyr.dog_img_stride(o);
+    for (int idx = threadIdx.x; idx < nlev * kDetHalo * kDetHalo; idx += kDetThreads) {
+        const int l = idx / (kDetHalo * kDetHalo), rem = idx % (kDetHalo * kDetHalo);
+        const int yy = ys - 1 + rem / kDetHalo, xx = xs - 1 + rem % kDetHalo;
+        float v = 0.0f;
+        if (xx < w && yy < h) v = __ldg(dogb + (long long)l * od.level_stride + (long long)yy * od.pitch + xx);
+        lv_s[idx] = v;
+    }
+    __syncthreads();
+
+    const int lx = threadIdx.x & 31, ly0 = threadIdx.x >> 5;
+    auto S = [&](int l, int xl, int yl) -> float {
+        return lv_s[l * kDetHalo * kDetHalo + yl * kDetHalo + xl];
+    };
+    // strictly_extremal (detect.cpp:11-28) on the staged tile
+    auto extremal = [&](int i, int xl, int yl, float v, bool is_max) -> bool {
+#pragma unroll
+        for (int dyy = -1; dyy <= 1; ++dyy)
+#pragma unroll
+            for (int dxx = -1; dxx <= 1; ++dxx) {
+                const float nb = S(i - 1, xl + dxx, yl + dyy), na = S(i + 1, xl + dxx, yl + dyy);
+                if (is_max ? (nb >= v || na >= v) : (nb <= v || na <= v)) return false;
+                if (dxx == 0 && dyy == 0) continue;
+                const float nm = S(i, xl + dxx, yl + dyy);
+                if (is_max ? nm >= v : nm <= v) return false;
+            }
+        return true;
+    };
+
+    // pass 1: count accepted outputs per thread; pass 2: write them.
+    int count = 0;
+    unsigned long long base = 0;
+    for (int pass = 0; pass < 2; ++pass) {
+        int k = 0;
+        for (int i = 1; i <= s; ++i) {
+            for (int q = 0; q < kDetTile / 8; ++q) {
+                const int ly = ly0 + 8 * q;
+                const int x = xs + lx, y = ys + ly;
+                if (x > w - 2 || y > h - 2) continue;
+                const float v = S(i, lx + 1, ly + 1);
+                if (!(fabsf(v) > a.pre_gate)) continue;
+                const bool is_max = v > 0.0f;
+                if (!extremal(i, lx + 1, ly + 1, v, is_max)) continue;
+                if (a.raw_mode) {
+                    if (pass == 1) {
+                        const unsigned long long slot = base + k;
+                        if ((long long)slot < a.cap) {
+                            DevCandidate c = {b, o, i, y, x, is_max ? 1 : 0};
+                            a.cand_out[slot] = c;
+                        }
+                    }
+                    ++k;
+                    continue;
+                }
+                DevKeypoint kp;
+                if (!refine_candidate(a, b, o, x, y, i, &kp)) continue;
+                if (pass == 1) {
+                    const unsigned long long slot = base + k;
+                    if ((long long)slot < a.cap) {
+                        a.out[slot] = kp;
+                        if (a.cand_out) {
+                            DevCandidate c = {b, o, i, y, x, is_max ? 1 : 0};
+                            a.cand_out[slot] = c;
+                        }
+                    }
+                }
+                ++k;
+            }
+        }
+        if (pass == 0) {
+            count = k;
+            // block exclusive scan of per-thread counts (thread order)
+            int incl = count;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int n = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lx >= d) incl += n;
+            }
+            if (lx == 31) warp_tot[ly0] = incl;
+            __syncthreads();
+            int warp_off = 0, tile_total = 0;
+            for (int wq = 0; wq < kDetThreads / 32; ++wq) {
+                if (wq < ly0) warp_off += warp_tot[wq];
+                tile_total += warp_tot[wq];
+            }
+            const unsigned long long tile_off =
+                scan_exclusive(a.scan, t, (unsigned long long)tile_total, a.n_tiles, &off_s);
+            base = tile_off + warp_off + (incl - count);
+            if (threadIdx.x == 0 && (long long)(tile_off + tile_total) > a.cap)
+                atomicOr(a.err, a.raw_mode ? kErrCandidateCapacity : kErrKeypointCapacity);
+        }
+    }
+}
+
+cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st) {
+    if (a.n_tiles == 0) return cudaSuccess;
+    const size_t smem = sizeof(float) * (size_t)(a.pyr.s + 2) * kDetHalo * kDetHalo;
+    cudaError_t e = cudaFuncSetAttribute(detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    detect_kernel<<<a.n_tiles, kDetThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace dsift

@@ -1,0 +1,242 @@
+// k_orient.cu — K4: dominant orientations + fan-out (reference:
+// orient.cpp:13-113, io.cpp:117-125).
+//
+// A warp owns one keypoint at a time; a CTA (4 warps) owns a ticket-ordered
+// tile of 16 keypoints.  The warp walks the window in the reference's scan
+// order (row-major, 32 pixels per step), computes float central differences,
+// sqrtf, the glibc-exact atan2f and float(exp()) weight per pixel, and feeds
+// each bin's contributions, in scan order, into that bin's binary-counter
+// tree (dsift_tree.cuh) — __match_any_sync groups the lanes that hit the same
+// bin, the bin's owner lane pushes them in lane order.  No float atomics; the
+// per-bin sums are bit-identical to tree_accumulate_histogram.  Smoothing,
+// peak picking and parabolic refinement follow orient.cpp:62-113 in the
+// reference's precision; peaks are ranked by warp ballot, and the tile's copy
+// count goes through the decoupled look-back so oriented keypoints land in
+// keypoint order (the reference's flattened per-candidate slots).
+#include <cuda_runtime.h>
+
+#include "dsift_common.cuh"
+#include "dsift_kernels.cuh"
+#include "dsift_math.cuh"
+#include "dsift_scan.cuh"
+#include "dsift_tree.cuh"
+
+namespace dsift {
+
+constexpr int kOriWarps = 4;
+constexpr int kOriPerWarp = 4;
+constexpr int kOriTile = kOriWarps * kOriPerWarp;
+
+__device__ __forceinline__ int nearest_level(const PyramidDesc& p, double sigma_rel) {
+    // nearest_gauss_level (orient.cpp:13-24): strict < keeps the lower index on ties
+    int best = 0;
+    double best_diff = fabs(p.level_sigma[0] - sigma_rel);
+    for (int i = 1; i < p.s + 3; ++i) {
+        const double d = fabs(p.level_sigma[i] - sigma_rel);
+        if (d < best_diff) {
+            best_diff = d;
+            best = i;
+        }
+    }
+    return best;
+}
+
+__global__ void __launch_bounds__(kOriWarps * 32)
+orient_kernel(const __grid_constant__ OrientArgs a) {
+    extern __shared__ __align__(16) unsigned char sm_raw[];
+    const int bins = a.bins;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // per-warp: node[bins][depth] doubles | count[bins] | mask[bins] | vals[32] | hist[2][bins]
+    const size_t per_warp = sizeof(double) * bins * a.depth + sizeof(unsigned) * bins * 2 +
+                            sizeof(float) * 32 + sizeof(float) * 2 * bins;
+    const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
+    unsigned char* wbase = sm_raw + warp * per_warp_al;
+    double* node = reinterpret_cast<double*>(wbase);
+    unsigned* cnt = reinterpret_cast<unsigned*>(node + bins * a.depth);
+    unsigned* mask = cnt + bins;
+    float* vals = reinterpret_cast<float*>(mask + bins);
+    float* hist = vals + 32;
+    float* hist2 = hist + bins;
+    // per-CTA: angles[kOriTile][bins], copies[kOriTile]
+    float* ang = reinterpret_cast<float*>(sm_raw + kOriWarps * per_warp_al);
+    int* ncopy = reinterpret_cast<int*>(ang + kOriTile * bins);
+    __shared__ unsigned ticket_s;
+    __shared__ unsigned long long off_s;
+
+    const unsigned t = scan_ticket(a.scan, &ticket_s);
+    const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
+    const long long k0 = (long long)t * kOriTile;
+
+    for (int j = 0; j < kOriPerWarp; ++j) {
+        const int slot = warp * kOriPerWarp + j;
+        const long long k = k0 + slot;
+        if (k >= n) {
+            if (lane == 0) ncopy[slot] = 0;
+            continue;
+        }
+        const DevKeypoint kp = a.kps[k];
+        const PyramidDesc& p = a.pyr;
+        const OctaveDesc& od = p.oct[kp.octave];
+        const double to_input = ldexp(1.0, kp.octave) * (p.upsampled ? 0.5 : 1.0);
+        const double cx = kp.x / to_input, cy = kp.y / to_input;
+        const double sigma_rel = kp.sigma / to_input;
+        const int lvl = nearest_level(p, sigma_rel);
+        const float* __restrict__ img = od.gauss + (long long)kp.image * p.gauss_img_stride(kp.octave) +
+                                        (long long)lvl * od.level_stride;
+        const int radius = (int)llround(3.0 * 1.5 * sigma_rel);
+        const double denom = 2.0 * (1.5 * sigma_rel) * (1.5 * sigma_rel);
+        const int x0 = (int)llround(cx), y0 = (int)llround(cy);
+        const int ya = max(y0 - radius, 1), yb = min(y0 + radius, od.h - 2);
+        const int xa = max(x0 - radius, 1), xb = min(x0 + radius, od.w - 2);
+        const int nx = xb - xa + 1, ny = yb - ya + 1;
+        const int npx = (nx > 0 && ny > 0) ? nx * ny : 0;
+
+        for (int bb = lane; bb < bins; bb += 32) {
+            cnt[bb] = 0;
+            mask[bb] = 0;
+        }
+        __syncwarp();
+        for (int base = 0; base < npx; base += 32) {
+            const int q = base + lane;
+            int bin = -1;
+            float val = 0.0f;
+            if (q < npx) {
+                const int x = xa + q % nx, y = ya + q / nx;
+                const float* r0 = img + (long long)y * od.pitch;
+                const float gx = F_SUB(__ldg(r0 + x + 1), __ldg(r0 + x - 1));
+                const float gy = F_SUB(__ldg(r0 + od.pitch + x), __ldg(r0 - od.pitch + x));
+                const float mag = F_SQRT(F_ADD(F_MUL(gx, gx), F_MUL(gy, gy)));
+                float theta = dsift_atan2f(gy, gx);
+                if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
+                bin = (int)D_DIV((double)F_MUL(theta, (float)bins), kTwoPi);
+                if (bin >= bins) bin -= bins;
+                const double ddx = D_SUB((double)x, cx), ddy = D_SUB((double)y, cy);
+                const double arg = D_DIV(-D_ADD(D_MUL(ddx, ddx), D_MUL(ddy, ddy)), denom);
+                const float wgt = (float)dsift_exp(arg);
+                val = F_MUL(mag, wgt);
+            }
+            const unsigned grp = __match_any_sync(0xffffffffu, bin);
+            if (bin >= 0 && lane == __ffs(grp) - 1) mask[bin] = grp;
+            vals[lane] = val;
+            __syncwarp();
+            for (int bb = lane; bb < bins; bb += 32) {
+                unsigned m = mask[bb];
+                if (!m) continue;
+                mask[bb] = 0;
+                while (m) {
+                    const int l = __ffs(m) - 1;
+                    m &= m - 1;
+                    tree_push_smem(node + bb * a.depth, &cnt[bb], (double)vals[l]);
+                }
+            }
+            __syncwarp();
+        }
+        for (int bb = lane; bb < bins; bb += 32)
+            hist[bb] = (float)tree_result_smem(node + bb * a.depth, cnt[bb]);
+        __syncwarp();
+        if (a.hist_out)
+            for (int bb = lane; bb < bins; bb += 32) a.hist_out[k * bins + bb] = hist[bb];
+
+        // smooth_histogram_circular, 2 passes (orient.cpp:62-75)
+        float* cur = hist;
+        float* nxt = hist2;
+        for (int pass = 0; pass < 2; ++pass) {
+            for (int bb = lane; bb < bins; bb += 32) {
+                const double prev = cur[(bb + bins - 1) % bins], mid = cur[bb], succ = cur[(bb + 1) % bins];
+                nxt[bb] = (float)(0.25 * prev + 0.5 * mid + 0.25 * succ);
+            }
+            __syncwarp();
+            float* tmpp = cur;
+            cur = nxt;
+            nxt = tmpp;
+        }
+        // peaks (orient.cpp:77-113)
+        float mx = 0.0f;
+        for (int bb = lane; bb < bins; bb += 32) mx = fmaxf(mx, cur[bb]);
+#pragma unroll
+        for (int d = 16; d; d >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+        int total = 0;
+        if (mx > 0.0f) {
+            const float gate = a.peak_ratio * mx;
+            for (int chunk = 0; chunk < bins; chunk += 32) {
+                const int bb = chunk + lane;
+                bool pk = false;
+                float angf = 0.0f;
+                if (bb < bins) {
+                    const float h0 = cur[bb], hm = cur[(bb + bins - 1) % bins], hp = cur[(bb + 1) % bins];
+                    if (h0 > hm && h0 > hp && h0 >= gate) {
+                        pk = true;
+                        const double den = (double)hm - 2.0 * h0 + hp;
+                        const double delta = den != 0.0 ? 0.5 * ((double)hm - hp) / den : 0.0;
+                        double angle = (bb + delta) * kTwoPi / bins;
+                        if (angle < 0.0) angle += kTwoPi;
+                        if (angle >= kTwoPi) angle -= kTwoPi;
+                        angf = (float)angle;
+                        if (angf == 0.0f) angf = 0.0f;
+                        if (angf >= (float)kTwoPi) angf = 0.0f;
+                    }
+                }
+                const unsigned pm = __ballot_sync(0xffffffffu, pk);
+                if (pk) ang[slot * bins + total + __popc(pm & ((1u << lane) - 1u))] = angf;
+                total += __popc(pm);
+            }
+        }
+        if (total == 0) {
+            if (lane == 0) ang[slot * bins] = 0.0f;
+            total = 1;
+        }
+        if (lane == 0) ncopy[slot] = total;
+        __syncwarp();
+    }
+    __syncthreads();
+
+    // tile fan-out offsets (decoupled look-back in keypoint order)
+    if (threadIdx.x < 32) {
+        int c = threadIdx.x < kOriTile ? ncopy[threadIdx.x] : 0;
+        int incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, incl, d);
+            if ((int)threadIdx.x >= d) incl += v;
+        }
+        if (threadIdx.x < kOriTile) ncopy[kOriTile + threadIdx.x] = incl - c;   // exclusive
+        if (threadIdx.x == 31) ncopy[2 * kOriTile] = incl;
+    }
+    __syncthreads();
+    const int tile_total = ncopy[2 * kOriTile];
+    const unsigned long long off = scan_exclusive(a.scan, t, (unsigned long long)tile_total, a.n_tiles, &off_s);
+    if (threadIdx.x == 0 && (long long)(off + tile_total) > a.cap) atomicOr(a.err, kErrOrientedCapacity);
+    for (int slot = warp; slot < kOriTile; slot += kOriWarps) {
+        const long long k = k0 + slot;
+        if (k >= n) continue;
+        const DevKeypoint kp = a.kps[k];
+        const int nc = ncopy[slot];
+        const long long dst0 = (long long)off + ncopy[kOriTile + slot];
+        for (int c = lane; c < nc; c += 32) {
+            if (dst0 + c >= a.cap) break;
+            DevKeypoint cp = kp;
+            cp.angle = ang[slot * bins + c];
+            a.out[dst0 + c] = cp;
+        }
+    }
+}
+
+size_t orient_smem_bytes(int bins, int depth) {
+    const size_t per_warp = sizeof(double) * bins * depth + sizeof(unsigned) * bins * 2 +
+                            sizeof(float) * 32 + sizeof(float) * 2 * bins;
+    const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
+    return kOriWarps * per_warp_al + sizeof(float) * kOriTile * bins + sizeof(int) * (2 * kOriTile + 1);
+}
+
+cudaError_t launch_orient(const OrientArgs& a, cudaStream_t st) {
+    if (a.n_tiles == 0) return cudaSuccess;
+    const size_t smem = orient_smem_bytes(a.bins, a.depth);
+    cudaError_t e = cudaFuncSetAttribute(orient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    orient_kernel<<<a.n_tiles, kOriWarps * 32, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+int orient_tile_size() { return kOriTile; }
+
+}  // namespace dsift

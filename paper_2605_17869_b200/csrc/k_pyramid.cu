@@ -1,0 +1,242 @@
+// k_pyramid.cu — K1: Gaussian scale space + DoG (reference:
+// scalespace.cpp:52-111 convolve_separable, :113-131 upsample2x,
+// :133-142 decimate2x, :144-214 build_scale_space).
+//
+// One launch produces one Gaussian level for every image of the batch
+// (grid.z = image) and, in the same pass, the DoG level below it
+// (DoG[i-1] = G[i] - G[i-1], scalespace.cpp:204-211): the previous level is
+// already staged in shared memory as the blur input, so each level is read
+// once and G/DoG are each written once.
+//
+// Tile: 64 x 64 outputs, 256 threads.  The (64+2R)^2 input tile is staged in
+// shared memory with reflect-101 indexing (multi-bounce, scalespace.cpp:41-48),
+// the horizontal pass writes a float-rounded (64+2R) x 64 temporary to shared
+// memory, the vertical pass produces the outputs.  Every output is
+// Sum_t k[t] * x[t] accumulated left-to-right in FP64 and rounded to float
+// once, exactly as the reference; the products of two binary32 values are
+// exact in binary64, so each step is one DFMA (bit-identical to mul+add).
+// Each thread computes 4 adjacent outputs from a sliding register window so a
+// staged value is converted to double once and feeds 4 DFMAs.
+//
+// Modes (where the loader gets level-0 input from):
+//   LEVEL     G[i-1] of the same octave                       (incremental blur)
+//   RAW       the input image, no upsampling                  (bridge blur)
+//   UPSAMPLE  2x bilinear upsample of the input on the fly    (bridge blur)
+//   DECIMATE  even samples of G[s] of the previous octave; the kernel also
+//             writes those samples as this octave's G[0]      (seed + first blur)
+#include <cuda_runtime.h>
+
+#include "dsift_common.cuh"
+#include "dsift_kernels.cuh"
+
+namespace dsift {
+
+constexpr int kTileW = 64;
+constexpr int kTileH = 64;
+constexpr int kBlurThreads = 256;
+
+__device__ __forceinline__ int reflect101(int p, int n) {
+    if (n == 1) return 0;
+    while (p < 0 || p >= n) {
+        if (p < 0) p = -p;
+        if (p >= n) p = 2 * n - 2 - p;
+    }
+    return p;
+}
+
+template <int MODE>
+__device__ __forceinline__ float fetch_input(const BlurArgs& a, const float* __restrict__ src,
+                                             int gx, int gy) {
+    if (MODE == kModeUpsample) {
+        // upsample2x (scalespace.cpp:113-131): 0.25 * (((a + b) + c) + d) in double
+        const int y0 = gy >> 1, x0 = gx >> 1;
+        const int y1 = (gy & 1) ? min(y0 + 1, a.src_h - 1) : y0;
+        const int x1 = (gx & 1) ? min(x0 + 1, a.src_w - 1) : x0;
+        const float* r0 = src + (long long)y0 * a.src_pitch;
+        const float* r1 = src + (long long)y1 * a.src_pitch;
+        const double s = (((double)__ldg(r0 + x0) + (double)__ldg(r0 + x1)) + (double)__ldg(r1 + x0)) +
+                         (double)__ldg(r1 + x1);
+        return (float)(0.25 * s);
+    } else if (MODE == kModeDecimate) {
+        return __ldg(src + (long long)(2 * gy) * a.src_pitch + 2 * gx);
+    } else {
+        return __ldg(src + (long long)gy * a.src_pitch + gx);
+    }
+}
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(kBlurThreads)
+blur_level_kernel(const __grid_constant__ BlurArgs a) {
+    constexpr int kLen = 2 * R + 1;
+    constexpr int kInH = kTileH + 2 * R;
+    constexpr int kInW = kTileW + 2 * R;
+    constexpr int kInPitch = (kInW + 3) & ~3;      // float4-aligned rows
+    constexpr int kChunks = (2 * R + 4 + 3) / 4;   // float4 chunks per H window
+    extern __shared__ __align__(16) float smem[];
+    float* in_s = smem;                            // [kInH][kInPitch]
+    float* tmp_s = smem + kInH * kInPitch;         // [kInH][kTileW]
+
+    const int b = blockIdx.z;
+    const int x0 = blockIdx.x * kTileW, y0 = blockIdx.y * kTileH;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float* __restrict__ src = a.src + b * a.src_img_stride;
+
+    // ---- stage the input tile (reflect-101 at the borders) -------------------
+    for (int r = warp; r < kInH; r += kBlurThreads / 32) {
+        const int gy = reflect101(y0 - R + r, a.h);
+        for (int c = lane; c < kInW; c += 32) {
+            const int gx = reflect101(x0 - R + c, a.w);
+            in_s[r * kInPitch + c] = fetch_input<MODE>(a, src, gx, gy);
+        }
+    }
+    __syncthreads();
+
+    // ---- horizontal pass: rows [0, kInH), 4 columns per thread ---------------
+    for (int item = tid; item < kInH * (kTileW / 4); item += kBlurThreads) {
+        const int r = item / (kTileW / 4), g = item % (kTileW / 4);
+        const float4* row = reinterpret_cast<const float4*>(in_s + r * kInPitch + 4 * g);
+        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+#pragma unroll
+        for (int q = 0; q < kChunks; ++q) {
+            const float4 v4 = row[q];
+            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int e = 4 * q + m;
+                if (e >= 2 * R + 4) break;
+                const double x = (double)vv[m];
+                if (e - 0 >= 0 && e - 0 < kLen) acc0 = __fma_rn(a.taps[e - 0], x, acc0);
+                if (e - 1 >= 0 && e - 1 < kLen) acc1 = __fma_rn(a.taps[e - 1], x, acc1);
+                if (e - 2 >= 0 && e - 2 < kLen) acc2 = __fma_rn(a.taps[e - 2], x, acc2);
+                if (e - 3 >= 0 && e - 3 < kLen) acc3 = __fma_rn(a.taps[e - 3], x, acc3);
+            }
+        }
+        *reinterpret_cast<float4*>(tmp_s + r * kTileW + 4 * g) =
+            make_float4((float)acc0, (float)acc1, (float)acc2, (float)acc3);
+    }
+    __syncthreads();
+
+    // ---- vertical pass: 4 rows per thread, lanes along x ---------------------
+    float* __restrict__ dst = a.dst + b * a.dst_img_stride;
+    float* __restrict__ dog = a.dog ? a.dog + b * a.dog_img_stride : nullptr;
+    float* __restrict__ seed = (MODE == kModeDecimate) ? a.seed + b * a.seed_img_stride : nullptr;
+    for (int item = tid; item < kTileW * (kTileH / 4); item += kBlurThreads) {
+        const int c = item % kTileW, rg = item / kTileW;
+        const int x = x0 + c;
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int e = 0; e < 2 * R + 4; ++e) {
+            const double v = (double)tmp_s[(4 * rg + e) * kTileW + c];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int t = e - j;
+                if (t >= 0 && t < kLen) acc[j] = __fma_rn(a.taps[t], v, acc[j]);
+            }
+        }
+        if (x < a.w) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int y = y0 + 4 * rg + j;
+                if (y >= a.h) break;
+                const float g = (float)acc[j];
+                const long long o = (long long)y * a.pitch + x;
+                dst[o] = g;
+                if (MODE == kModeLevel || MODE == kModeDecimate) {
+                    const float prev = in_s[(4 * rg + j + R) * kInPitch + c + R];
+                    if (MODE == kModeDecimate) seed[o] = prev;
+                    if (dog) dog[o] = g - prev;
+                }
+            }
+        }
+    }
+}
+
+// Generic-radius fallback (R up to kMaxRadius); same arithmetic, runtime taps.
+template <int MODE>
+__global__ void __launch_bounds__(kBlurThreads)
+blur_level_kernel_any(const __grid_constant__ BlurArgs a, int R) {
+    const int kLen = 2 * R + 1, kInH = kTileH + 2 * R, kInW = kTileW + 2 * R;
+    const int kInPitch = (kInW + 3) & ~3;
+    extern __shared__ __align__(16) float smem[];
+    float* in_s = smem;
+    float* tmp_s = smem + kInH * kInPitch;
+    const int b = blockIdx.z;
+    const int x0 = blockIdx.x * kTileW, y0 = blockIdx.y * kTileH;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float* __restrict__ src = a.src + b * a.src_img_stride;
+    for (int r = warp; r < kInH; r += kBlurThreads / 32) {
+        const int gy = reflect101(y0 - R + r, a.h);
+        for (int c = lane; c < kInW; c += 32)
+            in_s[r * kInPitch + c] = fetch_input<MODE>(a, src, reflect101(x0 - R + c, a.w), gy);
+    }
+    __syncthreads();
+    for (int item = tid; item < kInH * kTileW; item += kBlurThreads) {
+        const int r = item / kTileW, c = item % kTileW;
+        double acc = 0.0;
+        for (int t = 0; t < kLen; ++t) acc = __fma_rn(a.taps[t], (double)in_s[r * kInPitch + c + t], acc);
+        tmp_s[r * kTileW + c] = (float)acc;
+    }
+    __syncthreads();
+    float* __restrict__ dst = a.dst + b * a.dst_img_stride;
+    float* __restrict__ dog = a.dog ? a.dog + b * a.dog_img_stride : nullptr;
+    float* __restrict__ seed = (MODE == kModeDecimate) ? a.seed + b * a.seed_img_stride : nullptr;
+    for (int item = tid; item < kTileW * kTileH; item += kBlurThreads) {
+        const int c = item % kTileW, r = item / kTileW;
+        const int x = x0 + c, y = y0 + r;
+        double acc = 0.0;
+        for (int t = 0; t < kLen; ++t) acc = __fma_rn(a.taps[t], (double)tmp_s[(r + t) * kTileW + c], acc);
+        if (x < a.w && y < a.h) {
+            const float g = (float)acc;
+            const long long o = (long long)y * a.pitch + x;
+            dst[o] = g;
+            if (MODE == kModeLevel || MODE == kModeDecimate) {
+                const float prev = in_s[(r + R) * kInPitch + c + R];
+                if (MODE == kModeDecimate) seed[o] = prev;
+                if (dog) dog[o] = g - prev;
+            }
+        }
+    }
+}
+
+static size_t blur_smem_bytes(int R) {
+    const int in_h = kTileH + 2 * R, in_w = kTileW + 2 * R;
+    const int in_pitch = (in_w + 3) & ~3;
+    return sizeof(float) * (size_t)(in_h * in_pitch + in_h * kTileW);
+}
+
+template <int MODE>
+static cudaError_t launch_mode(const BlurArgs& a, int R, int batch, cudaStream_t st) {
+    const dim3 grid((a.w + kTileW - 1) / kTileW, (a.h + kTileH - 1) / kTileH, batch);
+    const size_t smem = blur_smem_bytes(R);
+    void (*fn)(BlurArgs) = nullptr;
+    switch (R) {
+#define DSIFT_R(r) case r: fn = blur_level_kernel<r, MODE>; break;
+        DSIFT_R(1) DSIFT_R(2) DSIFT_R(3) DSIFT_R(4) DSIFT_R(5) DSIFT_R(6) DSIFT_R(7) DSIFT_R(8)
+        DSIFT_R(9) DSIFT_R(10) DSIFT_R(11) DSIFT_R(12) DSIFT_R(13) DSIFT_R(14) DSIFT_R(15)
+        DSIFT_R(16)
+#undef DSIFT_R
+        default: break;
+    }
+    if (fn) {
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        fn<<<grid, kBlurThreads, smem, st>>>(a);
+        return cudaGetLastError();
+    }
+    cudaError_t e = cudaFuncSetAttribute(blur_level_kernel_any<MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    blur_level_kernel_any<MODE><<<grid, kBlurThreads, smem, st>>>(a, R);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStream_t st) {
+    switch (mode) {
+        case kModeLevel: return launch_mode<kModeLevel>(a, R, batch, st);
+        case kModeRaw: return launch_mode<kModeRaw>(a, R, batch, st);
+        case kModeUpsample: return launch_mode<kModeUpsample>(a, R, batch, st);
+        default: return launch_mode<kModeDecimate>(a, R, batch, st);
+    }
+}
+
+}  // namespace dsift
