@@ -153,6 +153,19 @@ int dsift_synth_value_noise(dsift_ctx* ctx, float* dev_out, int n, int w, int h,
 /* ---- accounting -------------------------------------------------------------- */
 /* Number of kernel launches the context has issued since creation. */
 int64_t dsift_kernel_launches(dsift_ctx* ctx);
+/* Stage timing with CUDA events on the context stream (bench/profiling):
+ * ms5 = {input+pyramid, extrema+refine, orientation, canonical sort,
+ * descriptors} of the last extract. */
+int dsift_set_profiling(dsift_ctx* ctx, int on);
+/* Options: DSIFT_OPT_FORCE_EXACT = 1 routes every descriptor through the
+ * exact scan-order kernel (test hook for the certified fast path). */
+#define DSIFT_OPT_FORCE_EXACT 1
+int dsift_set_option(dsift_ctx* ctx, int key, int64_t value);
+/* Statistics of the last synced result: DSIFT_STAT_EXACT_FALLBACKS = number
+ * of keypoints whose descriptor the fast path could not certify. */
+#define DSIFT_STAT_EXACT_FALLBACKS 1
+int64_t dsift_stat(dsift_ctx* ctx, int key);
+int dsift_stage_times(dsift_ctx* ctx, float* ms5);
 
 #ifdef __cplusplus
 }

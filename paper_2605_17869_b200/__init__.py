@@ -147,6 +147,8 @@ def load_library():
         "dsift_dsp_descriptors": ([vp, vp, i64, vp, vp], C.c_int),
         "dsift_synth_value_noise": ([vp, vp, i32, i32, i32, C.c_uint64, i32, i32], C.c_int),
         "dsift_kernel_launches": ([vp], C.c_int64),
+        "dsift_set_profiling": ([vp, i32], C.c_int), "dsift_stage_times": ([vp, vp], C.c_int),
+        "dsift_set_option": ([vp, i32, i64], C.c_int), "dsift_stat": ([vp, i32], C.c_int64),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -258,6 +260,22 @@ class Extractor:
         buf = C.create_string_buffer(65)
         _check(self.lib, self.lib.dsift_result_sha256(self.ctx, image, buf))
         return buf.value.decode()
+
+    def set_profiling(self, on: bool = True) -> None:
+        _check(self.lib, self.lib.dsift_set_profiling(self.ctx, int(on)))
+
+    def stage_times(self) -> dict:
+        ms = (C.c_float * 5)()
+        _check(self.lib, self.lib.dsift_stage_times(self.ctx, ms))
+        return dict(zip(("pyramid", "detect", "orient", "sort", "describe"), [float(v) for v in ms]))
+
+    def set_force_exact(self, on: bool = True) -> None:
+        """Route every descriptor through the exact scan-order kernel (test hook)."""
+        _check(self.lib, self.lib.dsift_set_option(self.ctx, 1, int(on)))
+
+    def exact_fallbacks(self) -> int:
+        """Keypoints of the last result whose fast-path certificate failed."""
+        return int(self.lib.dsift_stat(self.ctx, 1))
 
     def kernel_launches(self) -> int:
         return int(self.lib.dsift_kernel_launches(self.ctx))

@@ -190,7 +190,7 @@ struct Counters {          // one small device block, cleared per batch
     unsigned err;
     unsigned det_ticket;
     unsigned ori_ticket;
-    unsigned pad;
+    unsigned n_slow;      // keypoints the certified fast descriptor path handed to the exact kernel
 };
 
 }  // namespace dsift
@@ -207,7 +207,7 @@ struct dsift_ctx {
     int batch = 0;            // images in the current pyramid / result
     PyramidDesc pyr{};
     DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
-        pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out;
+        pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow;
     long long cap_det = 0, cap_ori = 0;
     long long launches = 0;
     bool result_pending = false, result_ready = false;
@@ -215,6 +215,10 @@ struct dsift_ctx {
     std::vector<int64_t> h_offsets;
     int sm_count = 148;
     cudaEvent_t done = nullptr;
+    bool profiling = false;
+    int force_exact = 0;
+    unsigned long long last_slow = 0;
+    cudaEvent_t stage_ev[6] = {};
 };
 
 namespace dsift {
@@ -482,20 +486,52 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
         double fmax = 0.0;
         for (double f : fs) fmax = std::max(fmax, f);
         const double bw = 3.0 * fmax * smax;
-        if ((2.0 * bw + 2.0) * (2.0 * bw + 2.0) >= 65535.0)
+        if ((2.0 * bw + 2.0) * (2.0 * bw + 2.0) >= 8191.0)
             invalid("descriptor: support window exceeds the per-bin tree capacity of this build");
     }
-    a.chunk_rows = 16;
+    a.chunk_rows = 8;
+    {
+        const long long cap_n = n_host >= 0 ? n_host : c->cap_ori;
+        c->trig.ensure(sizeof(double2) * (size_t)std::max<long long>(1, cap_n));
+        cuda_check(launch_trig(kps, n_dev, n_host, c->trig.as<double2>(), cap_n, c->stream), "trig");
+        ++c->launches;
+        a.trig = c->trig.as<double2>();
+    }
     a.desc = desc;
     a.desc_u8 = desc_u8;
     a.err = &counters(c)->err;
-    const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, raw_mode ? 1 : a.n_dsp);
-    if (smem > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
-    const int per_sm = std::max(1, describe_blocks_per_sm(smem));
+    if (raw_mode) {
+        const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, 1);
+        if (smem > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
+        int grid = c->sm_count * 4;
+        if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
+        cuda_check(launch_describe(a, grid, c->stream), "describe exact");
+        ++c->launches;
+        return;
+    }
+    // certified fast path over every keypoint, then the exact kernel over the
+    // (rare) keypoints whose certificate failed
+    const long long cap_n = n_host >= 0 ? n_host : c->cap_ori;
+    c->slow.ensure(sizeof(int) * (size_t)std::max<long long>(1, cap_n));
+    Counters* ctr = counters(c);
+    a.slow_out = c->slow.as<int>();
+    a.slow_count = &ctr->n_slow;
+    a.slow_cap = cap_n;
+    a.force_slow = c->force_exact;
+    const size_t smem_fast = describe_fast_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
+    const size_t smem_exact = describe_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
+    if (smem_fast > 200 * 1024 || smem_exact > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
+    const int per_sm = std::max(1, describe_blocks_per_sm(smem_fast));
     int grid = c->sm_count * per_sm;
     if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
-    cuda_check(launch_describe(a, grid, c->stream), "describe");
-    ++c->launches;
+    cuda_check(launch_describe_fast(a, grid, c->stream), "describe fast");
+    DescArgs b = a;
+    b.slow_list = c->slow.as<int>();
+    b.n_slow = &ctr->n_slow;
+    int grid2 = c->sm_count * 4;
+    if (n_host >= 0) grid2 = (int)std::max<long long>(1, std::min<long long>(grid2, n_host));
+    cuda_check(launch_describe(b, grid2, c->stream), "describe exact");
+    c->launches += 2;
 }
 
 static void ensure_counters(dsift_ctx* c) {
@@ -523,15 +559,19 @@ static void extract_batch(dsift_ctx* c, const float* images, int n, int w, int h
     build_pyramid_desc(c);
     ensure_counters(c);
     reset_counters(c);
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[0], c->stream), "event");
     const float* dev_in = stage_input(c, images, n, w, h, flags);
     launch_pyramid(c, dev_in);
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[1], c->stream), "event");
 
     c->cap_det = (long long)n * auto_cap(c, 1.0 / 24.0);
     c->cap_ori = (long long)n * auto_cap(c, 1.0 / 16.0);
     run_detect(c, 0, c->cap_det);
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[2], c->stream), "event");
     c->ori_kps.ensure(sizeof(DevKeypoint) * (size_t)c->cap_ori);
     run_orient(c, c->det_kps.as<DevKeypoint>(), -1, c->cap_det, c->ori_kps.as<DevKeypoint>(), c->cap_ori,
                nullptr, orient_depth(c->cfg.c, nullptr, c->plan));
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[3], c->stream), "event");
 
     // canonical order
     const long long cap = c->cap_ori;
@@ -554,11 +594,13 @@ static void extract_batch(dsift_ctx* c, const float* images, int n, int w, int h
                                      c->sorted_kps.as<DevKeypoint>(), c->pub_kps.as<dsift_keypoint>(), n,
                                      c->offsets.as<long long>(), c->stream, &c->launches),
                "sort");
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[4], c->stream), "event");
     c->desc.ensure(sizeof(float) * kDescDim * (size_t)cap);
     c->desc_u8.ensure((size_t)kDescDim * (size_t)cap);
     const double smax = c->cfg.c.sigma0 * std::pow(2.0, (c->cfg.c.intervals + 0.5) / c->cfg.c.intervals) * 1.001;
     run_describe(c, c->sorted_kps.as<DevKeypoint>(), -1, c->desc.as<float>(), c->desc_u8.as<unsigned char>(), 0,
                  0.0, smax, &ctr->n_ori);
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[5], c->stream), "event");
     cuda_check(cudaEventRecord(c->done, c->stream), "event");
     c->result_pending = true;
     c->result_ready = false;
@@ -583,6 +625,7 @@ static void result_sync(dsift_ctx* c) {
         throw Error{DSIFT_ECAPACITY, m};
     }
     c->total = (int64_t)h.n_ori;
+    c->last_slow = h.n_slow;
     c->h_offsets.assign(c->batch + 1, 0);
     cuda_check(cudaMemcpy(c->h_offsets.data(), c->offsets.as<void>(), sizeof(long long) * (c->batch + 1),
                           cudaMemcpyDeviceToHost), "D2H");
@@ -705,6 +748,8 @@ void dsift_destroy(dsift_ctx* c) {
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
     if (c->done) cudaEventDestroy(c->done);
+    for (auto& e : c->stage_ev)
+        if (e) cudaEventDestroy(e);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -1110,5 +1155,39 @@ int dsift_synth_value_noise(dsift_ctx* c, float* dev_out, int n, int w, int h, u
 }
 
 int64_t dsift_kernel_launches(dsift_ctx* c) { return c ? c->launches : 0; }
+
+int dsift_set_option(dsift_ctx* c, int key, int64_t value) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (key == DSIFT_OPT_FORCE_EXACT) c->force_exact = value ? 1 : 0;
+        else invalid("set_option: unknown key");
+    });
+}
+
+int64_t dsift_stat(dsift_ctx* c, int key) {
+    if (!c) return -1;
+    if (key == DSIFT_STAT_EXACT_FALLBACKS) return (int64_t)c->last_slow;
+    return -1;
+}
+
+int dsift_set_profiling(dsift_ctx* c, int on) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        set_device(c);
+        if (on && !c->stage_ev[0])
+            for (auto& e : c->stage_ev) cuda_check(cudaEventCreate(&e), "event");
+        c->profiling = on != 0;
+    });
+}
+
+int dsift_stage_times(dsift_ctx* c, float* ms5) {
+    return guard([&] {
+        if (!c || !c->profiling) throw Error{DSIFT_ESTATE, "profiling not enabled"};
+        set_device(c);
+        cuda_check(cudaEventSynchronize(c->stage_ev[5]), "sync");
+        for (int i = 0; i < 5; ++i)
+            cuda_check(cudaEventElapsedTime(&ms5[i], c->stage_ev[i], c->stage_ev[i + 1]), "elapsed");
+    });
+}
 
 }  // extern "C"

@@ -72,6 +72,13 @@ struct DescArgs {
     double raw_scale;
     int max_axis;
     int chunk_rows;
+    const double2* trig;   // [n] (cos, sin) of the angle
+    const int* slow_list;  // exact kernel: process only these keypoints (nullable)
+    const unsigned* n_slow;
+    int* slow_out;         // fast kernel: keypoints it could not certify
+    unsigned* slow_count;
+    long long slow_cap;
+    int force_slow;        // test hook: fail every certificate
     float* desc;
     unsigned char* desc_u8;
     unsigned* err;
@@ -93,5 +100,9 @@ cudaError_t launch_value_noise(float* out, int n, int w, int h, unsigned long lo
                                int cells, double* scratch, int nparts, cudaStream_t st);
 
 int describe_blocks_per_sm(size_t smem);
+size_t describe_fast_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
+cudaError_t launch_describe_fast(const DescArgs& a, int grid, cudaStream_t st);
+cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev, long long n_host, double2* trig,
+                        long long cap, cudaStream_t st);
 
 }  // namespace dsift

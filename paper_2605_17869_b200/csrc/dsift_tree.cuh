@@ -13,38 +13,53 @@
 
 namespace dsift {
 
-// Register-resident counter (slots statically indexed -> no local memory).
+// Register-resident counter.  push() is a compile-time chain of nested
+// branches (one per slot), so every slot index is static and the slots stay
+// in registers (a runtime loop with `break` is not unrolled by ptxas and would
+// spill the array to local memory).
+template <int J, int DEPTH>
+struct TreePushStep {
+    __device__ __forceinline__ static void run(double (&node)[DEPTH], unsigned c, double x) {
+        if (c & 1u) {
+            TreePushStep<J + 1, DEPTH>::run(node, c >> 1, node[J] + x);
+        } else {
+            node[J] = x;
+        }
+    }
+};
+template <int DEPTH>
+struct TreePushStep<DEPTH, DEPTH> {
+    __device__ __forceinline__ static void run(double (&)[DEPTH], unsigned, double) {}
+};
+template <int J, int DEPTH>
+struct TreeFoldStep {
+    __device__ __forceinline__ static void run(const double (&node)[DEPTH], unsigned c, double& r, bool& have) {
+        if (c & 1u) {
+            r = have ? node[J] + r : node[J];
+            have = true;
+        }
+        if (c >> 1) TreeFoldStep<J + 1, DEPTH>::run(node, c >> 1, r, have);
+    }
+};
+template <int DEPTH>
+struct TreeFoldStep<DEPTH, DEPTH> {
+    __device__ __forceinline__ static void run(const double (&)[DEPTH], unsigned, double&, bool&) {}
+};
+
 template <int DEPTH>
 struct TreeCounter {
     double node[DEPTH];
     unsigned count;
 
     __device__ __forceinline__ void reset() { count = 0; }
-
     __device__ __forceinline__ void push(double x) {
-        const unsigned c = count;
-#pragma unroll
-        for (int j = 0; j < DEPTH; ++j) {
-            if ((c >> j) & 1u) {
-                x = node[j] + x;
-            } else {
-                node[j] = x;
-                break;
-            }
-        }
-        count = c + 1;
+        TreePushStep<0, DEPTH>::run(node, count, x);
+        ++count;
     }
-
     __device__ __forceinline__ double result() const {
         double r = 0.0;
         bool have = false;
-#pragma unroll
-        for (int j = 0; j < DEPTH; ++j) {
-            if ((count >> j) & 1u) {
-                r = have ? node[j] + r : node[j];
-                have = true;
-            }
-        }
+        TreeFoldStep<0, DEPTH>::run(node, count, r, have);
         return r;
     }
 };

@@ -30,7 +30,8 @@
 namespace dsift {
 
 constexpr int kDescThreads = 128;
-constexpr int kTreeDepth = 16;   // per-bin leaves < 65536 (checked on the host)
+constexpr int kTreeDepth = 13;   // per-bin leaves < 8192 (checked on the host)
+constexpr int kRing = 32;        // per-bin leaf ring (flushed every 16 candidate points)
 constexpr float kUndef = -1.0f;  // describe.cpp:188
 
 struct DescSmem {
@@ -43,11 +44,13 @@ struct DescSmem {
     double* cv;     // cos*v
     float* frac;
     int* c0;
-    float* samp;    // [(chunk+2)][width+2]
-    float* pval;    // [chunk][width]
-    float* pfo;
-    unsigned char* po0;
+    float* samp;    // [(chunk+2)][max_axis]
+    float* pval;    // [chunk][pw]
+    float* pfo;     // [chunk][pw]
+    unsigned* omask;  // [chunk][8][nw]: bit cc set iff point o0 == o
     float* raw;     // [n_dsp][128]
+    float* ring;    // [kRing][128]: per-bin leaves not yet folded (slot-major)
+    double* node;   // [kTreeDepth-3][128]: per-bin pending 8-leaf-aligned tree nodes
 };
 
 __device__ __forceinline__ int nearest_level_d(const PyramidDesc& p, double sigma_rel) {
@@ -89,8 +92,8 @@ __device__ __forceinline__ double tree128(double v, double* red) {
     return (red[0] + red[1]) + (red[2] + red[3]);
 }
 
-__device__ void raw_descriptor_cta(const DescArgs& a, const DescSmem& S, const DevKeypoint& kp,
-                                   double f, double cosa, double sina, float* raw_out) {
+__device__ __forceinline__ void raw_descriptor_cta(const DescArgs& a, const DescSmem& S, const DevKeypoint& kp,
+                                                   double f, double cosa, double sina, float* raw_out) {
     const PyramidDesc& p = a.pyr;
     const OctaveDesc& od = p.oct[kp.octave];
     const double to_input = ldexp(1.0, kp.octave) * (p.upsampled ? 0.5 : 1.0);
@@ -102,7 +105,7 @@ __device__ void raw_descriptor_cta(const DescArgs& a, const DescSmem& S, const D
     const int w = od.w, h = od.h, pitch = od.pitch;
     const double bw = 3.0 * f * sigma_rel;
     const int radius = (int)llround(bw * (kDescCells + 1) * 0.5 * 1.4142135623730951);
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (2 * radius + 3 > a.max_axis) {   // host sized the tables for r_max; never silently clip
         if (tid == 0) atomicOr(a.err, kErrDescriptorLattice);
         raw_out[tid] = 0.0f;
@@ -112,7 +115,7 @@ __device__ void raw_descriptor_cta(const DescArgs& a, const DescSmem& S, const D
     const int kbase = -radius - 1;
     const int naxis = 2 * radius + 3;
 
-    // 1. per-axis tables
+    // 1. per-axis tables (describe.cpp:48-52, 72-73, 89-99 per-axis factors)
     for (int i = tid; i < naxis; i += kDescThreads) {
         const int k = kbase + i;
         const double q = D_DIV((double)k, bw);
@@ -139,17 +142,42 @@ __device__ void raw_descriptor_cta(const DescArgs& a, const DescSmem& S, const D
     }
     const int width = kmax - kmin + 1;       // points per lattice row
     const int swidth = width + 2;            // samples per row (guard ring)
-    // bin owned by this thread: (row, col, ori)
+    const int nw = (width + 31) >> 5;        // 32-point mask words per row
+    const int pw = nw << 5;
+    // bin owned by this thread: (row, col, ori) = describe.cpp:116 bin layout
     const int brow = tid >> 5, bcol = (tid >> 3) & 3, bori = tid & 7;
-    // u / v ranges of this bin's 2x2-cell rectangle: c0 in {b-1, b}
     int ua = 1 << 30, ub = -(1 << 30), va = 1 << 30, vb = -(1 << 30);
     for (int k = kmin; k <= kmax; ++k) {
         const int c = S.c0[k - kbase];
         if (c == bcol - 1 || c == bcol) { ua = min(ua, k); ub = max(ub, k); }
         if (c == brow - 1 || c == brow) { va = min(va, k); vb = max(vb, k); }
     }
-    TreeCounter<kTreeDepth> tc;
-    tc.reset();
+    const int ca = ua - kmin, cb = ub - kmin;   // this bin's column span in the point rows
+    // Per-bin fixed tree (detsum.cpp:13-71) as a binary counter whose three
+    // lowest levels are folded 8 leaves at a time: leaves land in a shared
+    // ring; every complete aligned 8-leaf block is reduced with the reference's
+    // pairing ((l0+l1)+(l2+l3))+((l4+l5)+(l6+l7)) and pushed as one node into
+    // a shared-memory counter over 8-blocks.  Same tree, no per-leaf branching.
+    float* ring = S.ring + tid;
+    double* node = S.node + tid;
+    unsigned cnt = 0, flushed = 0;
+    auto flush = [&]() {
+        while (cnt - flushed >= 8u) {
+            double l[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) l[i] = (double)ring[((flushed + i) & (kRing - 1)) * kDescThreads];
+            double t = ((l[0] + l[1]) + (l[2] + l[3])) + ((l[4] + l[5]) + (l[6] + l[7]));
+            unsigned m = flushed >> 3;
+            int j = 0;
+            while (m & 1u) {
+                t = node[j * kDescThreads] + t;
+                m >>= 1;
+                ++j;
+            }
+            node[j * kDescThreads] = t;
+            flushed += 8;
+        }
+    };
 
     const int ch = a.chunk_rows;
     for (int v0 = kmin; v0 <= kmax; v0 += ch) {
@@ -157,7 +185,7 @@ __device__ void raw_descriptor_cta(const DescArgs& a, const DescSmem& S, const D
         const int nrows = v1 - v0 + 1;
         // 2a. samples on rows [v0-1, v1+1] x cols [kmin-1, kmax+1]
         for (int idx = tid; idx < (nrows + 2) * swidth; idx += kDescThreads) {
-            const int rr = idx / swidth, cc = idx % swidth;
+            const int rr = idx / swidth, cc = idx - rr * swidth;
             const int v = v0 - 1 + rr, u = kmin - 1 + cc;
             const double px = D_SUB(S.ax[u - kbase], S.sv[v - kbase]);
             const double py = D_ADD(S.cy_su[u - kbase], S.cv[v - kbase]);
@@ -167,67 +195,149 @@ __device__ void raw_descriptor_cta(const DescArgs& a, const DescSmem& S, const D
             S.samp[idx] = sv;
         }
         __syncthreads();
-        // 2b. per-point gradient, orientation, weight
-        for (int idx = tid; idx < nrows * width; idx += kDescThreads) {
-            const int rr = idx / width, cc = idx % width;
+        // 2b. per-point gradient, orientation, weight; a warp owns 32 aligned points
+        //     of one row and publishes 8 orientation-membership masks by ballot
+        for (int task = warp; task < nrows * nw; task += kDescThreads / 32) {
+            const int rr = task / nw, wd = task - rr * nw;
+            const int cc = (wd << 5) + lane;
             const int v = v0 + rr, u = kmin + cc;
-            const float* sr = S.samp + (rr + 1) * swidth + (cc + 1);
-            const float left = sr[-1], right = sr[1], up = sr[-swidth], down = sr[swidth];
-            unsigned char o0 = 0xff;
+            int o0 = 8;
             float value = 0.0f, fo = 0.0f;
-            if (!(left == kUndef || right == kUndef || up == kUndef || down == kUndef)) {
-                const float du = F_MUL(0.5f, F_SUB(right, left));
-                const float dv = F_MUL(0.5f, F_SUB(down, up));
-                const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
-                float theta = dsift_atan2f(dv, du);
-                if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
-                double obin = D_DIV((double)F_MUL(theta, (float)kDescOrients), kTwoPi);
-                if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
-                const double arg = D_DIV(-D_ADD(S.q2[u - kbase], S.q2[v - kbase]), 8.0);
-                const float wgt = (float)dsift_exp(arg);
-                value = F_MUL(mag, wgt);
-                const int o = (int)floor(obin);
-                fo = (float)D_SUB(obin, (double)o);
-                o0 = (unsigned char)o;
+            if (cc < width) {
+                const float* sr = S.samp + (rr + 1) * swidth + (cc + 1);
+                const float left = sr[-1], right = sr[1], up = sr[-swidth], down = sr[swidth];
+                if (!(left == kUndef || right == kUndef || up == kUndef || down == kUndef)) {
+                    const float du = F_MUL(0.5f, F_SUB(right, left));
+                    const float dv = F_MUL(0.5f, F_SUB(down, up));
+                    const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
+                    float theta = dsift_atan2f(dv, du);
+                    if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
+                    double obin = D_DIV((double)F_MUL(theta, (float)kDescOrients), kTwoPi);
+                    if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
+                    // -(uu^2 + vv^2) / 8: division by 8 is an exact scaling, == * 0.125
+                    const double arg = D_MUL(-D_ADD(S.q2[u - kbase], S.q2[v - kbase]), 0.125);
+                    const float wgt = (float)dsift_exp(arg);
+                    value = F_MUL(mag, wgt);
+                    o0 = (int)floor(obin);
+                    fo = (float)D_SUB(obin, (double)o0);
+                }
             }
-            S.pval[idx] = value;
-            S.pfo[idx] = fo;
-            S.po0[idx] = o0;
+            S.pval[rr * pw + cc] = value;
+            S.pfo[rr * pw + cc] = fo;
+#pragma unroll
+            for (int o = 0; o < kDescOrients; ++o) {
+                const unsigned m = __ballot_sync(0xffffffffu, o0 == o);
+                if (lane == o) S.omask[(rr * kDescOrients + o) * nw + wd] = m;
+            }
         }
         __syncthreads();
-        // 3. bin-owner accumulation in scan order (describe.cpp:102-126)
+        // 3. bin-owner accumulation in scan order (describe.cpp:102-126): only the
+        //    points whose o0 or o0+1 is this bin's orientation are visited.
         const int ra = max(va, v0), rb = min(vb, v1);
+        const int om1 = (bori + kDescOrients - 1) & (kDescOrients - 1);
         for (int v = ra; v <= rb; ++v) {
+            const int rr = v - v0;
             const int r0 = S.c0[v - kbase];
             const float fr = S.frac[v - kbase];
             const float wr = (brow - r0) ? fr : F_SUB(1.0f, fr);
-            const int rowoff = (v - v0) * width - kmin;
-            for (int u = ua; u <= ub; ++u) {
-                const int o0 = S.po0[rowoff + u];
-                if (o0 == 0xff) continue;
-                const int oi = (bori - o0) & (kDescOrients - 1);
-                if (oi > 1) continue;
-                const int c0 = S.c0[u - kbase];
-                const float fc = S.frac[u - kbase];
-                const float wc = (bcol - c0) ? fc : F_SUB(1.0f, fc);
-                const float fo = S.pfo[rowoff + u];
-                const float wo = oi ? fo : F_SUB(1.0f, fo);
-                const float val = F_MUL(F_MUL(F_MUL(S.pval[rowoff + u], wr), wc), wo);
-                tc.push((double)val);
+            const unsigned* mo = S.omask + (rr * kDescOrients + bori) * nw;
+            const unsigned* mp = S.omask + (rr * kDescOrients + om1) * nw;
+            for (int hw = (ca >> 4); hw <= (cb >> 4); ++hw) {   // 16-point half words
+                const int wd = hw >> 1;
+                const int lo = max(ca - (wd << 5), 0), hi = min(cb - (wd << 5), 31);
+                const unsigned range = (hi >= 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u) &
+                                       ((hw & 1) ? 0xffff0000u : 0x0000ffffu);
+                const unsigned a0 = mo[wd];
+                unsigned bits = (a0 | mp[wd]) & range;
+                while (bits) {
+                    const int bpos = __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    const int cc = (wd << 5) + bpos;
+                    const int u = kmin + cc;
+                    const int c0 = S.c0[u - kbase];
+                    const float fc = S.frac[u - kbase];
+                    const float wc = (bcol - c0) ? fc : F_SUB(1.0f, fc);
+                    const float fo = S.pfo[rr * pw + cc];
+                    const float wo = ((a0 >> bpos) & 1u) ? F_SUB(1.0f, fo) : fo;
+                    const float val = F_MUL(F_MUL(F_MUL(S.pval[rr * pw + cc], wr), wc), wo);
+                    ring[(cnt & (kRing - 1)) * kDescThreads] = val;
+                    ++cnt;
+                }
+                flush();
             }
         }
         __syncthreads();
     }
-    raw_out[tid] = (float)tc.result();
+    // fold the pending nodes smallest-first: the < 8 tail leaves (as their
+    // 4/2/1 aligned blocks), then the 8-block counter levels
+    {
+        const unsigned m = cnt - flushed;
+        double r = 0.0;
+        bool have = false;
+        unsigned p = flushed + (m & 4u) + (m & 2u);
+        if (m & 1u) {
+            r = (double)ring[(p & (kRing - 1)) * kDescThreads];
+            have = true;
+        }
+        if (m & 2u) {
+            p = flushed + (m & 4u);
+            const double v2 = (double)ring[(p & (kRing - 1)) * kDescThreads] +
+                              (double)ring[((p + 1) & (kRing - 1)) * kDescThreads];
+            r = have ? v2 + r : v2;
+            have = true;
+        }
+        if (m & 4u) {
+            double l[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) l[i] = (double)ring[((flushed + i) & (kRing - 1)) * kDescThreads];
+            const double v4 = (l[0] + l[1]) + (l[2] + l[3]);
+            r = have ? v4 + r : v4;
+            have = true;
+        }
+        unsigned hb = flushed >> 3;
+        for (int j = 0; hb; ++j, hb >>= 1)
+            if (hb & 1u) {
+                r = have ? node[j * kDescThreads] + r : node[j * kDescThreads];
+                have = true;
+            }
+        raw_out[tid] = (float)r;
+    }
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(kDescThreads)
-describe_kernel(const __grid_constant__ DescArgs a) {
+// DSP mean over scales, L2 -> clip -> L2 -> RootSIFT, float + uint8 outputs
+// (describe.cpp:138-173); one value per thread (bin = threadIdx.x).
+__device__ __forceinline__ void dsp_epilogue(const DescArgs& a, const float* raw, long long k, double* red) {
+    const int tid = threadIdx.x;
+    TreeCounter<5> tc;   // n_dsp <= kMaxDsp = 16 leaves
+    tc.reset();
+    for (int fi = 0; fi < a.n_dsp; ++fi) tc.push((double)raw[fi * kDescDim + tid]);
+    float d = F_DIV((float)tc.result(), (float)a.n_dsp);
+    float norm = F_SQRT((float)tree128((double)F_MUL(d, d), red));
+    if (norm != 0.0f) {
+        d = F_DIV(d, norm);
+        d = (a.clip < d) ? a.clip : d;
+        norm = F_SQRT((float)tree128((double)F_MUL(d, d), red));
+        if (norm > 0.0f) d = F_DIV(d, norm);
+        const float l1 = (float)tree128((double)d, red);
+        if (l1 != 0.0f) d = F_SQRT(F_DIV(d, l1));
+    }
+    a.desc[k * kDescDim + tid] = d;
+    if (a.desc_u8) {
+        long long q = llround((double)d * 255.0);
+        a.desc_u8[k * kDescDim + tid] = (unsigned char)(q > 255 ? 255 : (q < 0 ? 0 : q));
+    }
+}
+
+// Exact path: per-bin scan-order trees (bit-identical by construction).  Runs
+// over all keypoints in stage mode, and over the keypoints the fast path
+// could not certify in the hot path.
+__global__ void __launch_bounds__(kDescThreads, 4)
+describe_exact_kernel(const __grid_constant__ DescArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ double red[4];
-    __shared__ double trig[2];
     const int A = a.max_axis;
+    const int PW = ((A + 31) >> 5) << 5;
     DescSmem S;
     unsigned char* pbuf = sm;
     S.q2 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
@@ -240,22 +350,20 @@ describe_kernel(const __grid_constant__ DescArgs a) {
     S.c0 = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * A;
     S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * (a.raw_mode ? 1 : a.n_dsp);
     S.samp = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * (a.chunk_rows + 2) * A;
-    S.pval = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * A;
-    S.pfo = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * A;
-    S.po0 = pbuf;
+    S.pval = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * PW;
+    S.pfo = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * PW;
+    S.omask = reinterpret_cast<unsigned*>(pbuf); pbuf += sizeof(unsigned) * a.chunk_rows * kDescOrients * (PW >> 5);
+    pbuf = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(pbuf) + 15) & ~size_t(15));
+    S.node = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * (kTreeDepth - 3) * kDescThreads;
+    S.ring = reinterpret_cast<float*>(pbuf);
 
-    const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
+    const long long n = a.slow_list ? (long long)*a.n_slow : (a.n_host >= 0 ? a.n_host : (long long)*a.n_dev);
     const int tid = threadIdx.x;
-    for (long long k = blockIdx.x; k < n; k += gridDim.x) {
+    for (long long i = blockIdx.x; i < n; i += gridDim.x) {
+        const long long k = a.slow_list ? (long long)a.slow_list[i] : i;
         const DevKeypoint kp = a.kps[k];
-        if (tid == 0) {
-            double sn, cs;
-            dsift_sincos((double)kp.angle, &sn, &cs);
-            trig[0] = cs;
-            trig[1] = sn;
-        }
-        __syncthreads();
-        const double cosa = trig[0], sina = trig[1];
+        const double2 cs = a.trig[k];   // (cos, sin) of the keypoint angle (trig_kernel)
+        const double cosa = cs.x, sina = cs.y;
         if (a.raw_mode) {
             raw_descriptor_cta(a, S, kp, a.raw_scale, cosa, sina, S.raw);
             a.desc[k * kDescDim + tid] = S.raw[tid];
@@ -264,48 +372,355 @@ describe_kernel(const __grid_constant__ DescArgs a) {
         }
         for (int fi = 0; fi < a.n_dsp; ++fi)
             raw_descriptor_cta(a, S, kp, a.dsp[fi], cosa, sina, S.raw + fi * kDescDim);
-        // DSP mean: tree over scales / (float)n (describe.cpp:153-162)
-        TreeCounter<kTreeDepth> tc;
-        tc.reset();
-        for (int fi = 0; fi < a.n_dsp; ++fi) tc.push((double)S.raw[fi * kDescDim + tid]);
-        float d = F_DIV((float)tc.result(), (float)a.n_dsp);
-        // L2 -> clip -> L2 -> RootSIFT (describe.cpp:138-173)
-        float norm = F_SQRT((float)tree128((double)F_MUL(d, d), red));
-        if (norm != 0.0f) {
-            d = F_DIV(d, norm);
-            d = (a.clip < d) ? a.clip : d;
-            norm = F_SQRT((float)tree128((double)F_MUL(d, d), red));
-            if (norm > 0.0f) d = F_DIV(d, norm);
-            const float l1 = (float)tree128((double)d, red);
-            if (l1 != 0.0f) d = F_SQRT(F_DIV(d, l1));
+        dsp_epilogue(a, S.raw, k, red);
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------------------
+// Fast path: order-free FP64 accumulation + per-bin rounding certificate.
+//
+// Every histogram bin of describe.cpp:126 is the reference's pairwise tree
+// over float leaves (detsum.cpp:19-31).  For nonnegative leaves that tree is
+// within D*u*S of the exact sum S (D = depth <= 13, u = 2^-53), and any FP64
+// summation whose terms nest at most K deep is within K*u*S of S.  The fast
+// path sums each bin's leaves in a balanced, point-parallel order; if the
+// interval [S(1-e), S(1+e)] with e = (K+D+slack)*u rounds to a single float,
+// that float IS the reference's bit pattern (rounding is monotone).  Bins that
+// fail the test (probability ~1e-7 each) send their keypoint to the exact
+// kernel above, so the output is bit-identical either way.
+// ------------------------------------------------------------------------------
+struct FastSmem {
+    double* q2;
+    double* bin;
+    double* ax;
+    double* cy_su;
+    double* sv;
+    double* cv;
+    float* frac;
+    int* c0;
+    float* samp;    // [(chunk+2)][A]
+    float* pval;    // [chunk][A]
+    float* pfo;     // [chunk][A]
+    unsigned char* po0;
+    double* acc;    // [8][128] item-private partial sums
+    int* lsb;       // [8][128] item-private min exponent of any leaf's lowest bit
+    float* raw;     // [n_dsp][128]
+    int* misc;      // band / column-range scratch
+};
+
+// exponent of the least significant mantissa bit of a nonzero float
+__device__ __forceinline__ int float_lsb_exp(float x) {
+    const int e = (int)((__float_as_uint(x) >> 23) & 0xffu);
+    return e == 0 ? -149 : e - 150;
+}
+
+__device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const FastSmem& S, const DevKeypoint& kp,
+                                                    double f, double cosa, double sina, float* raw_out) {
+    const PyramidDesc& p = a.pyr;
+    const OctaveDesc& od = p.oct[kp.octave];
+    const double to_input = ldexp(1.0, kp.octave) * (p.upsampled ? 0.5 : 1.0);
+    const double cx = kp.x / to_input, cy = kp.y / to_input;
+    const double sigma_rel = kp.sigma / to_input;
+    const int lvl = nearest_level_d(p, f * sigma_rel);
+    const float* __restrict__ img =
+        od.gauss + (long long)kp.image * p.gauss_img_stride(kp.octave) + (long long)lvl * od.level_stride;
+    const int w = od.w, h = od.h, pitch = od.pitch;
+    const double bw = 3.0 * f * sigma_rel;
+    const int radius = (int)llround(bw * (kDescCells + 1) * 0.5 * 1.4142135623730951);
+    const int tid = threadIdx.x;
+    if (2 * radius + 3 > a.max_axis) {
+        if (tid == 0) atomicOr(a.err, kErrDescriptorLattice);
+        raw_out[tid] = 0.0f;
+        __syncthreads();
+        return true;
+    }
+    const int kbase = -radius - 1;
+    const int naxis = 2 * radius + 3;
+    for (int i = tid; i < naxis; i += kDescThreads) {
+        const int k = kbase + i;
+        const double q = D_DIV((double)k, bw);
+        const double bn = D_ADD(q, (double)(kDescCells / 2 - 0.5));
+        const int c = (int)floor(bn);
+        S.q2[i] = D_MUL(q, q);
+        S.bin[i] = bn;
+        S.c0[i] = c;
+        S.frac[i] = (float)D_SUB(bn, (double)c);
+        S.ax[i] = D_ADD(cx, D_MUL(cosa, (double)k));
+        S.cy_su[i] = D_ADD(cy, D_MUL(sina, (double)k));
+        S.sv[i] = D_MUL(sina, (double)k);
+        S.cv[i] = D_MUL(cosa, (double)k);
+    }
+    __syncthreads();
+    // misc[0..1] = kmin, kmax; misc[2+2c], misc[3+2c] = column span of cell col c;
+    // misc[10+2R'], misc[11+2R'] = row span of band R = R'-1
+    if (tid < 16) S.misc[tid] = (tid & 1) ? -(1 << 30) : (1 << 30);
+    __syncthreads();
+    if (tid < 32) {
+        for (int i = 1 + tid; i < naxis - 1; i += 32) {
+            const double bn = S.bin[i];
+            if (bn > -1.0 && bn < (double)kDescCells) {
+                const int k = kbase + i, c = S.c0[i];
+                atomicMin(&S.misc[0], k);
+                atomicMax(&S.misc[1], k);
+                for (int cc = 0; cc < kDescCells; ++cc)
+                    if (c == cc - 1 || c == cc) {
+                        atomicMin(&S.misc[2 + 2 * cc], k);
+                        atomicMax(&S.misc[3 + 2 * cc], k);
+                    }
+            }
         }
-        a.desc[k * kDescDim + tid] = d;
-        if (a.desc_u8) {
-            long long q = llround((double)d * 255.0);
-            a.desc_u8[k * kDescDim + tid] = (unsigned char)(q > 255 ? 255 : (q < 0 ? 0 : q));
+    }
+    __syncthreads();
+    const int kmin = S.misc[0], kmax = S.misc[1];
+    const int width = kmax - kmin + 1;
+    const int swidth = width + 2;
+    const int A = a.max_axis;
+    const int brow = tid >> 5, bcol = (tid >> 3) & 3, bori = tid & 7;
+    double binacc = 0.0;
+    int binlsb = 1 << 20;   // min lowest-bit exponent over this bin's nonzero leaves
+    int kterms = 0;   // max sequential terms in any partial sum this thread formed
+
+    // bands: rows whose vbin floor is R (R = -1..3) feed histogram rows R and R+1
+    int v = kmin;
+    for (int R = -1; R < kDescCells && v <= kmax; ++R) {
+        const int vb0 = v;
+        while (v <= kmax && S.c0[v - kbase] == R) ++v;
+        const int vb1 = v - 1;
+        if (vb1 < vb0) continue;
+        const int tr_first = R < 0 ? 0 : R;
+        const int ntr = (R < 0 || R + 1 >= kDescCells) ? 1 : 2;
+        const int npairs = ntr * kDescCells;
+        const int nsl = kDescThreads / npairs;      // slices per (row, col) pair
+        const int pair = tid / nsl, slice = tid - pair * nsl;
+        const int tr = tr_first + (pair >> 2), tc = pair & 3;
+        const int uc0 = S.misc[2 + 2 * tc], uc1 = S.misc[3 + 2 * tc];
+        const int ucount = uc1 - uc0 + 1;
+        const bool upper = (tr != R);               // ri = 1 -> wr = fr
+#pragma unroll
+        for (int o = 0; o < kDescOrients; ++o) {
+            S.acc[o * kDescThreads + tid] = 0.0;
+            S.lsb[o * kDescThreads + tid] = 1 << 20;
         }
+        int myterms = 0;
+        for (int v0 = vb0; v0 <= vb1; v0 += a.chunk_rows) {
+            const int v1 = min(v0 + a.chunk_rows - 1, vb1);
+            const int nrows = v1 - v0 + 1;
+            __syncthreads();
+            for (int idx = tid; idx < (nrows + 2) * swidth; idx += kDescThreads) {
+                const int rr = idx / swidth, cc = idx - rr * swidth;
+                const int vv = v0 - 1 + rr, u = kmin - 1 + cc;
+                const double px = D_SUB(S.ax[u - kbase], S.sv[vv - kbase]);
+                const double py = D_ADD(S.cy_su[u - kbase], S.cv[vv - kbase]);
+                float sv = kUndef;
+                if (!(px < 0.0 || px > (double)(w - 1) || py < 0.0 || py > (double)(h - 1)))
+                    sv = sample_bilinear(img, w, h, pitch, px, py);
+                S.samp[idx] = sv;
+            }
+            __syncthreads();
+            for (int idx = tid; idx < nrows * width; idx += kDescThreads) {
+                const int rr = idx / width, cc = idx - rr * width;
+                const int vv = v0 + rr, u = kmin + cc;
+                const float* sr = S.samp + (rr + 1) * swidth + (cc + 1);
+                const float left = sr[-1], right = sr[1], up = sr[-swidth], down = sr[swidth];
+                unsigned char o0 = 0xff;
+                float value = 0.0f, fo = 0.0f;
+                if (!(left == kUndef || right == kUndef || up == kUndef || down == kUndef)) {
+                    const float du = F_MUL(0.5f, F_SUB(right, left));
+                    const float dv = F_MUL(0.5f, F_SUB(down, up));
+                    const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
+                    float theta = dsift_atan2f(dv, du);
+                    if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
+                    double obin = D_DIV((double)F_MUL(theta, (float)kDescOrients), kTwoPi);
+                    if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
+                    const double arg = D_MUL(-D_ADD(S.q2[u - kbase], S.q2[vv - kbase]), 0.125);
+                    const float wgt = (float)dsift_exp(arg);
+                    value = F_MUL(mag, wgt);
+                    const int o = (int)floor(obin);
+                    fo = (float)D_SUB(obin, (double)o);
+                    o0 = (unsigned char)o;
+                }
+                S.pval[rr * A + cc] = value;
+                S.pfo[rr * A + cc] = fo;
+                S.po0[rr * A + cc] = o0;
+            }
+            __syncthreads();
+            // balanced accumulation: item (pair, slice) takes every nsl-th point
+            // of the pair's rows x [uc0, uc1] block; two leaves per point
+            const int tot = nrows * ucount;
+            int rr = slice / ucount, cu = slice - rr * ucount;
+            for (int i = slice; i < tot; i += nsl) {
+                const int cc = uc0 - kmin + cu;
+                const unsigned char o0 = S.po0[rr * A + cc];
+                if (o0 != 0xff) {
+                    const int vv = v0 + rr, u = uc0 + cu;
+                    const float fr = S.frac[vv - kbase], fc = S.frac[u - kbase];
+                    const float wr = upper ? fr : F_SUB(1.0f, fr);
+                    const float wc = (tc - S.c0[u - kbase]) ? fc : F_SUB(1.0f, fc);
+                    const float fo = S.pfo[rr * A + cc];
+                    const float t = F_MUL(F_MUL(S.pval[rr * A + cc], wr), wc);
+                    const float l0 = F_MUL(t, F_SUB(1.0f, fo));   // orientation o0
+                    const float l1 = F_MUL(t, fo);                // orientation o0 + 1
+                    const int i0 = o0 * kDescThreads + tid;
+                    const int i1 = ((o0 + 1) & (kDescOrients - 1)) * kDescThreads + tid;
+                    S.acc[i0] = S.acc[i0] + (double)l0;
+                    S.acc[i1] = S.acc[i1] + (double)l1;
+                    if (l0 != 0.0f) S.lsb[i0] = min(S.lsb[i0], float_lsb_exp(l0));
+                    if (l1 != 0.0f) S.lsb[i1] = min(S.lsb[i1], float_lsb_exp(l1));
+                    ++myterms;
+                }
+                cu += nsl;
+                while (cu >= ucount) {
+                    cu -= ucount;
+                    ++rr;
+                }
+            }
+        }
+        kterms = max(kterms, myterms);
+        __syncthreads();
+        // fold this band's slices into the bins of rows R, R+1 (fixed order)
+        if (brow >= tr_first && brow < tr_first + ntr) {
+            const int bp = ((brow - tr_first) << 2) + bcol;
+            double sacc = 0.0;
+            for (int sl = 0; sl < nsl; ++sl) {
+                sacc = sacc + S.acc[bori * kDescThreads + bp * nsl + sl];
+                binlsb = min(binlsb, S.lsb[bori * kDescThreads + bp * nsl + sl]);
+            }
+            binacc = binacc + sacc;
+        }
+        __syncthreads();   // the next band re-zeroes S.acc
+    }
+    // certificate: |tree - S| <= 13u S,  |binacc - S| <= (K + 32 + 2) u S
+    const int kmaxterms = __reduce_max_sync(0xffffffffu, kterms);
+    if ((tid & 31) == 0) S.misc[16 + (tid >> 5)] = kmaxterms;
+    __syncthreads();
+    const int K = max(max(S.misc[16], S.misc[17]), max(S.misc[18], S.misc[19]));
+    // (a) exact case: if every leaf's lowest bit and the sum's top bit span at
+    //     most 53 bits, every partial sum in ANY order is exact, so the tree
+    //     and this sum are both the exact S;
+    // (b) otherwise the interval test above.
+    bool ok;
+    float res;
+    const int top = (int)((__double_as_longlong(binacc) >> 52) & 0x7ff) - 1023;
+    if (binacc == 0.0 || top - binlsb <= 52) {
+        ok = true;
+        res = __double2float_rn(binacc);
+    } else {
+        const double e = (double)(K + 64 + 16) * 0x1p-53;
+        const double lo = binacc * (1.0 - e), hi = binacc * (1.0 + e);
+        const float flo = __double2float_rn(lo), fhi = __double2float_rn(hi);
+        ok = (flo == fhi);
+        res = flo;
+    }
+    ok = ok && !a.force_slow;
+    raw_out[tid] = res;
+    __syncthreads();
+    return ok;
+}
+
+__global__ void __launch_bounds__(kDescThreads, 5)
+describe_fast_kernel(const __grid_constant__ DescArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ double red[4];
+    __shared__ int misc[24];
+    const int A = a.max_axis;
+    FastSmem S;
+    unsigned char* pbuf = sm;
+    S.q2 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
+    S.bin = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
+    S.ax = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
+    S.cy_su = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
+    S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
+    S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
+    S.acc = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * kDescOrients * kDescThreads;
+    S.lsb = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * kDescOrients * kDescThreads;
+    S.frac = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * A;
+    S.c0 = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * A;
+    S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * a.n_dsp;
+    S.samp = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * (a.chunk_rows + 2) * A;
+    S.pval = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * A;
+    S.pfo = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * A;
+    S.po0 = pbuf;
+    S.misc = misc;
+
+    const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
+    const int tid = threadIdx.x;
+    for (long long k = blockIdx.x; k < n; k += gridDim.x) {
+        const DevKeypoint kp = a.kps[k];
+        const double2 cs = a.trig[k];
+        bool ok = true;
+        for (int fi = 0; fi < a.n_dsp; ++fi)
+            ok &= raw_descriptor_fast(a, S, kp, a.dsp[fi], cs.x, cs.y, S.raw + fi * kDescDim);
+        const bool all_ok = __syncthreads_and(ok);
+        if (!all_ok) {
+            if (tid == 0) {
+                const unsigned slot = atomicAdd(a.slow_count, 1u);
+                if ((long long)slot < a.slow_cap) a.slow_out[slot] = (int)k;
+                else atomicOr(a.err, kErrDescriptorLattice);
+            }
+            continue;   // the exact kernel writes this keypoint's descriptor
+        }
+        dsp_epilogue(a, S.raw, k, red);
         __syncthreads();
     }
 }
 
 size_t describe_smem_bytes(int max_axis, int chunk_rows, int n_dsp) {
     const size_t A = (size_t)max_axis;
+    const size_t PW = ((A + 31) / 32) * 32, NW = PW / 32;
     return sizeof(double) * 6 * A + sizeof(float) * A + sizeof(int) * A + sizeof(float) * kDescDim * n_dsp +
-           sizeof(float) * (chunk_rows + 2) * A + sizeof(float) * 2 * chunk_rows * A + chunk_rows * A + 16;
+           sizeof(float) * (chunk_rows + 2) * A + sizeof(float) * 2 * chunk_rows * PW +
+           sizeof(unsigned) * chunk_rows * kDescOrients * NW + 16 + sizeof(double) * (kTreeDepth - 3) * kDescThreads +
+           sizeof(float) * kRing * kDescThreads;
+}
+
+// cos/sin of every keypoint angle (describe.cpp:51-52), once per keypoint.
+__global__ void trig_kernel(const DevKeypoint* __restrict__ kps, const unsigned long long* n_dev, long long n_host,
+                            double2* __restrict__ trig) {
+    const long long n = n_host >= 0 ? n_host : (long long)*n_dev;
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n; k += (long long)gridDim.x * blockDim.x) {
+        double sn, cs;
+        dsift_sincos((double)kps[k].angle, &sn, &cs);
+        trig[k] = make_double2(cs, sn);
+    }
+}
+
+cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev, long long n_host, double2* trig,
+                        long long cap, cudaStream_t st) {
+    const long long n = n_host >= 0 ? n_host : cap;
+    const int grid = (int)std::max<long long>(1, std::min<long long>((n + 255) / 256, 148 * 8));
+    trig_kernel<<<grid, 256, 0, st>>>(kps, n_dev, n_host, trig);
+    return cudaGetLastError();
+}
+
+size_t describe_fast_smem_bytes(int max_axis, int chunk_rows, int n_dsp) {
+    const size_t A = (size_t)max_axis;
+    return sizeof(double) * 6 * A + sizeof(double) * kDescOrients * kDescThreads +
+           sizeof(int) * kDescOrients * kDescThreads + sizeof(float) * A +
+           sizeof(int) * A + sizeof(float) * kDescDim * n_dsp + sizeof(float) * (chunk_rows + 2) * A +
+           sizeof(float) * 2 * chunk_rows * A + chunk_rows * A + 16;
 }
 
 int describe_blocks_per_sm(size_t smem) {
-    cudaFuncSetAttribute(describe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(describe_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, describe_kernel, kDescThreads, smem) != cudaSuccess) n = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, describe_fast_kernel, kDescThreads, smem) != cudaSuccess) n = 1;
     return n;
 }
 
 cudaError_t launch_describe(const DescArgs& a, int grid, cudaStream_t st) {
     const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, a.raw_mode ? 1 : a.n_dsp);
-    cudaError_t e = cudaFuncSetAttribute(describe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(describe_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    describe_kernel<<<grid, kDescThreads, smem, st>>>(a);
+    describe_exact_kernel<<<grid, kDescThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_describe_fast(const DescArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = describe_fast_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
+    cudaError_t e = cudaFuncSetAttribute(describe_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    describe_fast_kernel<<<grid, kDescThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -80,6 +80,12 @@ def main():
               f"kps bitwise={fs.keypoints.tobytes() == kr.tobytes()} "
               f"desc bitwise={fs.descriptors.tobytes() == dr.tobytes()} "
               f"sha gpu={ex.sha256(0)[:16]} ref={ref.hash_features(kr, dr)[:16]}", flush=True)
+        print(f"    exact fallbacks: {ex.exact_fallbacks()}", flush=True)
+        ex.set_force_exact(True)
+        fs2 = ex.extract(img)
+        ex.set_force_exact(False)
+        print(f"    forced-exact path identical: {fs2.descriptors.tobytes() == fs.descriptors.tobytes()} "
+              f"(fallbacks {ex.exact_fallbacks()})", flush=True)
         if len(fs) == len(kr) and len(kr):
             q = ds.quantize_u8(dr)
             print(f"    u8 mismatch {int((fs.descriptors_u8 != q).sum())} desc float mism "
