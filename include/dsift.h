@@ -33,7 +33,8 @@ enum {
     DSIFT_ECAPACITY = 2, /* a device work list overflowed; nothing truncated  */
     DSIFT_ECUDA = 3,     /* CUDA runtime error / no device / extension absent */
     DSIFT_ENOMEM = 4,    /* device or host allocation failed                  */
-    DSIFT_ESTATE = 5     /* call order violated (e.g. no result yet)          */
+    DSIFT_ESTATE = 5,    /* call order violated (e.g. no result yet)          */
+    DSIFT_ERANGE = 6     /* std::out_of_range in the reference (NaN input)   */
 };
 
 /* detsift::SiftConfig (core.hpp:30-47).  dsp_scales is borrowed by the call. */
@@ -165,6 +166,11 @@ int dsift_set_option(dsift_ctx* ctx, int key, int64_t value);
  * of keypoints whose descriptor the fast path could not certify. */
 #define DSIFT_STAT_EXACT_FALLBACKS 1
 int64_t dsift_stat(dsift_ctx* ctx, int key);
+/* Test probe: evaluates the device restatements of the host libm calls on
+ * the path (dsift_math.cuh) over n inputs.  mode 0: atan2f, in = n x {y, x}
+ * float32 pairs, out = n float32; mode 1: exp, in/out = n float64; mode 2:
+ * sin/cos, in = n float64, out = n x {sin, cos} float64. */
+int dsift_libm_probe(dsift_ctx* ctx, int mode, const void* in, int64_t n, void* out);
 int dsift_stage_times(dsift_ctx* ctx, float* ms5);
 
 #ifdef __cplusplus

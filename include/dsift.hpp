@@ -1,0 +1,171 @@
+// include/dsift.hpp — header-only C++ face of the C ABI, mirroring the
+// reference's extraction API so existing C++ callers swap one include:
+//
+//   reference:  detsift::FeatureSet detsift::extract(const GrayImage&, const SiftConfig&, int workers)
+//               (/root/reference/proj/include/detsift/io.hpp:17-19)
+//   here:       dsift::FeatureSet  dsift::extract(const GrayImage&, const SiftConfig&, int device)
+//
+// The types restate detsift's (core.hpp:11-78) field for field; Keypoint is
+// layout-identical to the reference struct and to dsift_keypoint.  Errors
+// surface as the same exception types the reference throws:
+// std::invalid_argument for DSIFT_EINVAL, std::runtime_error otherwise.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "dsift.h"
+
+namespace dsift {
+
+struct GrayImage {   // core.hpp:11-26
+    int width = 0;
+    int height = 0;
+    std::vector<float> data;
+    GrayImage() = default;
+    GrayImage(int w, int h, float fill = 0.0f) : width(w), height(h), data(size_t(w) * h, fill) {}
+    float& at(int x, int y) { return data[size_t(y) * width + x]; }
+    float at(int x, int y) const { return data[size_t(y) * width + x]; }
+    size_t size() const { return data.size(); }
+    bool empty() const { return width <= 0 || height <= 0; }
+};
+
+struct SiftConfig {   // core.hpp:30-47
+    float sigma0 = 1.6f;
+    int intervals_per_octave = 3;
+    float assumed_input_blur = 0.5f;
+    float contrast_threshold = 0.04f;
+    float edge_ratio = 10.0f;
+    int max_refine_iters = 5;
+    int64_t upsample_pixel_limit = 4'000'000;
+    std::vector<double> dsp_scales = {0.5, 1.0 / 1.4142135623730951, 1.0, 1.4142135623730951, 2.0};
+    float descriptor_clip = 0.2f;
+    int orientation_bins = 36;
+    float orientation_peak_ratio = 0.8f;
+    int num_octaves = 0;
+
+    dsift_config to_c() const {
+        dsift_config c;
+        c.sigma0 = sigma0;
+        c.intervals = intervals_per_octave;
+        c.assumed_blur = assumed_input_blur;
+        c.contrast_threshold = contrast_threshold;
+        c.edge_ratio = edge_ratio;
+        c.max_refine_iters = max_refine_iters;
+        c.upsample_pixel_limit = upsample_pixel_limit;
+        c.dsp_scales = dsp_scales.data();
+        c.n_dsp_scales = int32_t(dsp_scales.size());
+        c.descriptor_clip = descriptor_clip;
+        c.orientation_bins = orientation_bins;
+        c.orientation_peak_ratio = orientation_peak_ratio;
+        c.num_octaves = num_octaves;
+        return c;
+    }
+    void validate() const;   // SiftConfig::validate (core.cpp:17-46)
+};
+
+struct Keypoint {   // core.hpp:55-63
+    float x = 0.0f, y = 0.0f, sigma = 0.0f, angle = 0.0f, response = 0.0f;
+    int32_t octave = 0, interval = 0;
+};
+static_assert(sizeof(Keypoint) == sizeof(dsift_keypoint), "Keypoint must stay layout-identical");
+static_assert(sizeof(Keypoint) == 28, "detsift::Keypoint is 7 x 4 bytes");
+
+struct FeatureSet {   // core.hpp:66-78
+    std::vector<Keypoint> keypoints;
+    std::vector<float> descriptors;
+    std::vector<uint8_t> descriptors_u8;   // q(v) = min(255, lround(v * 255))
+    int dim = 128;
+    size_t size() const { return keypoints.size(); }
+    std::span<const float> row(size_t i) const { return {descriptors.data() + i * dim, size_t(dim)}; }
+};
+
+[[noreturn]] inline void throw_status(int rc) {
+    const std::string msg = dsift_last_error();
+    if (rc == DSIFT_EINVAL) throw std::invalid_argument(msg);
+    if (rc == DSIFT_ERANGE) throw std::out_of_range(msg);
+    throw std::runtime_error(std::string(dsift_strerror(rc)) + ": " + msg);
+}
+inline void check(int rc) {
+    if (rc != DSIFT_OK) throw_status(rc);
+}
+
+inline void SiftConfig::validate() const {
+    const dsift_config c = to_c();
+    check(dsift_config_validate(&c));
+}
+
+// RAII context: one device, one stream, reusable across many images.
+class Extractor {
+   public:
+    explicit Extractor(const SiftConfig& cfg = {}, int device = 0) : cfg_(cfg) {
+        const dsift_config c = cfg_.to_c();
+        dsift_ctx* ctx = nullptr;
+        check(dsift_create(device, &c, &ctx));
+        ctx_.reset(ctx);
+    }
+    // detsift::extract (io.cpp:111-142) for one image.
+    FeatureSet extract(const GrayImage& img) {
+        return std::move(extract_batch(&img, 1)[0]);
+    }
+    // Same-size images in one batch (one pipeline pass over the batch).
+    std::vector<FeatureSet> extract_batch(const GrayImage* imgs, int n) {
+        if (n <= 0) return {};
+        const int w = imgs[0].width, h = imgs[0].height;
+        std::vector<float> packed;
+        const float* src = imgs[0].data.data();
+        if (n > 1) {
+            packed.resize(size_t(n) * w * h);
+            for (int i = 0; i < n; ++i) {
+                if (imgs[i].width != w || imgs[i].height != h)
+                    throw std::invalid_argument("extract_batch: images must share one size");
+                std::copy(imgs[i].data.begin(), imgs[i].data.end(), packed.begin() + size_t(i) * w * h);
+            }
+            src = packed.data();
+        }
+        check(dsift_extract_batch(ctx_.get(), src, n, w, h, DSIFT_INPUT_HOST));
+        int64_t total = 0;
+        check(dsift_result_sync(ctx_.get(), &total));
+        std::vector<Keypoint> kps(static_cast<size_t>(total));
+        std::vector<float> desc(static_cast<size_t>(total) * 128);
+        std::vector<uint8_t> desc8(static_cast<size_t>(total) * 128);
+        std::vector<int64_t> offs(static_cast<size_t>(n) + 1);
+        check(dsift_result_copy(ctx_.get(), reinterpret_cast<dsift_keypoint*>(kps.data()), desc.data(),
+                                desc8.data(), offs.data()));
+        std::vector<FeatureSet> out(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) {
+            const size_t b = size_t(offs[i]), e = size_t(offs[i + 1]);
+            out[i].keypoints.assign(kps.begin() + b, kps.begin() + e);
+            out[i].descriptors.assign(desc.begin() + b * 128, desc.begin() + e * 128);
+            out[i].descriptors_u8.assign(desc8.begin() + b * 128, desc8.begin() + e * 128);
+        }
+        return out;
+    }
+    std::string sha256(int image = 0) {
+        char hex[65];
+        check(dsift_result_sha256(ctx_.get(), image, hex));
+        return hex;
+    }
+    dsift_ctx* handle() { return ctx_.get(); }
+
+   private:
+    struct Deleter {
+        void operator()(dsift_ctx* c) const { dsift_destroy(c); }
+    };
+    SiftConfig cfg_;
+    std::unique_ptr<dsift_ctx, Deleter> ctx_;
+};
+
+// Drop-in for detsift::extract; `device` replaces `workers` (output is
+// bit-identical to the reference for any device, as the reference's is for
+// any worker count).
+inline FeatureSet extract(const GrayImage& img, const SiftConfig& cfg = {}, int device = 0) {
+    Extractor ex(cfg, device);
+    return ex.extract(img);
+}
+
+}  // namespace dsift

@@ -30,7 +30,7 @@ KEYPOINT_DTYPE = np.dtype(
      ("response", "<f4"), ("octave", "<i4"), ("interval", "<i4")])
 DESC_DIM = 128
 
-DSIFT_OK, DSIFT_EINVAL, DSIFT_ECAPACITY, DSIFT_ECUDA, DSIFT_ENOMEM, DSIFT_ESTATE = range(6)
+DSIFT_OK, DSIFT_EINVAL, DSIFT_ECAPACITY, DSIFT_ECUDA, DSIFT_ENOMEM, DSIFT_ESTATE, DSIFT_ERANGE = range(7)
 INPUT_HOST, INPUT_DEVICE = 0, 1
 
 
@@ -42,6 +42,10 @@ class DsiftError(RuntimeError):
 
 class InvalidArgument(DsiftError, ValueError):
     """std::invalid_argument in the reference."""
+
+
+class OutOfRange(DsiftError, IndexError):
+    """std::out_of_range in the reference (detsum.cpp:138-141)."""
 
 
 class _Config(C.Structure):
@@ -149,6 +153,7 @@ def load_library():
         "dsift_kernel_launches": ([vp], C.c_int64),
         "dsift_set_profiling": ([vp, i32], C.c_int), "dsift_stage_times": ([vp, vp], C.c_int),
         "dsift_set_option": ([vp, i32, i64], C.c_int), "dsift_stat": ([vp, i32], C.c_int64),
+        "dsift_libm_probe": ([vp, i32, vp, i64, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -163,6 +168,8 @@ def _check(lib, rc: int) -> None:
         msg = lib.dsift_last_error().decode()
         if rc == DSIFT_EINVAL:
             raise InvalidArgument(rc, msg)
+        if rc == DSIFT_ERANGE:
+            raise OutOfRange(rc, msg)
         raise DsiftError(rc, f"{lib.dsift_strerror(rc).decode()}: {msg}")
 
 
@@ -276,6 +283,35 @@ class Extractor:
     def exact_fallbacks(self) -> int:
         """Keypoints of the last result whose fast-path certificate failed."""
         return int(self.lib.dsift_stat(self.ctx, 1))
+
+    def libm_probe(self, mode: int, inputs: np.ndarray) -> np.ndarray:
+        """Device restatements of atan2f (mode 0, inputs [n, 2] float32 (y, x)),
+        exp (mode 1, float64) and sin/cos (mode 2, float64 -> [n, 2] (sin, cos))."""
+        if mode == 0:
+            a = np.ascontiguousarray(inputs, np.float32).reshape(-1, 2)
+            out = np.empty(len(a), np.float32)
+        elif mode == 1:
+            a = np.ascontiguousarray(inputs, np.float64).ravel()
+            out = np.empty(len(a), np.float64)
+        else:
+            a = np.ascontiguousarray(inputs, np.float64).ravel()
+            out = np.empty((len(a), 2), np.float64)
+        _check(self.lib, self.lib.dsift_libm_probe(self.ctx, mode, a.ctypes.data, len(a), out.ctypes.data))
+        return out
+
+    def export_torch(self, which: int = 1):
+        """Zero-copy DLPack export of the last result as a torch CUDA tensor
+        (0 keypoints [n, 7] float32 view, 1 descriptors [n, 128] float32,
+        2 descriptors [n, 128] uint8)."""
+        import torch
+
+        ptr = C.c_void_p()
+        _check(self.lib, self.lib.dsift_export_dlpack(self.ctx, which, C.byref(ptr)))
+        pyapi = C.pythonapi
+        pyapi.PyCapsule_New.restype = C.py_object
+        pyapi.PyCapsule_New.argtypes = [C.c_void_p, C.c_char_p, C.c_void_p]
+        cap = pyapi.PyCapsule_New(ptr, b"dltensor", None)
+        return torch.utils.dlpack.from_dlpack(cap)
 
     def kernel_launches(self) -> int:
         return int(self.lib.dsift_kernel_launches(self.ctx))

@@ -58,6 +58,7 @@ enum : unsigned {
     kErrOrientedCapacity = 2u,
     kErrCandidateCapacity = 4u,
     kErrDescriptorLattice = 8u,
+    kErrHistogramRange = 16u,   // NaN gradient -> out-of-range bin (detsum.cpp:138-141 throws)
 };
 
 // Decoupled look-back scan state (per ticket): bit 63..62 = status.
@@ -68,7 +69,8 @@ constexpr unsigned long long kLbValueMask = (1ull << 62) - 1;
 struct ScanState {
     unsigned long long* states;   // [n_tiles]
     unsigned int* ticket;         // dynamic tile ticket
-    unsigned long long* total;    // inclusive total (written by the last tile)
+    unsigned long long* total;    // inclusive total (written by the last tile), clamped to cap
+    unsigned long long cap;       // capacity of the compacted output
 };
 
 }  // namespace dsift

@@ -376,6 +376,7 @@ static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
     a.scan.states = c->det_states.as<unsigned long long>();
     a.scan.ticket = &ctr->det_ticket;
     a.scan.total = &ctr->n_det;
+    a.scan.cap = (unsigned long long)cap;
     if (raw_mode) {
         c->det_cand.ensure(sizeof(DevCandidate) * (size_t)cap);
         a.cand_out = c->det_cand.as<DevCandidate>();
@@ -410,6 +411,7 @@ static void run_detect_with_candidates(dsift_ctx* c, long long cap) {
     a.scan.states = c->det_states.as<unsigned long long>();
     a.scan.ticket = &ctr->det_ticket;
     a.scan.total = &ctr->n_det;
+    a.scan.cap = (unsigned long long)cap;
     cuda_check(launch_detect(a, c->stream), "detect");
     ++c->launches;
 }
@@ -453,6 +455,7 @@ static void run_orient(dsift_ctx* c, const DevKeypoint* kps, long long n_host, l
     a.scan.states = c->ori_states.as<unsigned long long>();
     a.scan.ticket = &ctr->ori_ticket;
     a.scan.total = &ctr->n_ori;
+    a.scan.cap = (unsigned long long)cap_out;
     cuda_check(launch_orient(a, c->stream), "orient");
     ++c->launches;
 }
@@ -615,6 +618,8 @@ static void result_sync(dsift_ctx* c) {
     Counters h{};
     cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(Counters), cudaMemcpyDeviceToHost), "D2H");
     c->result_pending = false;
+    if (h.err & kErrHistogramRange)   // same text as detsum.cpp:140 (std::out_of_range)
+        throw Error{DSIFT_ERANGE, "histogram: bin index out of range"};
     if (h.err) {
         std::string m = "device work list overflow:";
         if (h.err & kErrKeypointCapacity) m += " keypoints";
@@ -690,6 +695,7 @@ const char* dsift_strerror(int code) {
         case DSIFT_ECUDA: return "CUDA error";
         case DSIFT_ENOMEM: return "out of memory";
         case DSIFT_ESTATE: return "invalid call order";
+        case DSIFT_ERANGE: return "out of range";
         default: return "unknown error";
     }
 }
@@ -1126,6 +1132,7 @@ static void stage_describe(dsift_ctx* c, const dsift_keypoint* kps, int64_t n, f
     cuda_check(cudaStreamSynchronize(c->stream), "sync");
     Counters h{};
     cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+    if (h.err & kErrHistogramRange) throw Error{DSIFT_ERANGE, "histogram: bin index out of range"};
     if (h.err & kErrDescriptorLattice) throw Error{DSIFT_ECAPACITY, "descriptor lattice exceeds table capacity"};
     cuda_check(cudaMemcpy(out, d, sizeof(float) * kDescDim * (size_t)n, cudaMemcpyDeviceToHost), "D2H");
     if (out_u8 && !raw_mode)
@@ -1155,6 +1162,24 @@ int dsift_synth_value_noise(dsift_ctx* c, float* dev_out, int n, int w, int h, u
 }
 
 int64_t dsift_kernel_launches(dsift_ctx* c) { return c ? c->launches : 0; }
+
+int dsift_libm_probe(dsift_ctx* c, int mode, const void* in, int64_t n, void* out) {
+    return guard([&] {
+        if (!c || !in || !out) invalid("null argument");
+        if (mode < 0 || mode > 2) invalid("libm_probe: mode must be 0 (atan2f), 1 (exp) or 2 (sincos)");
+        set_device(c);
+        const size_t isz = mode == 0 ? 8 : 8, osz = mode == 0 ? 4 : (mode == 1 ? 8 : 16);
+        void *din = nullptr, *dout = nullptr;
+        cuda_check(cudaMalloc(&din, isz * (size_t)std::max<int64_t>(n, 1)), "cudaMalloc");
+        cuda_check(cudaMalloc(&dout, osz * (size_t)std::max<int64_t>(n, 1)), "cudaMalloc");
+        cuda_check(cudaMemcpy(din, in, isz * (size_t)n, cudaMemcpyHostToDevice), "H2D");
+        cuda_check(launch_libm_probe(mode, din, n, dout, c->stream), "probe");
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        cuda_check(cudaMemcpy(out, dout, osz * (size_t)n, cudaMemcpyDeviceToHost), "D2H");
+        cudaFree(din);
+        cudaFree(dout);
+    });
+}
 
 int dsift_set_option(dsift_ctx* c, int key, int64_t value) {
     return guard([&] {

@@ -100,6 +100,7 @@ cudaError_t launch_value_noise(float* out, int n, int w, int h, unsigned long lo
                                int cells, double* scratch, int nparts, cudaStream_t st);
 
 int describe_blocks_per_sm(size_t smem);
+cudaError_t launch_libm_probe(int mode, const void* in, long long n, void* out, cudaStream_t st);
 size_t describe_fast_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
 cudaError_t launch_describe_fast(const DescArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev, long long n_host, double2* trig,

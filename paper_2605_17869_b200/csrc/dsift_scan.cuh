@@ -51,7 +51,8 @@ __device__ __forceinline__ unsigned long long scan_exclusive(const ScanState& st
             }
             st_release_u64(&st.states[ticket], kLbPrefix | (excl + count));
         }
-        if (ticket == n_tiles - 1) *st.total = excl + count;
+        // downstream stages read this count: never let it exceed what was written
+        if (ticket == n_tiles - 1) *st.total = min(excl + count, st.cap);
         *slot = excl;
     }
     __syncthreads();

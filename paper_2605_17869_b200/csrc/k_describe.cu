@@ -212,6 +212,10 @@ __device__ __forceinline__ void raw_descriptor_cta(const DescArgs& a, const Desc
                     const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
                     float theta = dsift_atan2f(dv, du);
                     if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
+                    if (isnan(theta)) {   // reference: negative bin -> std::out_of_range
+                        atomicOr(a.err, kErrHistogramRange);
+                        theta = 0.0f;
+                    }
                     double obin = D_DIV((double)F_MUL(theta, (float)kDescOrients), kTwoPi);
                     if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
                     // -(uu^2 + vv^2) / 8: division by 8 is an exact scaling, == * 0.125
@@ -531,6 +535,10 @@ __device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const Fas
                     const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
                     float theta = dsift_atan2f(dv, du);
                     if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
+                    if (isnan(theta)) {   // reference: negative bin -> std::out_of_range
+                        atomicOr(a.err, kErrHistogramRange);
+                        theta = 0.0f;
+                    }
                     double obin = D_DIV((double)F_MUL(theta, (float)kDescOrients), kTwoPi);
                     if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
                     const double arg = D_MUL(-D_ADD(S.q2[u - kbase], S.q2[vv - kbase]), 0.125);

@@ -108,6 +108,10 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 const float mag = F_SQRT(F_ADD(F_MUL(gx, gx), F_MUL(gy, gy)));
                 float theta = dsift_atan2f(gy, gx);
                 if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
+                if (isnan(theta)) {   // the reference's int(NaN) bin is out of range -> it throws
+                    atomicOr(a.err, kErrHistogramRange);
+                    theta = 0.0f;
+                }
                 bin = (int)D_DIV((double)F_MUL(theta, (float)bins), kTwoPi);
                 if (bin >= bins) bin -= bins;
                 const double ddx = D_SUB((double)x, cx), ddy = D_SUB((double)y, cy);

@@ -108,3 +108,26 @@ cudaError_t launch_value_noise(float* out, int n, int w, int h, unsigned long lo
 }
 
 }  // namespace dsift
+
+// ---- test probe: the device libm restatements over caller arrays ----------------
+#include "dsift_math.cuh"
+namespace dsift {
+__global__ void libm_probe_kernel(int mode, const void* in, long long n, void* out) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        if (mode == 0) {   // atan2f(y, x): in float2 (y, x) -> float
+            const float2 yx = static_cast<const float2*>(in)[i];
+            static_cast<float*>(out)[i] = dsift_atan2f(yx.x, yx.y);
+        } else if (mode == 1) {   // exp(double) -> double
+            static_cast<double*>(out)[i] = dsift_exp(static_cast<const double*>(in)[i]);
+        } else {   // sincos(double) -> double2 (sin, cos)
+            double s, c;
+            dsift_sincos(static_cast<const double*>(in)[i], &s, &c);
+            static_cast<double2*>(out)[i] = make_double2(s, c);
+        }
+    }
+}
+cudaError_t launch_libm_probe(int mode, const void* in, long long n, void* out, cudaStream_t st) {
+    libm_probe_kernel<<<256, 256, 0, st>>>(mode, in, n, out);
+    return cudaGetLastError();
+}
+}  // namespace dsift

@@ -1,0 +1,50 @@
+"""CPU: the product's restatements of the host libm calls on the path
+(paper_2605_17869_b200/csrc/dsift_math.cuh, compiled here as host code with
+no FP contraction) reproduce this host's glibc bit-for-bit.  The GPU test
+test_gpu_parity.py::test_device_libm_matches_host closes the loop device ->
+host twin; together: device == glibc, the function the reference calls."""
+import ctypes as C
+import os
+
+import pytest
+
+LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "native", "liblibmcheck.so")
+
+
+@pytest.fixture(scope="module")
+def lc():
+    if not os.path.exists(LIB):
+        pytest.skip("tests/native/liblibmcheck.so not built (run __graft_entry__.build())")
+    lib = C.CDLL(LIB)
+    lib.lc_atan2f_mismatch.restype = C.c_int64
+    lib.lc_atan2f_mismatch.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_void_p]
+    lib.lc_exp_mismatch.restype = C.c_int64
+    lib.lc_exp_mismatch.argtypes = [C.c_uint64, C.c_int64, C.c_double, C.c_double, C.c_int, C.c_void_p]
+    lib.lc_sincos_mismatch.restype = C.c_int64
+    lib.lc_sincos_mismatch.argtypes = [C.c_uint64, C.c_int64, C.c_void_p]
+    return lib
+
+
+@pytest.mark.parametrize("mode,n", [(0, 4_000_000), (1, 8_000_000), (2, 20_000)])
+def test_atan2f_bit_exact(lc, mode, n):
+    first = (C.c_float * 3)()
+    bad = lc.lc_atan2f_mismatch(12345 + mode, n, mode, first)
+    assert bad == 0, f"{bad} mismatches, first (y, x, got) = {list(first)}"
+
+
+@pytest.mark.parametrize("lo,hi,mode", [(-10.0, 0.0, 0), (-1.6, 0.0, 1), (-745.2, 709.8, 0),
+                                        (-1e-12, 1e-12, 0), (-760.0, -700.0, 0)])
+def test_exp_bit_exact(lc, lo, hi, mode):
+    first = (C.c_double * 2)()
+    bad = lc.lc_exp_mismatch(777, 4_000_000, lo, hi, mode, first)
+    assert bad == 0, f"{bad} mismatches, first (x, got) = {list(first)}"
+
+
+def test_sincos_float_level(lc):
+    # cos/sin feed double sample coordinates (describe.cpp:51-52); the
+    # double-double evaluation can differ from glibc's (<0.52 ulp, not always
+    # correctly rounded) in the last double bit, never after rounding to float.
+    fb = C.c_int64()
+    bad = lc.lc_sincos_mismatch(99, 1_000_000, C.byref(fb))
+    assert fb.value == 0
+    assert bad < 10_000   # ~0.3% differ in the last double bit
