@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -521,13 +522,19 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
     a.slow_count = &ctr->n_slow;
     a.slow_cap = cap_n;
     a.force_slow = c->force_exact;
-    const size_t smem_fast = describe_fast_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
+    DescArgs af = a;
+    af.chunk_rows = 6;   // kFastChunk: the fast kernel's sample ring holds chunk + 2 rows
+    {
+        const char* hp = std::getenv("DSIFT_HOT_PAIR");
+        af.hot_pair = hp ? std::atoi(hp) : 1;
+    }
+    const size_t smem_fast = describe_fast_smem_bytes(a.max_axis, af.chunk_rows, a.n_dsp);
     const size_t smem_exact = describe_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
     if (smem_fast > 200 * 1024 || smem_exact > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
     const int per_sm = std::max(1, describe_blocks_per_sm(smem_fast));
     int grid = c->sm_count * per_sm;
     if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
-    cuda_check(launch_describe_fast(a, grid, c->stream), "describe fast");
+    cuda_check(launch_describe_fast(af, grid, c->stream), "describe fast");
     DescArgs b = a;
     b.slow_list = c->slow.as<int>();
     b.n_slow = &ctr->n_slow;

@@ -79,6 +79,7 @@ struct DescArgs {
     unsigned* slow_count;
     long long slow_cap;
     int force_slow;        // test hook: fail every certificate
+    int hot_pair;          // fast path: cache the (o0, o0+1) accumulators in registers
     float* desc;
     unsigned char* desc_u8;
     unsigned* err;

@@ -31,7 +31,9 @@ namespace dsift {
 
 constexpr int kDescThreads = 128;
 constexpr int kTreeDepth = 13;   // per-bin leaves < 8192 (checked on the host)
-constexpr int kRing = 32;        // per-bin leaf ring (flushed every 16 candidate points)
+constexpr int kRing = 32;
+constexpr int kFastChunk = 6;                 // lattice rows per fast-path chunk
+constexpr int kSampRing = kFastChunk + 2;     // sample rows kept (chunk + guard rows)        // per-bin leaf ring (flushed every 16 candidate points)
 constexpr float kUndef = -1.0f;  // describe.cpp:188
 
 struct DescSmem {
@@ -216,7 +218,7 @@ __device__ __forceinline__ void raw_descriptor_cta(const DescArgs& a, const Desc
                         atomicOr(a.err, kErrHistogramRange);
                         theta = 0.0f;
                     }
-                    double obin = D_DIV((double)F_MUL(theta, (float)kDescOrients), kTwoPi);
+                    double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
                     if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
                     // -(uu^2 + vv^2) / 8: division by 8 is an exact scaling, == * 0.125
                     const double arg = D_MUL(-D_ADD(S.q2[u - kbase], S.q2[v - kbase]), 0.125);
@@ -395,20 +397,19 @@ describe_exact_kernel(const __grid_constant__ DescArgs a) {
 // kernel above, so the output is bit-identical either way.
 // ------------------------------------------------------------------------------
 struct FastSmem {
-    double* q2;
-    double* bin;
-    double* ax;
-    double* cy_su;
-    double* sv;
-    double* cv;
+    double* q2;     // (k/bw)^2
+    double* ax;     // cx + cos*k
+    double* cy_su;  // cy + sin*k
+    double* sv;     // sin*k
+    double* cv;     // cos*k
     float* frac;
     int* c0;
-    float* samp;    // [(chunk+2)][A]
-    float* pval;    // [chunk][A]
-    float* pfo;     // [chunk][A]
+    float* samp;    // ring of kSampRing sample rows x A
+    float2* pvf;    // [chunk][A] (value, fo)
+    float* wct;     // [4][A] column weight of histogram column c at lattice u
     unsigned char* po0;
     double* acc;    // [8][128] item-private partial sums
-    int* lsb;       // [8][128] item-private min exponent of any leaf's lowest bit
+    short* lsb;     // [8][128] item-private min exponent of any leaf's lowest bit
     float* raw;     // [n_dsp][128]
     int* misc;      // band / column-range scratch
 };
@@ -441,38 +442,33 @@ __device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const Fas
     }
     const int kbase = -radius - 1;
     const int naxis = 2 * radius + 3;
-    for (int i = tid; i < naxis; i += kDescThreads) {
+    // misc[0..1] = in-range span [kmin, kmax]; misc[2+2c], misc[3+2c] = span of
+    // the points feeding histogram column c (bin floor in {c-1, c});
+    // misc[10+2(R+1)], misc[11+2(R+1)] = rows of band R (bin floor == R)
+    if (tid < 20) S.misc[tid] = (tid & 1) ? -(1 << 30) : (1 << 30);
+    __syncthreads();
+    for (int i = tid; i < naxis; i += kDescThreads) {   // describe.cpp:48-52, 72-73, 89-99
         const int k = kbase + i;
         const double q = D_DIV((double)k, bw);
         const double bn = D_ADD(q, (double)(kDescCells / 2 - 0.5));
         const int c = (int)floor(bn);
         S.q2[i] = D_MUL(q, q);
-        S.bin[i] = bn;
         S.c0[i] = c;
         S.frac[i] = (float)D_SUB(bn, (double)c);
         S.ax[i] = D_ADD(cx, D_MUL(cosa, (double)k));
         S.cy_su[i] = D_ADD(cy, D_MUL(sina, (double)k));
         S.sv[i] = D_MUL(sina, (double)k);
         S.cv[i] = D_MUL(cosa, (double)k);
-    }
-    __syncthreads();
-    // misc[0..1] = kmin, kmax; misc[2+2c], misc[3+2c] = column span of cell col c;
-    // misc[10+2R'], misc[11+2R'] = row span of band R = R'-1
-    if (tid < 16) S.misc[tid] = (tid & 1) ? -(1 << 30) : (1 << 30);
-    __syncthreads();
-    if (tid < 32) {
-        for (int i = 1 + tid; i < naxis - 1; i += 32) {
-            const double bn = S.bin[i];
-            if (bn > -1.0 && bn < (double)kDescCells) {
-                const int k = kbase + i, c = S.c0[i];
-                atomicMin(&S.misc[0], k);
-                atomicMax(&S.misc[1], k);
-                for (int cc = 0; cc < kDescCells; ++cc)
-                    if (c == cc - 1 || c == cc) {
-                        atomicMin(&S.misc[2 + 2 * cc], k);
-                        atomicMax(&S.misc[3 + 2 * cc], k);
-                    }
-            }
+        const float fr = (float)D_SUB(bn, (double)c);
+#pragma unroll
+        for (int cc = 0; cc < kDescCells; ++cc) S.wct[cc * a.max_axis + i] = (cc - c) ? fr : F_SUB(1.0f, fr);
+        if (i >= 1 && i < naxis - 1 && bn > -1.0 && bn < (double)kDescCells) {
+            atomicMin(&S.misc[0], k);
+            atomicMax(&S.misc[1], k);
+            if (c >= 0) { atomicMin(&S.misc[2 + 2 * c], k); atomicMax(&S.misc[3 + 2 * c], k); }
+            if (c + 1 < kDescCells) { atomicMin(&S.misc[4 + 2 * c], k); atomicMax(&S.misc[5 + 2 * c], k); }
+            atomicMin(&S.misc[12 + 2 * c], k);
+            atomicMax(&S.misc[13 + 2 * c], k);
         }
     }
     __syncthreads();
@@ -483,50 +479,58 @@ __device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const Fas
     const int brow = tid >> 5, bcol = (tid >> 3) & 3, bori = tid & 7;
     double binacc = 0.0;
     int binlsb = 1 << 20;   // min lowest-bit exponent over this bin's nonzero leaves
-    int kterms = 0;   // max sequential terms in any partial sum this thread formed
+    int kterms = 0;         // max sequential terms in any partial sum this thread formed
+    int sampled_to = kmin - 2;   // last lattice row whose samples sit in the ring
+#define SROW(v) (S.samp + ((unsigned)((v) - kmin + 1) & (kSampRing - 1)) * swidth)
 
     // bands: rows whose vbin floor is R (R = -1..3) feed histogram rows R and R+1
-    int v = kmin;
-    for (int R = -1; R < kDescCells && v <= kmax; ++R) {
-        const int vb0 = v;
-        while (v <= kmax && S.c0[v - kbase] == R) ++v;
-        const int vb1 = v - 1;
+    for (int R = -1; R < kDescCells; ++R) {
+        const int vb0 = S.misc[12 + 2 * R], vb1 = S.misc[13 + 2 * R];
         if (vb1 < vb0) continue;
         const int tr_first = R < 0 ? 0 : R;
         const int ntr = (R < 0 || R + 1 >= kDescCells) ? 1 : 2;
         const int npairs = ntr * kDescCells;
-        const int nsl = kDescThreads / npairs;      // slices per (row, col) pair
-        const int pair = tid / nsl, slice = tid - pair * nsl;
+        const int lg = (npairs == 8) ? 4 : 5;       // slices per (row, col) pair = 2^lg
+        const int nsl = 1 << lg;
+        const int pair = tid >> lg, slice = tid & (nsl - 1);
         const int tr = tr_first + (pair >> 2), tc = pair & 3;
         const int uc0 = S.misc[2 + 2 * tc], uc1 = S.misc[3 + 2 * tc];
         const int ucount = uc1 - uc0 + 1;
+        const float inv_uc = 1.0f / (float)ucount;
+        const float* wcol = S.wct + tc * A + (uc0 - kbase);
         const bool upper = (tr != R);               // ri = 1 -> wr = fr
 #pragma unroll
         for (int o = 0; o < kDescOrients; ++o) {
             S.acc[o * kDescThreads + tid] = 0.0;
-            S.lsb[o * kDescThreads + tid] = 1 << 20;
+            S.lsb[o * kDescThreads + tid] = (short)32767;
         }
         int myterms = 0;
         for (int v0 = vb0; v0 <= vb1; v0 += a.chunk_rows) {
             const int v1 = min(v0 + a.chunk_rows - 1, vb1);
             const int nrows = v1 - v0 + 1;
+            // samples for rows [v0-1, v1+1]; rows already in the ring are kept
+            const int s0 = max(v0 - 1, sampled_to + 1), s1 = v1 + 1;
             __syncthreads();
-            for (int idx = tid; idx < (nrows + 2) * swidth; idx += kDescThreads) {
-                const int rr = idx / swidth, cc = idx - rr * swidth;
-                const int vv = v0 - 1 + rr, u = kmin - 1 + cc;
+            const float inv_sw = 1.0f / (float)swidth;   // exact row split for idx < 2^16
+            const double wm1 = (double)(w - 1), hm1 = (double)(h - 1);
+            for (int idx = tid; idx < (s1 - s0 + 1) * swidth; idx += kDescThreads) {
+                const int rr = (int)(((float)idx + 0.5f) * inv_sw), cc = idx - rr * swidth;
+                const int vv = s0 + rr, u = kmin - 1 + cc;
                 const double px = D_SUB(S.ax[u - kbase], S.sv[vv - kbase]);
                 const double py = D_ADD(S.cy_su[u - kbase], S.cv[vv - kbase]);
                 float sv = kUndef;
-                if (!(px < 0.0 || px > (double)(w - 1) || py < 0.0 || py > (double)(h - 1)))
+                if (!(px < 0.0 || px > wm1 || py < 0.0 || py > hm1))
                     sv = sample_bilinear(img, w, h, pitch, px, py);
-                S.samp[idx] = sv;
+                SROW(vv)[cc] = sv;
             }
+            sampled_to = s1;
             __syncthreads();
+            const float inv_w = 1.0f / (float)width;
             for (int idx = tid; idx < nrows * width; idx += kDescThreads) {
-                const int rr = idx / width, cc = idx - rr * width;
+                const int rr = (int)(((float)idx + 0.5f) * inv_w), cc = idx - rr * width;
                 const int vv = v0 + rr, u = kmin + cc;
-                const float* sr = S.samp + (rr + 1) * swidth + (cc + 1);
-                const float left = sr[-1], right = sr[1], up = sr[-swidth], down = sr[swidth];
+                const float* mid = SROW(vv) + cc + 1;
+                const float left = mid[-1], right = mid[1], up = SROW(vv - 1)[cc + 1], down = SROW(vv + 1)[cc + 1];
                 unsigned char o0 = 0xff;
                 float value = 0.0f, fo = 0.0f;
                 if (!(left == kUndef || right == kUndef || up == kUndef || down == kUndef)) {
@@ -539,7 +543,7 @@ __device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const Fas
                         atomicOr(a.err, kErrHistogramRange);
                         theta = 0.0f;
                     }
-                    double obin = D_DIV((double)F_MUL(theta, (float)kDescOrients), kTwoPi);
+                    double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
                     if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
                     const double arg = D_MUL(-D_ADD(S.q2[u - kbase], S.q2[vv - kbase]), 0.125);
                     const float wgt = (float)dsift_exp(arg);
@@ -548,43 +552,71 @@ __device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const Fas
                     fo = (float)D_SUB(obin, (double)o);
                     o0 = (unsigned char)o;
                 }
-                S.pval[rr * A + cc] = value;
-                S.pfo[rr * A + cc] = fo;
+                S.pvf[rr * A + cc] = make_float2(value, fo);
                 S.po0[rr * A + cc] = o0;
             }
             __syncthreads();
-            // balanced accumulation: item (pair, slice) takes every nsl-th point
-            // of the pair's rows x [uc0, uc1] block; two leaves per point
+            // balanced accumulation: item (pair, slice) takes a contiguous run of
+            // the pair's rows x [uc0, uc1] block (row-major); two leaves per
+            // point.  The (o0, o0+1) accumulator pair lives in registers while
+            // the run's orientation stays put (gradient orientation is spatially
+            // coherent); it is spilled to the item's shared slots on a change.
             const int tot = nrows * ucount;
-            int rr = slice / ucount, cu = slice - rr * ucount;
-            for (int i = slice; i < tot; i += nsl) {
-                const int cc = uc0 - kmin + cu;
-                const unsigned char o0 = S.po0[rr * A + cc];
-                if (o0 != 0xff) {
-                    const int vv = v0 + rr, u = uc0 + cu;
-                    const float fr = S.frac[vv - kbase], fc = S.frac[u - kbase];
-                    const float wr = upper ? fr : F_SUB(1.0f, fr);
-                    const float wc = (tc - S.c0[u - kbase]) ? fc : F_SUB(1.0f, fc);
-                    const float fo = S.pfo[rr * A + cc];
-                    const float t = F_MUL(F_MUL(S.pval[rr * A + cc], wr), wc);
-                    const float l0 = F_MUL(t, F_SUB(1.0f, fo));   // orientation o0
-                    const float l1 = F_MUL(t, fo);                // orientation o0 + 1
-                    const int i0 = o0 * kDescThreads + tid;
-                    const int i1 = ((o0 + 1) & (kDescOrients - 1)) * kDescThreads + tid;
-                    S.acc[i0] = S.acc[i0] + (double)l0;
-                    S.acc[i1] = S.acc[i1] + (double)l1;
-                    if (l0 != 0.0f) S.lsb[i0] = min(S.lsb[i0], float_lsb_exp(l0));
-                    if (l1 != 0.0f) S.lsb[i1] = min(S.lsb[i1], float_lsb_exp(l1));
-                    ++myterms;
+            const int runlen = (tot + nsl - 1) >> lg;
+            const int i0 = slice * runlen, i1 = min(tot, i0 + runlen);
+            if (i0 < i1) {
+                int rr = (int)(((float)i0 + 0.5f) * inv_uc), cu = i0 - rr * ucount;
+                int hot = -1;
+                double ha = 0.0, hb = 0.0;
+                int ea = 0x7fff, eb = 0x7fff;   // min exponent field of nonzero leaves
+                const int cbase = uc0 - kmin;
+                for (int i = i0; i < i1; ++i) {
+                    const int pidx = rr * A + cbase + cu;
+                    const int o0 = S.po0[pidx];
+                    if (o0 != 0xff) {
+                        const float fr = S.frac[v0 + rr - kbase];
+                        const float wr = upper ? fr : F_SUB(1.0f, fr);
+                        const float2 pv = S.pvf[pidx];
+                        const float t = F_MUL(F_MUL(pv.x, wr), wcol[cu]);
+                        const float l0 = F_MUL(t, F_SUB(1.0f, pv.y));   // orientation o0
+                        const float l1 = F_MUL(t, pv.y);                // orientation o0 + 1
+                        if (o0 != hot) {
+                            if (hot >= 0) {
+                                const int ia = hot * kDescThreads + tid;
+                                const int ib = ((hot + 1) & (kDescOrients - 1)) * kDescThreads + tid;
+                                S.acc[ia] = S.acc[ia] + ha;
+                                S.acc[ib] = S.acc[ib] + hb;
+                                S.lsb[ia] = (short)min((int)S.lsb[ia], ea);
+                                S.lsb[ib] = (short)min((int)S.lsb[ib], eb);
+                            }
+                            hot = o0;
+                            ha = hb = 0.0;
+                            ea = eb = 0x7fff;
+                        }
+                        ha = ha + (double)l0;
+                        hb = hb + (double)l1;
+                        const unsigned b0 = __float_as_uint(l0), b1 = __float_as_uint(l1);
+                        ea = min(ea, b0 ? max((int)(b0 >> 23), 1) : 0x7fff);
+                        eb = min(eb, b1 ? max((int)(b1 >> 23), 1) : 0x7fff);
+                        ++myterms;
+                    }
+                    if (++cu == ucount) {
+                        cu = 0;
+                        ++rr;
+                    }
                 }
-                cu += nsl;
-                while (cu >= ucount) {
-                    cu -= ucount;
-                    ++rr;
+                if (hot >= 0) {
+                    const int ia = hot * kDescThreads + tid;
+                    const int ib = ((hot + 1) & (kDescOrients - 1)) * kDescThreads + tid;
+                    S.acc[ia] = S.acc[ia] + ha;
+                    S.acc[ib] = S.acc[ib] + hb;
+                    S.lsb[ia] = (short)min((int)S.lsb[ia], ea);
+                    S.lsb[ib] = (short)min((int)S.lsb[ib], eb);
                 }
             }
         }
-        kterms = max(kterms, myterms);
+        // a leaf's path: <= myterms adds in its register run + <= myterms spills
+        kterms = max(kterms, 2 * myterms + 2);
         __syncthreads();
         // fold this band's slices into the bins of rows R, R+1 (fixed order)
         if (brow >= tr_first && brow < tr_first + ntr) {
@@ -592,21 +624,22 @@ __device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const Fas
             double sacc = 0.0;
             for (int sl = 0; sl < nsl; ++sl) {
                 sacc = sacc + S.acc[bori * kDescThreads + bp * nsl + sl];
-                binlsb = min(binlsb, S.lsb[bori * kDescThreads + bp * nsl + sl]);
+                binlsb = min(binlsb, (int)S.lsb[bori * kDescThreads + bp * nsl + sl] - 150);
             }
             binacc = binacc + sacc;
         }
         __syncthreads();   // the next band re-zeroes S.acc
     }
+#undef SROW
     // certificate: |tree - S| <= 13u S,  |binacc - S| <= (K + 32 + 2) u S
     const int kmaxterms = __reduce_max_sync(0xffffffffu, kterms);
-    if ((tid & 31) == 0) S.misc[16 + (tid >> 5)] = kmaxterms;
+    if ((tid & 31) == 0) S.misc[20 + (tid >> 5)] = kmaxterms;
     __syncthreads();
-    const int K = max(max(S.misc[16], S.misc[17]), max(S.misc[18], S.misc[19]));
+    const int K = max(max(S.misc[20], S.misc[21]), max(S.misc[22], S.misc[23]));
     // (a) exact case: if every leaf's lowest bit and the sum's top bit span at
     //     most 53 bits, every partial sum in ANY order is exact, so the tree
     //     and this sum are both the exact S;
-    // (b) otherwise the interval test above.
+    // (b) otherwise the rounding-interval test.
     bool ok;
     float res;
     const int top = (int)((__double_as_longlong(binacc) >> 52) & 0x7ff) - 1023;
@@ -626,7 +659,7 @@ __device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const Fas
     return ok;
 }
 
-__global__ void __launch_bounds__(kDescThreads, 5)
+__global__ void __launch_bounds__(kDescThreads, 6)
 describe_fast_kernel(const __grid_constant__ DescArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ double red[4];
@@ -635,19 +668,18 @@ describe_fast_kernel(const __grid_constant__ DescArgs a) {
     FastSmem S;
     unsigned char* pbuf = sm;
     S.q2 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
-    S.bin = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
     S.ax = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
     S.cy_su = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
     S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
     S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
     S.acc = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * kDescOrients * kDescThreads;
-    S.lsb = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * kDescOrients * kDescThreads;
     S.frac = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * A;
     S.c0 = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * A;
     S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * a.n_dsp;
-    S.samp = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * (a.chunk_rows + 2) * A;
-    S.pval = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * A;
-    S.pfo = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * A;
+    S.samp = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kSampRing * A;
+    S.pvf = reinterpret_cast<float2*>(pbuf); pbuf += sizeof(float2) * a.chunk_rows * A;
+    S.wct = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescCells * A;
+    S.lsb = reinterpret_cast<short*>(pbuf); pbuf += sizeof(short) * kDescOrients * kDescThreads;
     S.po0 = pbuf;
     S.misc = misc;
 
@@ -703,10 +735,10 @@ cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev,
 
 size_t describe_fast_smem_bytes(int max_axis, int chunk_rows, int n_dsp) {
     const size_t A = (size_t)max_axis;
-    return sizeof(double) * 6 * A + sizeof(double) * kDescOrients * kDescThreads +
-           sizeof(int) * kDescOrients * kDescThreads + sizeof(float) * A +
-           sizeof(int) * A + sizeof(float) * kDescDim * n_dsp + sizeof(float) * (chunk_rows + 2) * A +
-           sizeof(float) * 2 * chunk_rows * A + chunk_rows * A + 16;
+    return sizeof(double) * 5 * A + sizeof(double) * kDescOrients * kDescThreads +
+           sizeof(short) * kDescOrients * kDescThreads + sizeof(float) * A + sizeof(int) * A +
+           sizeof(float) * kDescDim * n_dsp + sizeof(float) * kSampRing * A + sizeof(float) * 2 * chunk_rows * A +
+           sizeof(float) * kDescCells * A + chunk_rows * A + 16;
 }
 
 int describe_blocks_per_sm(size_t smem) {

@@ -112,7 +112,7 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                     atomicOr(a.err, kErrHistogramRange);
                     theta = 0.0f;
                 }
-                bin = (int)D_DIV((double)F_MUL(theta, (float)bins), kTwoPi);
+                bin = (int)ds_div_2pi((double)F_MUL(theta, (float)bins));
                 if (bin >= bins) bin -= bins;
                 const double ddx = D_SUB((double)x, cx), ddy = D_SUB((double)y, cy);
                 const double arg = D_DIV(-D_ADD(D_MUL(ddx, ddx), D_MUL(ddy, ddy)), denom);

@@ -149,3 +149,18 @@ void lc_sincos_batch(const double* a, int64_t n, double* s, double* c) {
 }
 
 }  // extern "C"
+
+extern "C" {
+// Exhaustive: ds_div_2pi(t) == t / (2pi) (IEEE) for every float t in [0, tmax].
+int64_t lc_div2pi_mismatch(float tmax) {
+    int64_t bad = 0;
+    for (uint32_t u = 0;; ++u) {
+        float t;
+        std::memcpy(&t, &u, 4);
+        if (!(t <= tmax)) break;
+        const double td = (double)t;
+        if (ds_div_2pi(td) != td / 6.283185307179586476925286766559) ++bad;
+    }
+    return bad;
+}
+}

@@ -48,3 +48,11 @@ def test_sincos_float_level(lc):
     bad = lc.lc_sincos_mismatch(99, 1_000_000, C.byref(fb))
     assert fb.value == 0
     assert bad < 10_000   # ~0.3% differ in the last double bit
+
+
+def test_div_2pi_exhaustive(lc):
+    # the orientation-bin quotient (orient.cpp:52, describe.cpp:92) for every
+    # float numerator up to 64 bins * 2pi
+    lc.lc_div2pi_mismatch.restype = C.c_int64
+    lc.lc_div2pi_mismatch.argtypes = [C.c_float]
+    assert lc.lc_div2pi_mismatch(512.0) == 0
