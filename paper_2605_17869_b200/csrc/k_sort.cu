@@ -107,7 +107,7 @@ cudaError_t launch_canonical_sort(const DevKeypoint* in, const unsigned long lon
         cudaError_t e = cub::DeviceRadixSort::SortPairs(sb.temp, tb, sb.keys_a, sb.keys_b, vin, vout,
                                                         (int)cap, 0, 64, st);
         if (e != cudaSuccess) return e;
-        *launches += 4;  // onesweep: histogram + passes (approximate accounting)
+        *launches += 10;  // onesweep on 64-bit keys: histogram + exclusive sum + 8 digit passes
         perm = vout;
         cur_idx = vout;
     }
