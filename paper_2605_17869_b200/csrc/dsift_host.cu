@@ -192,6 +192,9 @@ struct Counters {          // one small device block, cleared per batch
     unsigned det_ticket;
     unsigned ori_ticket;
     unsigned n_slow;      // keypoints the certified fast descriptor path handed to the exact kernel
+    unsigned ref_ticket;
+    unsigned pad2;
+    unsigned long long n_kp;   // refined keypoints (compacted)
 };
 
 }  // namespace dsift
@@ -208,7 +211,8 @@ struct dsift_ctx {
     int batch = 0;            // images in the current pyramid / result
     PyramidDesc pyr{};
     DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
-        pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow;
+        pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow,
+        ref_states, keep;
     long long cap_det = 0, cap_ori = 0;
     long long launches = 0;
     bool result_pending = false, result_ready = false;
@@ -388,32 +392,29 @@ static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
     ++c->launches;
 }
 
-static void run_detect_with_candidates(dsift_ctx* c, long long cap) {
-    // refine mode + originating candidates (stage API only)
+// K3: refine the compacted candidates (count n_det) into compacted keypoints
+// (count n_kp), candidate order kept.
+static void run_refine(dsift_ctx* c, long long cap, int* keep = nullptr) {
     const dsift_config& cf = c->cfg.c;
     DetectArgs a{};
     a.pyr = c->pyr;
-    a.n_tiles = detect_tiles(c->pyr, a.oct_tile_base, &a.tiles_per_image);
-    a.pre_gate = 0.5f * cf.contrast_threshold / cf.intervals;
     a.contrast_gate = double(cf.contrast_threshold) / cf.intervals;
     a.edge_r = cf.edge_ratio;
     a.max_iters = cf.max_refine_iters;
-    a.raw_mode = 0;
     c->det_kps.ensure(sizeof(DevKeypoint) * (size_t)cap);
-    c->det_cand.ensure(sizeof(DevCandidate) * (size_t)cap);
     a.out = c->det_kps.as<DevKeypoint>();
-    a.cand_out = c->det_cand.as<DevCandidate>();
     a.cap = cap;
     Counters* ctr = counters(c);
     a.err = &ctr->err;
-    c->det_states.ensure(sizeof(unsigned long long) * (size_t)std::max(1u, a.n_tiles));
-    cuda_check(cudaMemsetAsync(c->det_states.as<void>(), 0, sizeof(unsigned long long) * std::max(1u, a.n_tiles),
+    const unsigned max_tiles = (unsigned)((cap + 255) / 256);
+    c->ref_states.ensure(sizeof(unsigned long long) * (size_t)std::max(1u, max_tiles));
+    cuda_check(cudaMemsetAsync(c->ref_states.as<void>(), 0, sizeof(unsigned long long) * std::max(1u, max_tiles),
                                c->stream), "memset");
-    a.scan.states = c->det_states.as<unsigned long long>();
-    a.scan.ticket = &ctr->det_ticket;
-    a.scan.total = &ctr->n_det;
+    a.scan.states = c->ref_states.as<unsigned long long>();
+    a.scan.ticket = &ctr->ref_ticket;
+    a.scan.total = &ctr->n_kp;
     a.scan.cap = (unsigned long long)cap;
-    cuda_check(launch_detect(a, c->stream), "detect");
+    cuda_check(launch_refine(a, c->det_cand.as<DevCandidate>(), &ctr->n_det, cap, keep, c->stream), "refine");
     ++c->launches;
 }
 
@@ -439,7 +440,7 @@ static void run_orient(dsift_ctx* c, const DevKeypoint* kps, long long n_host, l
     a.pyr = c->pyr;
     a.kps = kps;
     Counters* ctr = counters(c);
-    a.n_dev = &ctr->n_det;
+    a.n_dev = &ctr->n_kp;
     a.n_host = n_host;
     a.bins = cf.orientation_bins;
     a.peak_ratio = cf.orientation_peak_ratio;
@@ -574,9 +575,10 @@ static void extract_batch(dsift_ctx* c, const float* images, int n, int w, int h
     launch_pyramid(c, dev_in);
     if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[1], c->stream), "event");
 
-    c->cap_det = (long long)n * auto_cap(c, 1.0 / 24.0);
+    c->cap_det = (long long)n * auto_cap(c, 1.0 / 12.0);   // candidates (extrema) per batch
     c->cap_ori = (long long)n * auto_cap(c, 1.0 / 16.0);
-    run_detect(c, 0, c->cap_det);
+    run_detect(c, 1, c->cap_det);                        // K2: compacted extrema
+    run_refine(c, c->cap_det);                           // K3: one thread per candidate
     if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[2], c->stream), "event");
     c->ori_kps.ensure(sizeof(DevKeypoint) * (size_t)c->cap_ori);
     run_orient(c, c->det_kps.as<DevKeypoint>(), -1, c->cap_det, c->ori_kps.as<DevKeypoint>(), c->cap_ori,
@@ -1027,28 +1029,37 @@ int dsift_detect(dsift_ctx* c, dsift_keypoint* out, int64_t cap, int64_t* n) {
         long long dcap = 0;
         for (int o = 0; o < c->plan.n_oct; ++o) dcap += (long long)c->plan.ow[o] * c->plan.oh[o] * c->plan.s / 2 + 16;
         reset_counters(c);
-        run_detect_with_candidates(c, dcap);
+        c->keep.ensure(sizeof(int) * (size_t)dcap);
+        run_detect(c, 1, dcap);   // the hot path's kernels: extrema, then refine
+        run_refine(c, dcap, c->keep.as<int>());
         cuda_check(cudaStreamSynchronize(c->stream), "sync");
         Counters h{};
         cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
-        const size_t m = (size_t)h.n_det;
+        const size_t mc = (size_t)h.n_det, m = (size_t)h.n_kp;
         std::vector<DevKeypoint> kp(m);
-        std::vector<DevCandidate> cd(m);
-        if (m) {
-            cuda_check(cudaMemcpy(kp.data(), c->det_kps.as<void>(), m * sizeof(DevKeypoint), cudaMemcpyDeviceToHost), "D2H");
-            cuda_check(cudaMemcpy(cd.data(), c->det_cand.as<void>(), m * sizeof(DevCandidate), cudaMemcpyDeviceToHost), "D2H");
+        std::vector<DevCandidate> cd(mc);
+        std::vector<int> keep(mc);
+        if (m) cuda_check(cudaMemcpy(kp.data(), c->det_kps.as<void>(), m * sizeof(DevKeypoint), cudaMemcpyDeviceToHost), "D2H");
+        if (mc) {
+            cuda_check(cudaMemcpy(cd.data(), c->det_cand.as<void>(), mc * sizeof(DevCandidate), cudaMemcpyDeviceToHost), "D2H");
+            cuda_check(cudaMemcpy(keep.data(), c->keep.as<void>(), mc * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
         }
-        std::vector<size_t> order(m);
-        for (size_t i = 0; i < m; ++i) order[i] = i;
-        std::stable_sort(order.begin(), order.end(), [&](size_t i, size_t j) {
-            const DevCandidate &a = cd[i], &b = cd[j];
+        // survivors are compacted in candidate-array order; pair each with its
+        // candidate, then restore the reference's (octave, interval, row, col) order
+        std::vector<std::pair<size_t, size_t>> surv;   // (candidate, keypoint)
+        for (size_t i = 0, j = 0; i < mc; ++i)
+            if (keep[i]) surv.push_back({i, j++});
+        std::stable_sort(surv.begin(), surv.end(), [&](const auto& p, const auto& q) {
+            const DevCandidate &a = cd[p.first], &b = cd[q.first];
             if (a.octave != b.octave) return a.octave < b.octave;
             if (a.interval != b.interval) return a.interval < b.interval;
             if (a.row != b.row) return a.row < b.row;
             return a.col < b.col;
         });
-        *n = (int64_t)m;
-        for (size_t k = 0; k < m && (int64_t)k < cap; ++k) {
+        std::vector<size_t> order;
+        for (const auto& p : surv) order.push_back(p.second);
+        *n = (int64_t)order.size();
+        for (size_t k = 0; k < order.size() && (int64_t)k < cap; ++k) {
             const DevKeypoint& s = kp[order[k]];
             out[k] = dsift_keypoint{s.x, s.y, s.sigma, s.angle, s.response, s.octave, s.interval};
         }

@@ -41,6 +41,8 @@ struct DetectArgs {
     ScanState scan;
 };
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st);
+cudaError_t launch_refine(const DetectArgs& a, const DevCandidate* cand, const unsigned long long* n_cand,
+                          long long cap, int* keep, cudaStream_t st);
 
 struct OrientArgs {
     PyramidDesc pyr;

@@ -135,13 +135,14 @@ detect_kernel(const __grid_constant__ DetectArgs a) {
         return true;
     };
 
-    // pass 1: count accepted outputs per thread; pass 2: write them.
+    // pass 1 tests every (level, row) of this thread once and remembers hits in
+    // a bitmask (bit = level-major index); pass 2 only replays the hits.
+    unsigned long long hits = 0;
     int count = 0;
-    unsigned long long base = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-        int k = 0;
+    {
+        int bit = 0;
         for (int i = 1; i <= s; ++i) {
-            for (int q = 0; q < kDetTile / 8; ++q) {
+            for (int q = 0; q < kDetTile / 8; ++q, ++bit) {
                 const int ly = ly0 + 8 * q;
                 const int x = xs + lx, y = ys + ly;
                 if (x > w - 2 || y > h - 2) continue;
@@ -149,55 +150,89 @@ detect_kernel(const __grid_constant__ DetectArgs a) {
                 if (!(fabsf(v) > a.pre_gate)) continue;
                 const bool is_max = v > 0.0f;
                 if (!extremal(i, lx + 1, ly + 1, v, is_max)) continue;
-                if (a.raw_mode) {
-                    if (pass == 1) {
-                        const unsigned long long slot = base + k;
-                        if ((long long)slot < a.cap) {
-                            DevCandidate c = {b, o, i, y, x, is_max ? 1 : 0};
-                            a.cand_out[slot] = c;
-                        }
-                    }
-                    ++k;
-                    continue;
-                }
-                DevKeypoint kp;
-                if (!refine_candidate(a, b, o, x, y, i, &kp)) continue;
-                if (pass == 1) {
-                    const unsigned long long slot = base + k;
-                    if ((long long)slot < a.cap) {
-                        a.out[slot] = kp;
-                        if (a.cand_out) {
-                            DevCandidate c = {b, o, i, y, x, is_max ? 1 : 0};
-                            a.cand_out[slot] = c;
-                        }
-                    }
-                }
-                ++k;
+                hits |= 1ull << bit;
+                ++count;
             }
-        }
-        if (pass == 0) {
-            count = k;
-            // block exclusive scan of per-thread counts (thread order)
-            int incl = count;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int n = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lx >= d) incl += n;
-            }
-            if (lx == 31) warp_tot[ly0] = incl;
-            __syncthreads();
-            int warp_off = 0, tile_total = 0;
-            for (int wq = 0; wq < kDetThreads / 32; ++wq) {
-                if (wq < ly0) warp_off += warp_tot[wq];
-                tile_total += warp_tot[wq];
-            }
-            const unsigned long long tile_off =
-                scan_exclusive(a.scan, t, (unsigned long long)tile_total, a.n_tiles, &off_s);
-            base = tile_off + warp_off + (incl - count);
-            if (threadIdx.x == 0 && (long long)(tile_off + tile_total) > a.cap)
-                atomicOr(a.err, a.raw_mode ? kErrCandidateCapacity : kErrKeypointCapacity);
         }
     }
+    int incl = count;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int nb = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lx >= d) incl += nb;
+    }
+    if (lx == 31) warp_tot[ly0] = incl;
+    __syncthreads();
+    int warp_off = 0, tile_total = 0;
+    for (int wq = 0; wq < kDetThreads / 32; ++wq) {
+        if (wq < ly0) warp_off += warp_tot[wq];
+        tile_total += warp_tot[wq];
+    }
+    const unsigned long long tile_off = scan_exclusive(a.scan, t, (unsigned long long)tile_total, a.n_tiles, &off_s);
+    if (threadIdx.x == 0 && (long long)(tile_off + tile_total) > a.cap) atomicOr(a.err, kErrCandidateCapacity);
+    unsigned long long slot = tile_off + warp_off + (incl - count);
+    while (hits) {
+        const int bit = __ffsll(hits) - 1;
+        hits &= hits - 1;
+        const int i = 1 + bit / (kDetTile / 8), q = bit % (kDetTile / 8);
+        const int ly = ly0 + 8 * q;
+        const int x = xs + lx, y = ys + ly;
+        if ((long long)slot < a.cap) {
+            DevCandidate c = {b, o, i, y, x, S(i, lx + 1, ly + 1) > 0.0f ? 1 : 0};
+            a.cand_out[slot] = c;
+        }
+        ++slot;
+    }
+}
+
+// K3 as its own pass: one thread per candidate (every lane busy, refinement
+// runs once), tiles of 256 candidates in ticket order; survivors are
+// compacted with a block scan + decoupled look-back, so they keep the
+// candidate order (detect.cpp:158-172) and the orientation stage only sees
+// real keypoints.  keep[c] (optional, stage API) records each verdict.
+__global__ void __launch_bounds__(256)
+refine_kernel(const __grid_constant__ DetectArgs a, const DevCandidate* __restrict__ cand,
+              const unsigned long long* n_cand, int* keep) {
+    __shared__ unsigned ticket_s;
+    __shared__ unsigned long long off_s;
+    __shared__ int warp_tot[8];
+    const long long n = (long long)*n_cand;
+    const unsigned n_tiles = (unsigned)((n + 255) / 256);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (;;) {
+        const unsigned t = scan_ticket(a.scan, &ticket_s);
+        if (t >= n_tiles) break;
+        const long long c = (long long)t * 256 + threadIdx.x;
+        DevKeypoint kp;
+        bool ok = false;
+        if (c < n) {
+            const DevCandidate e = cand[c];
+            ok = refine_candidate(a, e.image, e.octave, e.col, e.row, e.interval, &kp);
+            if (keep) keep[c] = ok ? 1 : 0;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) warp_tot[warp] = __popc(m);
+        __syncthreads();
+        int warp_off = 0, tile_total = 0;
+        for (int wq = 0; wq < 8; ++wq) {
+            if (wq < warp) warp_off += warp_tot[wq];
+            tile_total += warp_tot[wq];
+        }
+        const unsigned long long off = scan_exclusive(a.scan, t, (unsigned long long)tile_total, n_tiles, &off_s);
+        if (ok) {
+            const unsigned long long slot = off + warp_off + __popc(m & ((1u << lane) - 1u));
+            if ((long long)slot < a.cap) a.out[slot] = kp;
+        }
+        if (threadIdx.x == 0 && (long long)(off + tile_total) > a.cap) atomicOr(a.err, kErrKeypointCapacity);
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_refine(const DetectArgs& a, const DevCandidate* cand, const unsigned long long* n_cand,
+                          long long cap, int* keep, cudaStream_t st) {
+    const int grid = (int)std::max<long long>(1, std::min<long long>((cap + 255) / 256, 148 * 8));
+    refine_kernel<<<grid, 256, 0, st>>>(a, cand, n_cand, keep);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st) {

@@ -63,18 +63,23 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
     __shared__ unsigned ticket_s;
     __shared__ unsigned long long off_s;
 
-    const unsigned t = scan_ticket(a.scan, &ticket_s);
     const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
+    const unsigned n_tiles = (unsigned)((n + kOriTile - 1) / kOriTile);
+    // persistent: CTAs take ticket-ordered tiles until the device-side count
+    // is covered (no empty tiles, no capacity-sized grid)
+    for (;;) {
+    const unsigned t = scan_ticket(a.scan, &ticket_s);
+    if (t >= n_tiles) break;
     const long long k0 = (long long)t * kOriTile;
 
     for (int j = 0; j < kOriPerWarp; ++j) {
         const int slot = warp * kOriPerWarp + j;
         const long long k = k0 + slot;
-        if (k >= n) {
+        const DevKeypoint kp = a.kps[min(k, n - 1 >= 0 ? n - 1 : 0)];
+        if (k >= n || kp.octave < 0) {   // past the end, or a rejected candidate slot
             if (lane == 0) ncopy[slot] = 0;
             continue;
         }
-        const DevKeypoint kp = a.kps[k];
         const PyramidDesc& p = a.pyr;
         const OctaveDesc& od = p.oct[kp.octave];
         const double to_input = ldexp(1.0, kp.octave) * (p.upsampled ? 0.5 : 1.0);
@@ -208,12 +213,13 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
     }
     __syncthreads();
     const int tile_total = ncopy[2 * kOriTile];
-    const unsigned long long off = scan_exclusive(a.scan, t, (unsigned long long)tile_total, a.n_tiles, &off_s);
+    const unsigned long long off = scan_exclusive(a.scan, t, (unsigned long long)tile_total, n_tiles, &off_s);
     if (threadIdx.x == 0 && (long long)(off + tile_total) > a.cap) atomicOr(a.err, kErrOrientedCapacity);
     for (int slot = warp; slot < kOriTile; slot += kOriWarps) {
         const long long k = k0 + slot;
         if (k >= n) continue;
         const DevKeypoint kp = a.kps[k];
+        if (kp.octave < 0) continue;
         const int nc = ncopy[slot];
         const long long dst0 = (long long)off + ncopy[kOriTile + slot];
         for (int c = lane; c < nc; c += 32) {
@@ -222,6 +228,8 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
             cp.angle = ang[slot * bins + c];
             a.out[dst0 + c] = cp;
         }
+    }
+    __syncthreads();   // smem (ang, ncopy, ticket) is reused by the next tile
     }
 }
 
@@ -237,7 +245,13 @@ cudaError_t launch_orient(const OrientArgs& a, cudaStream_t st) {
     const size_t smem = orient_smem_bytes(a.bins, a.depth);
     cudaError_t e = cudaFuncSetAttribute(orient_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    orient_kernel<<<a.n_tiles, kOriWarps * 32, smem, st>>>(a);
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, orient_kernel, kOriWarps * 32, smem);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned grid = (unsigned)std::min<long long>((long long)a.n_tiles, (long long)sms * std::max(1, per_sm));
+    orient_kernel<<<std::max(1u, grid), kOriWarps * 32, smem, st>>>(a);
     return cudaGetLastError();
 }
 
