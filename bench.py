@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
+    ap.add_argument("--desc-kernel", type=int, default=2, help="certified descriptor kernel (A/B)")
     return ap.parse_args()
 
 
@@ -229,6 +230,7 @@ def run_ours(args, rank, local_rank, world):
     stream = torch.cuda.Stream()
     ex.set_stream(stream.cuda_stream)
     ex.set_profiling(True)
+    ex.set_desc_kernel(args.desc_kernel)
     imgs = torch.empty((B, H, W), dtype=torch.float32, device="cuda")
     ex.synth_value_noise(imgs.data_ptr(), B, W, H, SEED0 + rank * B, 5, cells_for(W))
     stream.synchronize()
@@ -255,6 +257,7 @@ def run_ours(args, rank, local_rank, world):
         t_end.record(stream)
         torch.cuda.synchronize()
     launches = ex.kernel_launches() - launches0
+    fallbacks = ex.exact_fallbacks()
     ms = t_start.elapsed_time(t_end)
     barrier()
     ms_max = max_over_ranks(ms)
@@ -331,7 +334,8 @@ def run_ours(args, rank, local_rank, world):
                      "kernel": "K5/K6 descriptor (dominant)",
                      "keypoints_per_s": kps_per_image * B / desc_s,
                      "lattice_points_per_s_est": kps_per_image * B * lattice_per_kp / desc_s,
-                     "share_of_step": stages["describe"] / max(1e-9, sum(stages.values()))}
+                     "share_of_step": stages["describe"] / max(1e-9, sum(stages.values())),
+                     "exact_fallbacks_last_step": fallbacks, "desc_kernel": args.desc_kernel}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

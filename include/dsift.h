@@ -161,6 +161,10 @@ int dsift_set_profiling(dsift_ctx* ctx, int on);
 /* Options: DSIFT_OPT_FORCE_EXACT = 1 routes every descriptor through the
  * exact scan-order kernel (test hook for the certified fast path). */
 #define DSIFT_OPT_FORCE_EXACT 1
+/* DSIFT_OPT_DESC_KERNEL selects the certified descriptor kernel: 2 (default)
+ * = band-streamed cell-lane kernel, 1 = the earlier item/run kernel.  Both are
+ * bit-identical to the reference; the option exists for A/B measurement. */
+#define DSIFT_OPT_DESC_KERNEL 2
 int dsift_set_option(dsift_ctx* ctx, int key, int64_t value);
 /* Statistics of the last synced result: DSIFT_STAT_EXACT_FALLBACKS = number
  * of keypoints whose descriptor the fast path could not certify. */

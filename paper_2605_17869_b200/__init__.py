@@ -280,6 +280,10 @@ class Extractor:
         """Route every descriptor through the exact scan-order kernel (test hook)."""
         _check(self.lib, self.lib.dsift_set_option(self.ctx, 1, int(on)))
 
+    def set_desc_kernel(self, which: int) -> None:
+        """Certified descriptor kernel: 2 = band-streamed cell-lane (default), 1 = earlier run kernel."""
+        _check(self.lib, self.lib.dsift_set_option(self.ctx, 2, int(which)))
+
     def exact_fallbacks(self) -> int:
         """Keypoints of the last result whose fast-path certificate failed."""
         return int(self.lib.dsift_stat(self.ctx, 1))

@@ -222,6 +222,7 @@ struct dsift_ctx {
     cudaEvent_t done = nullptr;
     bool profiling = false;
     int force_exact = 0;
+    int desc_kernel = 2;   // 2 = stream (cell-lane) certified kernel, 1 = previous fast kernel
     unsigned long long last_slow = 0;
     cudaEvent_t stage_ev[6] = {};
 };
@@ -529,13 +530,28 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
         const char* hp = std::getenv("DSIFT_HOT_PAIR");
         af.hot_pair = hp ? std::atoi(hp) : 1;
     }
-    const size_t smem_fast = describe_fast_smem_bytes(a.max_axis, af.chunk_rows, a.n_dsp);
+    {
+        double fmax = 0.0;
+        for (double f : fs) fmax = std::max(fmax, f);
+        af.max_span = 2 * (int)std::ceil(2.5 * 3.0 * fmax * smax) + 8;
+    }
     const size_t smem_exact = describe_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
-    if (smem_fast > 200 * 1024 || smem_exact > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
-    const int per_sm = std::max(1, describe_blocks_per_sm(smem_fast));
-    int grid = c->sm_count * per_sm;
-    if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
-    cuda_check(launch_describe_fast(af, grid, c->stream), "describe fast");
+    if (smem_exact > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
+    if (c->desc_kernel == 1) {   // previous certified kernel (kept for A/B measurements)
+        const size_t smem_fast = describe_fast_smem_bytes(a.max_axis, af.chunk_rows, a.n_dsp);
+        if (smem_fast > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
+        const int per_sm = std::max(1, describe_blocks_per_sm(smem_fast));
+        int grid = c->sm_count * per_sm;
+        if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
+        cuda_check(launch_describe_fast(af, grid, c->stream), "describe fast");
+    } else {
+        const size_t smem_s = describe_stream_smem_bytes(af.max_span, a.n_dsp);
+        if (smem_s > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
+        const int per_sm = std::max(1, describe_stream_blocks_per_sm(smem_s));
+        int grid = c->sm_count * per_sm;
+        if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
+        cuda_check(launch_describe_stream(af, grid, c->stream), "describe stream");
+    }
     DescArgs b = a;
     b.slow_list = c->slow.as<int>();
     b.n_slow = &ctr->n_slow;
@@ -1202,7 +1218,11 @@ int dsift_libm_probe(dsift_ctx* c, int mode, const void* in, int64_t n, void* ou
 int dsift_set_option(dsift_ctx* c, int key, int64_t value) {
     return guard([&] {
         if (!c) invalid("null context");
-        if (key == DSIFT_OPT_FORCE_EXACT) c->force_exact = value ? 1 : 0;
+        if (key == DSIFT_OPT_FORCE_EXACT) c->force_exact = value > 0 ? 1 : (int)value;   // < 0: diagnostics (-1 trust fast sums, -2 dump)
+        else if (key == DSIFT_OPT_DESC_KERNEL) {
+            if (value != 1 && value != 2) invalid("set_option: descriptor kernel must be 1 or 2");
+            c->desc_kernel = (int)value;
+        }
         else invalid("set_option: unknown key");
     });
 }

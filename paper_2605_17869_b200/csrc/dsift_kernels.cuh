@@ -82,6 +82,7 @@ struct DescArgs {
     long long slow_cap;
     int force_slow;        // test hook: fail every certificate
     int hot_pair;          // fast path: cache the (o0, o0+1) accumulators in registers
+    int max_span;          // stream kernel: table/ring width bound (in-range span + guards)
     float* desc;
     unsigned char* desc_u8;
     unsigned* err;
@@ -106,6 +107,9 @@ int describe_blocks_per_sm(size_t smem);
 cudaError_t launch_libm_probe(int mode, const void* in, long long n, void* out, cudaStream_t st);
 size_t describe_fast_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
 cudaError_t launch_describe_fast(const DescArgs& a, int grid, cudaStream_t st);
+size_t describe_stream_smem_bytes(int max_span, int n_dsp);
+int describe_stream_blocks_per_sm(size_t smem);
+cudaError_t launch_describe_stream(const DescArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev, long long n_host, double2* trig,
                         long long cap, cudaStream_t st);
 

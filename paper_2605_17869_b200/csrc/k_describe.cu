@@ -705,6 +705,436 @@ describe_fast_kernel(const __grid_constant__ DescArgs a) {
     }
 }
 
+// ------------------------------------------------------------------------------
+// Stream path (the production certified kernel): band-streamed, cell-lane.
+//
+// Per (keypoint, DSP scale) the in-range lattice (bins in (-1, 4) on both
+// axes, describe.cpp:84-87) splits into 5 x 5 cells (R, C) = (floor(vbin),
+// floor(ubin)).  Every point of cell (R, C) feeds exactly the bins
+// (R+ri, C+ci, o0+oi), ri, ci, oi in {0, 1} (describe.cpp:102-124).  The
+// lattice is processed in passes of whole cell-rows (<= 30 lattice rows):
+//   P1  bilinear samples of the pass rows + guard rows into a 32-row ring
+//       (rows shared with the previous pass are kept);
+//   P2  lane (cell, part) walks its share of the cell's points: gradient,
+//       sqrtf, glibc-exact atan2f, orientation bin, float(exp()) weight, the
+//       8 exact float leaves value*wr*wc*wo, each added in FP64 to the lane's
+//       private slot [ri][ci][o] in shared memory (no divergence, no atomics);
+//   P3  bin-owner threads fold the lane slots of the pass into their FP64 bin
+//       sum (fixed lane order), overlapped with the next pass's P1.
+// Each bin is then certified exactly like the fast path above (exact-span or
+// rounding-interval test against the reference's pairwise tree); keypoints
+// with an uncertified bin go to the exact kernel.
+// ------------------------------------------------------------------------------
+constexpr int kSRing = 32;                 // sample rows resident (power of two)
+constexpr int kSMaxPassRows = kSRing - 2;  // lattice rows per pass (+2 guard rows)
+constexpr int kSLanes = 125;               // accumulation lanes: 5 cells x 25 parts ... 25 x 5
+constexpr int kSSlotStride = 129;          // doubles per slot-entry row (spreads the fold over banks)
+constexpr int kSSlotE = 8 * kSSlotStride;  // stride between (ri, ci) groups
+
+struct StreamSmem {
+    double* ax;     // cx + cos*k        [span] indexed k - kA
+    double* cysu;   // cy + sin*k
+    double* sv;     // sin*k
+    double* cv;     // cos*k
+    double* q2;     // (k/bw)^2
+    double* slot;   // [32 entries (ri, ci, o)][kSSlotStride lanes]
+    float2* wp;     // (1 - frac, frac): weight of histogram index floor(bin) + {0, 1}
+    int* ew;        // min biased exponent (>= 1) of the nonzero weights in wp
+    float* ring;    // [kSRing][ring_pitch] bilinear samples, -1 = undefined
+    float* raw;     // [n_dsp][128]
+    int* lanelsb;   // [128] per-lane lower bound on the leaves' lowest-bit exponent (+531: sum of 4 biased exponents)
+    int* misc;      // [2][8]: kmin, kmax, start of cell c = -1..3 (double-buffered per scale)
+};
+
+// Biased exponent of x > 0 (floor(log2 x) + 127); denormals map to -22
+// (= -149 + 127, their smallest possible value).  For a chain of float
+// products leaf = fl(fl(fl(a*b)*c)*d) of positive factors, leaf >= 2^(sum of
+// floor(log2)) (rounding is monotone and 2^k is representable), so the leaf's
+// lowest bit is >= 2^(sum E - 23).
+__device__ __forceinline__ int efield1(float x) {
+    const int e = (int)((__float_as_uint(x) >> 23) & 0xffu);
+    return e ? e : -22;
+}
+
+__device__ __forceinline__ void stream_misc_init(int* misc) {
+    const int t = threadIdx.x;
+    if (t < 16) misc[t] = ((t & 7) == 1) ? -(1 << 30) : (1 << 30);
+}
+// Re-arm one misc buffer after its last read.  The buffer is next written two
+// scale calls later, with at least one CTA barrier in between.
+__device__ __forceinline__ void stream_misc_rearm(int* misc) {
+    const int t = threadIdx.x;
+    if (t < 8) misc[t] = (t == 1) ? -(1 << 30) : (1 << 30);
+}
+
+__device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const StreamSmem& S, const DevKeypoint& kp,
+                                                      double f, double cosa, double sina, float* raw_out,
+                                                      int ring_pitch, int* misc) {
+    const PyramidDesc& p = a.pyr;
+    const OctaveDesc& od = p.oct[kp.octave];
+    const double to_input = ldexp(1.0, kp.octave) * (p.upsampled ? 0.5 : 1.0);
+    const double cx = kp.x / to_input, cy = kp.y / to_input;
+    const double sigma_rel = kp.sigma / to_input;
+    const int lvl = nearest_level_d(p, f * sigma_rel);
+    const float* __restrict__ img =
+        od.gauss + (long long)kp.image * p.gauss_img_stride(kp.octave) + (long long)lvl * od.level_stride;
+    const int w = od.w, h = od.h, pitch = od.pitch;
+    const double bw = 3.0 * f * sigma_rel;
+    const int radius = (int)llround(bw * (kDescCells + 1) * 0.5 * 1.4142135623730951);
+    const int tid = threadIdx.x;
+    // table span [kA, kB] contains the in-range span and its guard entries
+    const double hb = 2.5 * bw;
+    const int kA = max(-radius - 1, (int)floor(-hb) - 3);
+    const int kB = min(radius + 1, (int)ceil(hb) + 3);
+    const int span = kB - kA + 1;
+    if (span > a.max_span) {   // host sized the tables from the largest sigma; never clip silently
+        if (tid == 0) atomicOr(a.err, kErrDescriptorLattice);
+        raw_out[tid] = 0.0f;
+        __syncthreads();
+        return true;
+    }
+    // ---- per-axis tables (describe.cpp:48-52, 72-73, 84-99 per-axis factors)
+    for (int i = tid; i < span; i += kDescThreads) {
+        const int k = kA + i;
+        const double q = D_DIV((double)k, bw);
+        const double bn = D_ADD(q, (double)(kDescCells / 2 - 0.5));
+        const int c = (int)floor(bn);
+        const float fr = (float)D_SUB(bn, (double)c);
+        const float gr = F_SUB(1.0f, fr);
+        S.q2[i] = D_MUL(q, q);
+        S.wp[i] = make_float2(gr, fr);
+        S.ew[i] = min(fr != 0.0f ? efield1(fr) : 255, gr != 0.0f ? efield1(gr) : 255);
+        S.ax[i] = D_ADD(cx, D_MUL(cosa, (double)k));
+        S.cysu[i] = D_ADD(cy, D_MUL(sina, (double)k));
+        S.sv[i] = D_MUL(sina, (double)k);
+        S.cv[i] = D_MUL(cosa, (double)k);
+        if (k >= -radius && k <= radius && bn > -1.0 && bn < (double)kDescCells) {
+            atomicMin(&misc[0], k);
+            atomicMax(&misc[1], k);
+            atomicMin(&misc[2 + (c + 1)], k);
+        }
+    }
+    __syncthreads();
+    const int kmin = misc[0], kmax = misc[1];
+    if (kmin > kmax) {   // no in-range lattice point: an all-zero histogram
+        raw_out[tid] = 0.0f;
+        __syncthreads();
+        stream_misc_rearm(misc);
+        return true;
+    }
+    int st[6];   // first lattice index of cell c = -1..3 at st[c + 1]; st[5] = kmax + 1
+    st[5] = kmax + 1;
+#pragma unroll
+    for (int c = 4; c >= 0; --c) st[c] = min(misc[2 + c], st[c + 1]);
+    int maxnc = 0;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) maxnc = max(maxnc, st[c + 1] - st[c]);
+    const int ub = kmin - 1;        // lattice index of ring column 0
+    const int sw = kmax - kmin + 3; // ring columns in use
+    const double wm1 = (double)(w - 1), hm1 = (double)(h - 1);
+    const int brow = tid >> 5, bcol = (tid >> 3) & 3, bori = tid & 7;
+
+    double binacc = 0.0;
+    int binlsb = 1 << 20;   // lowest-bit exponent bound of the bin's leaves, + 4*127 + 23
+    int kchain = 0;         // longest in-lane addition chain of any pass
+    int npass = 0;
+    int pRa = 0, pRb = -1, pP = 1;
+    bool pending = false;
+    int R = -1, sub = 0, have_hi = kmin - 3;
+    while (true) {
+        const bool have = R <= 3;
+        int Ra = 0, Rb = -1, va = 0, vb = -1, P = 1;
+        if (have) {
+            const int rows = st[R + 2] - st[R + 1];
+            if (sub > 0 || rows > kSMaxPassRows) {   // a cell-row taller than a pass: equal row splits
+                const int nsplit = (rows + kSMaxPassRows - 1) / kSMaxPassRows;
+                const int chunk = (rows + nsplit - 1) / nsplit;
+                va = st[R + 1] + sub * chunk;
+                vb = min(va + chunk, st[R + 2]) - 1;
+                Ra = Rb = R;
+                if (++sub == nsplit) {
+                    sub = 0;
+                    ++R;
+                }
+            } else {                                 // whole cell-rows while they fit
+                Ra = R;
+                int tot = rows;
+                ++R;
+                while (R <= 3) {
+                    const int rr = st[R + 2] - st[R + 1];
+                    if (rr > kSMaxPassRows || tot + rr > kSMaxPassRows) break;
+                    tot += rr;
+                    ++R;
+                }
+                Rb = R - 1;
+                va = st[Ra + 1];
+                vb = st[Rb + 2] - 1;
+            }
+            P = kSLanes / ((Rb - Ra + 1) * 5);
+            // P1: samples of rows [va-1, vb+1] not yet in the ring (describe.cpp:56-65)
+            const int s0 = max(va - 1, have_hi + 1), s1 = vb + 1;
+            if (s1 >= s0) {
+                // two samples per thread per iteration, branch-free (the loads of
+                // both are in flight together); out-of-image samples read a
+                // clamped pixel and are replaced by kUndef
+                const float inv_sw = 1.0f / (float)sw;   // exact row split for idx < 2^16
+                const int ns = (s1 - s0 + 1) * sw;
+                for (int idx = tid; idx < ns; idx += 2 * kDescThreads) {
+                    int off[2], slot[2];
+                    float fx[2], fy[2];
+                    bool inb[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int id = min(idx + j * kDescThreads, ns - 1);
+                        const int rr = (int)(((float)id + 0.5f) * inv_sw), cc = id - rr * sw;
+                        const int vv = s0 + rr, u = ub + cc;
+                        const double px = D_SUB(S.ax[u - kA], S.sv[vv - kA]);
+                        const double py = D_ADD(S.cysu[u - kA], S.cv[vv - kA]);
+                        inb[j] = !(px < 0.0 || px > wm1 || py < 0.0 || py > hm1);
+                        // sample_bilinear (describe.cpp:17-29); the clamp at 0 only
+                        // affects samples that are discarded
+                        const int ix = min(max((int)floor(px), 0), w - 2);
+                        const int iy = min(max((int)floor(py), 0), h - 2);
+                        fx[j] = (float)D_SUB(px, (double)ix);
+                        fy[j] = (float)D_SUB(py, (double)iy);
+                        off[j] = iy * pitch + ix;
+                        slot[j] = (vv & (kSRing - 1)) * ring_pitch + cc;
+                    }
+                    float v00[2], v10[2], v01[2], v11[2];
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const float* r0 = img + off[j];
+                        v00[j] = __ldg(r0);
+                        v10[j] = __ldg(r0 + 1);
+                        v01[j] = __ldg(r0 + pitch);
+                        v11[j] = __ldg(r0 + pitch + 1);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const float top = F_ADD(v00[j], F_MUL(fx[j], F_SUB(v10[j], v00[j])));
+                        const float bot = F_ADD(v01[j], F_MUL(fx[j], F_SUB(v11[j], v01[j])));
+                        const float sv = F_ADD(top, F_MUL(fy[j], F_SUB(bot, top)));
+                        if (idx + j * kDescThreads < ns) S.ring[slot[j]] = inb[j] ? sv : kUndef;
+                    }
+                }
+                have_hi = s1;
+            }
+        }
+        if (pending) {   // P3 of the previous pass: fold the lane slots into this thread's bin
+            double se = 0.0, so = 0.0;
+            int lm = 1 << 20;
+#pragma unroll
+            for (int dr = 0; dr < 2; ++dr) {
+                const int Rc = brow - 1 + dr;          // ri = 1 - dr
+                if (Rc < pRa || Rc > pRb) continue;
+#pragma unroll
+                for (int dc = 0; dc < 2; ++dc) {
+                    const int Cc = bcol - 1 + dc;      // ci = 1 - dc
+                    const int cell = (Rc - pRa) * 5 + (Cc + 1);
+                    const int e = ((1 - dr) * 2 + (1 - dc)) * 8 + bori;
+                    const double* sp = S.slot + e * kSSlotStride + cell * pP;
+                    const int* lp = S.lanelsb + cell * pP;
+                    int q = 0;
+                    for (; q + 1 < pP; q += 2) {
+                        se = se + sp[q];
+                        so = so + sp[q + 1];
+                        lm = min(lm, min(lp[q], lp[q + 1]));
+                    }
+                    if (q < pP) {
+                        se = se + sp[q];
+                        lm = min(lm, lp[q]);
+                    }
+                }
+            }
+            binacc = binacc + (se + so);
+            binlsb = min(binlsb, lm);
+        }
+        __syncthreads();
+        if (!have) break;
+        // P2: lane (cell, part) over its share of the cell's points
+        {
+            const int ncells = (Rb - Ra + 1) * 5;
+            const int cell = tid / P, part = tid - cell * P;
+            int npts = 0, nc = 1, rv0 = 0, cu0 = 0;
+            if (cell < ncells) {
+                const int Rl = Ra + cell / 5, Cl = cell % 5 - 1;
+                const int r0 = max(va, st[Rl + 1]), r1 = min(vb, st[Rl + 2] - 1);
+                cu0 = st[Cl + 1];
+                nc = st[Cl + 2] - cu0;
+                rv0 = r0;
+                if (r1 >= r0 && nc > 0) npts = (r1 - r0 + 1) * nc;
+            }
+            double* my = S.slot + tid;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) my[e * kSSlotStride] = 0.0;
+            int lmin = 1 << 20;
+            const float inv_nc = 1.0f / (float)max(nc, 1);
+            for (int pi = part; pi < npts; pi += P) {
+                const int rr = (int)(((float)pi + 0.5f) * inv_nc), cc = pi - rr * nc;
+                const int v = rv0 + rr, u = cu0 + cc;
+                const int col = u - ub;
+                const float* mid = S.ring + (v & (kSRing - 1)) * ring_pitch + col;
+                const float left = mid[-1], right = mid[1];
+                const float up = S.ring[((v - 1) & (kSRing - 1)) * ring_pitch + col];
+                const float down = S.ring[((v + 1) & (kSRing - 1)) * ring_pitch + col];
+                if (left == kUndef || right == kUndef || up == kUndef || down == kUndef) continue;
+                // describe.cpp:89-100
+                const float du = F_MUL(0.5f, F_SUB(right, left));
+                const float dv = F_MUL(0.5f, F_SUB(down, up));
+                const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
+                float theta = dsift_atan2f(dv, du);
+                if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
+                if (isnan(theta)) {   // reference: negative bin -> std::out_of_range
+                    atomicOr(a.err, kErrHistogramRange);
+                    theta = 0.0f;
+                }
+                double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
+                if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
+                const double arg = D_MUL(-D_ADD(S.q2[u - kA], S.q2[v - kA]), 0.125);
+                const float val = F_MUL(mag, (float)dsift_exp(arg));
+                const int o0 = (int)floor(obin);
+                const float fo = (float)D_SUB(obin, (double)o0);
+                const float go = F_SUB(1.0f, fo);
+                // leaves value*wr*wc*wo (describe.cpp:102-124), FP64 slot accumulation
+                const float2 wr = S.wp[v - kA], wc = S.wp[u - kA];
+                const float a0 = F_MUL(val, wr.x), a1 = F_MUL(val, wr.y);
+                const float t00 = F_MUL(a0, wc.x), t01 = F_MUL(a0, wc.y);
+                const float t10 = F_MUL(a1, wc.x), t11 = F_MUL(a1, wc.y);
+                double* pa = my + (o0 & 7) * kSSlotStride;
+                double* pb = my + ((o0 + 1) & 7) * kSSlotStride;
+                double x0 = pa[0], x1 = pb[0], x2 = pa[kSSlotE], x3 = pb[kSSlotE];
+                double x4 = pa[2 * kSSlotE], x5 = pb[2 * kSSlotE], x6 = pa[3 * kSSlotE], x7 = pb[3 * kSSlotE];
+                x0 = x0 + (double)F_MUL(t00, go);
+                x1 = x1 + (double)F_MUL(t00, fo);
+                x2 = x2 + (double)F_MUL(t01, go);
+                x3 = x3 + (double)F_MUL(t01, fo);
+                x4 = x4 + (double)F_MUL(t10, go);
+                x5 = x5 + (double)F_MUL(t10, fo);
+                x6 = x6 + (double)F_MUL(t11, go);
+                x7 = x7 + (double)F_MUL(t11, fo);
+                pa[0] = x0;
+                pb[0] = x1;
+                pa[kSSlotE] = x2;
+                pb[kSSlotE] = x3;
+                pa[2 * kSSlotE] = x4;
+                pb[2 * kSSlotE] = x5;
+                pa[3 * kSSlotE] = x6;
+                pb[3 * kSSlotE] = x7;
+                if (val > 0.0f) {
+                    // lowest nonzero orientation weight: min(fo, 1-fo), or ~1 (>= 2^-1) if one is 0
+                    const float mo = fminf(fo, go);
+                    const int eo = mo > 0.0f ? efield1(mo) : 126;
+                    lmin = min(lmin, efield1(val) + eo + S.ew[v - kA] + S.ew[u - kA]);
+                }
+            }
+            S.lanelsb[tid] = lmin;
+        }
+        kchain = max(kchain, ((vb - va + 1) * maxnc + P - 1) / P);
+        ++npass;
+        __syncthreads();
+        pending = true;
+        pRa = Ra;
+        pRb = Rb;
+        pP = P;
+    }
+    stream_misc_rearm(misc);   // every thread read misc before the pass barriers
+    // certificate (see the fast path): chain <= kchain in a lane slot, <= 51 in
+    // the fold, <= npass across passes; the reference tree is <= 13 deep
+    bool ok;
+    float res;
+    const int top = (int)((__double_as_longlong(binacc) >> 52) & 0x7ff) - 1023;
+    if (binacc == 0.0 || top - (binlsb - 4 * 127 - 23) <= 52) {
+        ok = true;
+        res = __double2float_rn(binacc);
+    } else {
+        const double e = (double)(kchain + npass + 51 + 13 + 64) * 0x1p-53;
+        const double lo = binacc * (1.0 - e), hi = binacc * (1.0 + e);
+        const float flo = __double2float_rn(lo), fhi = __double2float_rn(hi);
+        ok = (flo == fhi);
+        res = flo;
+    }
+    raw_out[tid] = res;
+    if (a.force_slow == -2) {   // diagnostic dump (block 0, keypoint 0): rows fi*4 + field
+        const int fi = (int)(raw_out - S.raw) / kDescDim;
+        a.desc[(fi * 4 + 0) * kDescDim + tid] = (float)binacc;
+        a.desc[(fi * 4 + 1) * kDescDim + tid] = (float)(binlsb - 4 * 127 - 23);
+        a.desc[(fi * 4 + 2) * kDescDim + tid] = (float)(kchain * 1000 + npass);
+        a.desc[(fi * 4 + 3) * kDescDim + tid] = ok ? 1.0f : 0.0f;
+    }
+    if (a.force_slow < 0) return true;   // diagnostic: trust the fast sums unconditionally
+    return ok && !a.force_slow;
+}
+
+__global__ void __launch_bounds__(kDescThreads, 4)
+describe_stream_kernel(const __grid_constant__ DescArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ double red[4];
+    __shared__ int misc[16];
+    const int SP = a.max_span;
+    const int RP = (SP + 1) & ~1;
+    StreamSmem S;
+    unsigned char* pbuf = sm;
+    S.ax = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
+    S.cysu = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
+    S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
+    S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
+    S.q2 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
+    S.slot = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * 32 * kSSlotStride;
+    S.wp = reinterpret_cast<float2*>(pbuf); pbuf += sizeof(float2) * SP;
+    S.ew = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * SP;
+    S.ring = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kSRing * RP;
+    S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * a.n_dsp;
+    S.lanelsb = reinterpret_cast<int*>(pbuf);
+    S.misc = misc;
+    stream_misc_init(misc);
+    __syncthreads();
+
+    const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
+    const int tid = threadIdx.x;
+    int call = 0;
+    for (long long k = blockIdx.x; k < (a.force_slow == -2 ? (blockIdx.x == 0 ? 1 : 0) : n); k += gridDim.x) {
+        const DevKeypoint kp = a.kps[k];
+        const double2 cs = a.trig[k];
+        bool ok = true;
+        for (int fi = 0; fi < a.n_dsp; ++fi, ++call)
+            ok &= raw_descriptor_stream(a, S, kp, a.dsp[fi], cs.x, cs.y, S.raw + fi * kDescDim, RP,
+                                        misc + 8 * (call & 1));
+        const bool all_ok = __syncthreads_and(ok);
+        if (!all_ok) {
+            if (tid == 0) {
+                const unsigned slot = atomicAdd(a.slow_count, 1u);
+                if ((long long)slot < a.slow_cap) a.slow_out[slot] = (int)k;
+                else atomicOr(a.err, kErrDescriptorLattice);
+            }
+            continue;   // the exact kernel writes this keypoint's descriptor
+        }
+        if (a.force_slow != -2) dsp_epilogue(a, S.raw, k, red);
+        __syncthreads();
+    }
+}
+
+size_t describe_stream_smem_bytes(int max_span, int n_dsp) {
+    const size_t SP = (size_t)max_span, RP = (SP + 1) & ~(size_t)1;
+    return sizeof(double) * 5 * SP + sizeof(double) * 32 * kSSlotStride + sizeof(float2) * SP + sizeof(int) * SP +
+           sizeof(float) * kSRing * RP + sizeof(float) * kDescDim * n_dsp + sizeof(int) * kDescThreads;
+}
+
+int describe_stream_blocks_per_sm(size_t smem) {
+    cudaFuncSetAttribute(describe_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, describe_stream_kernel, kDescThreads, smem) != cudaSuccess)
+        n = 1;
+    return n;
+}
+
+cudaError_t launch_describe_stream(const DescArgs& a, int grid, cudaStream_t st) {
+    const size_t smem = describe_stream_smem_bytes(a.max_span, a.n_dsp);
+    cudaError_t e = cudaFuncSetAttribute(describe_stream_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    describe_stream_kernel<<<grid, kDescThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
 size_t describe_smem_bytes(int max_axis, int chunk_rows, int n_dsp) {
     const size_t A = (size_t)max_axis;
     const size_t PW = ((A + 31) / 32) * 32, NW = PW / 32;

@@ -161,11 +161,15 @@ def test_determinism_batch_single_and_exact_path(port):
         for i in range(4):
             ex.extract(imgs[i])
             singles.append(ex.sha256(0))
+        ex.set_desc_kernel(1)
+        ex.extract_batch(imgs)
+        h4 = [ex.sha256(i) for i in range(4)]
+        ex.set_desc_kernel(2)
         ex.set_force_exact(True)
         ex.extract_batch(imgs)
         h3 = [ex.sha256(i) for i in range(4)]
         assert ex.exact_fallbacks() > 0
-    assert h1 == h2 == singles == h3
+    assert h1 == h2 == singles == h3 == h4
     for i in range(4):
         k, d = port.extract(imgs[i])
         assert port.hash_features(k, d) == h1[i]
@@ -261,7 +265,9 @@ def test_c3_full_size_properties_and_sampled_parity(port):
         shas = [ex.sha256(i) for i in range(2)]
         ex.extract_batch(imgs)
         assert shas == [ex.sha256(i) for i in range(2)]
-        assert ex.exact_fallbacks() < 50
+        # certificate failures (exact midpoint sums the lane-level lowest-bit
+        # bound cannot prove exact) go to the exact kernel: a small fraction
+        assert ex.exact_fallbacks() <= 0.005 * len(res[0]) * 2
     fs = res[0]
     assert 10000 < len(fs) < 25000
     k = fs.keypoints
