@@ -767,6 +767,14 @@ __device__ __forceinline__ void stream_misc_rearm(int* misc) {
     if (t < 8) misc[t] = (t == 1) ? -(1 << 30) : (1 << 30);
 }
 
+// a[i] for a register array indexed by a runtime value (select chain, no local memory)
+__device__ __forceinline__ int pick6(const int (&v)[6], int i) {
+    int r = v[0];
+#pragma unroll
+    for (int k = 1; k < 6; ++k) r = (i == k) ? v[k] : r;
+    return r;
+}
+
 __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const StreamSmem& S, const DevKeypoint& kp,
                                                       double f, double cosa, double sina, float* raw_out,
                                                       int ring_pitch, int* misc) {
@@ -822,7 +830,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         stream_misc_rearm(misc);
         return true;
     }
-    int st[6];   // first lattice index of cell c = -1..3 at st[c + 1]; st[5] = kmax + 1
+    int st[6];   // first lattice index of cell c = -1..3 at st[c + 1]; st[5] = kmax + 1 (registers, read via pick6)
     st[5] = kmax + 1;
 #pragma unroll
     for (int c = 4; c >= 0; --c) st[c] = min(misc[2 + c], st[c + 1]);
@@ -845,12 +853,12 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         const bool have = R <= 3;
         int Ra = 0, Rb = -1, va = 0, vb = -1, P = 1;
         if (have) {
-            const int rows = st[R + 2] - st[R + 1];
+            const int rows = pick6(st, R + 2) - pick6(st, R + 1);
             if (sub > 0 || rows > kSMaxPassRows) {   // a cell-row taller than a pass: equal row splits
                 const int nsplit = (rows + kSMaxPassRows - 1) / kSMaxPassRows;
                 const int chunk = (rows + nsplit - 1) / nsplit;
-                va = st[R + 1] + sub * chunk;
-                vb = min(va + chunk, st[R + 2]) - 1;
+                va = pick6(st, R + 1) + sub * chunk;
+                vb = min(va + chunk, pick6(st, R + 2)) - 1;
                 Ra = Rb = R;
                 if (++sub == nsplit) {
                     sub = 0;
@@ -861,14 +869,14 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 int tot = rows;
                 ++R;
                 while (R <= 3) {
-                    const int rr = st[R + 2] - st[R + 1];
+                    const int rr = pick6(st, R + 2) - pick6(st, R + 1);
                     if (rr > kSMaxPassRows || tot + rr > kSMaxPassRows) break;
                     tot += rr;
                     ++R;
                 }
                 Rb = R - 1;
-                va = st[Ra + 1];
-                vb = st[Rb + 2] - 1;
+                va = pick6(st, Ra + 1);
+                vb = pick6(st, Rb + 2) - 1;
             }
             P = kSLanes / ((Rb - Ra + 1) * 5);
             // P1: samples of rows [va-1, vb+1] not yet in the ring (describe.cpp:56-65)
@@ -958,9 +966,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
             int npts = 0, nc = 1, rv0 = 0, cu0 = 0;
             if (cell < ncells) {
                 const int Rl = Ra + cell / 5, Cl = cell % 5 - 1;
-                const int r0 = max(va, st[Rl + 1]), r1 = min(vb, st[Rl + 2] - 1);
-                cu0 = st[Cl + 1];
-                nc = st[Cl + 2] - cu0;
+                const int r0 = max(va, pick6(st, Rl + 1)), r1 = min(vb, pick6(st, Rl + 2) - 1);
+                cu0 = pick6(st, Cl + 1);
+                nc = pick6(st, Cl + 2) - cu0;
                 rv0 = r0;
                 if (r1 >= r0 && nc > 0) npts = (r1 - r0 + 1) * nc;
             }
@@ -991,7 +999,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
                 if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
                 const double arg = D_MUL(-D_ADD(S.q2[u - kA], S.q2[v - kA]), 0.125);
-                const float val = F_MUL(mag, (float)dsift_exp(arg));
+                const float val = F_MUL(mag, (float)dsift_exp_mid(arg));
                 const int o0 = (int)floor(obin);
                 const float fo = (float)D_SUB(obin, (double)o0);
                 const float go = F_SUB(1.0f, fo);

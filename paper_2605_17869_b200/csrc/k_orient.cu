@@ -121,7 +121,7 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 if (bin >= bins) bin -= bins;
                 const double ddx = D_SUB((double)x, cx), ddy = D_SUB((double)y, cy);
                 const double arg = D_DIV(-D_ADD(D_MUL(ddx, ddx), D_MUL(ddy, ddy)), denom);
-                const float wgt = (float)dsift_exp(arg);
+                const float wgt = (float)dsift_exp_mid(arg);
                 val = F_MUL(mag, wgt);
             }
             const unsigned grp = __match_any_sync(0xffffffffu, bin);

@@ -33,7 +33,8 @@ def test_atan2f_bit_exact(lc, mode, n):
 
 
 @pytest.mark.parametrize("lo,hi,mode", [(-10.0, 0.0, 0), (-1.6, 0.0, 1), (-745.2, 709.8, 0),
-                                        (-1e-12, 1e-12, 0), (-760.0, -700.0, 0)])
+                                        (-1e-12, 1e-12, 0), (-1e-15, 1e-15, 0), (-760.0, -700.0, 0),
+                                        (-511.9, 511.9, 0)])
 def test_exp_bit_exact(lc, lo, hi, mode):
     first = (C.c_double * 2)()
     bad = lc.lc_exp_mismatch(777, 4_000_000, lo, hi, mode, first)
