@@ -193,7 +193,7 @@ struct Counters {          // one small device block, cleared per batch
     unsigned ori_ticket;
     unsigned n_slow;      // keypoints the certified fast descriptor path handed to the exact kernel
     unsigned ref_ticket;
-    unsigned pad2;
+    unsigned n_fixed;     // (keypoint, scale) pairs the stream kernel recomputed exactly in place
     unsigned long long n_kp;   // refined keypoints (compacted)
 };
 
@@ -522,6 +522,7 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
     Counters* ctr = counters(c);
     a.slow_out = c->slow.as<int>();
     a.slow_count = &ctr->n_slow;
+    a.fix_count = &ctr->n_fixed;
     a.slow_cap = cap_n;
     a.force_slow = c->force_exact;
     DescArgs af = a;
@@ -545,7 +546,8 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
         if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
         cuda_check(launch_describe_fast(af, grid, c->stream), "describe fast");
     } else {
-        const size_t smem_s = describe_stream_smem_bytes(af.max_span, a.n_dsp);
+        const size_t smem_s = std::max(describe_stream_smem_bytes(af.max_span, a.n_dsp),
+                                       describe_stream_exact_smem_bytes(af.max_axis, af.chunk_rows, a.n_dsp));
         if (smem_s > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
         const int per_sm = std::max(1, describe_stream_blocks_per_sm(smem_s));
         int grid = c->sm_count * per_sm;
@@ -655,7 +657,7 @@ static void result_sync(dsift_ctx* c) {
         throw Error{DSIFT_ECAPACITY, m};
     }
     c->total = (int64_t)h.n_ori;
-    c->last_slow = h.n_slow;
+    c->last_slow = (unsigned long long)h.n_slow + h.n_fixed;
     c->h_offsets.assign(c->batch + 1, 0);
     cuda_check(cudaMemcpy(c->h_offsets.data(), c->offsets.as<void>(), sizeof(long long) * (c->batch + 1),
                           cudaMemcpyDeviceToHost), "D2H");

@@ -79,6 +79,7 @@ struct DescArgs {
     const unsigned* n_slow;
     int* slow_out;         // fast kernel: keypoints it could not certify
     unsigned* slow_count;
+    unsigned* fix_count;   // stream kernel: (keypoint, scale) pairs recomputed exactly in place
     long long slow_cap;
     int force_slow;        // test hook: fail every certificate
     int hot_pair;          // fast path: cache the (o0, o0+1) accumulators in registers
@@ -108,6 +109,7 @@ cudaError_t launch_libm_probe(int mode, const void* in, long long n, void* out, 
 size_t describe_fast_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
 cudaError_t launch_describe_fast(const DescArgs& a, int grid, cudaStream_t st);
 size_t describe_stream_smem_bytes(int max_span, int n_dsp);
+size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
 int describe_stream_blocks_per_sm(size_t smem);
 cudaError_t launch_describe_stream(const DescArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev, long long n_host, double2* trig,

@@ -335,17 +335,13 @@ __device__ __forceinline__ void dsp_epilogue(const DescArgs& a, const float* raw
     }
 }
 
-// Exact path: per-bin scan-order trees (bit-identical by construction).  Runs
-// over all keypoints in stage mode, and over the keypoints the fast path
-// could not certify in the hot path.
-__global__ void __launch_bounds__(kDescThreads, 4)
-describe_exact_kernel(const __grid_constant__ DescArgs a) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ double red[4];
+// Shared-memory carve of the exact path: raw[nraw][128] first, then the
+// per-scale working set (whose size exact_work_bytes reports).
+__device__ __forceinline__ DescSmem carve_exact_smem(unsigned char* pbuf, const DescArgs& a, int nraw) {
     const int A = a.max_axis;
     const int PW = ((A + 31) >> 5) << 5;
     DescSmem S;
-    unsigned char* pbuf = sm;
+    S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * nraw;
     S.q2 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
     S.bin = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
     S.ax = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
@@ -354,7 +350,6 @@ describe_exact_kernel(const __grid_constant__ DescArgs a) {
     S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
     S.frac = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * A;
     S.c0 = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * A;
-    S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * (a.raw_mode ? 1 : a.n_dsp);
     S.samp = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * (a.chunk_rows + 2) * A;
     S.pval = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * PW;
     S.pfo = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * PW;
@@ -362,6 +357,17 @@ describe_exact_kernel(const __grid_constant__ DescArgs a) {
     pbuf = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(pbuf) + 15) & ~size_t(15));
     S.node = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * (kTreeDepth - 3) * kDescThreads;
     S.ring = reinterpret_cast<float*>(pbuf);
+    return S;
+}
+
+// Exact path: per-bin scan-order trees (bit-identical by construction).  Runs
+// over all keypoints in stage mode, and over the keypoints the fast path
+// could not certify in the hot path.
+__global__ void __launch_bounds__(kDescThreads, 4)
+describe_exact_kernel(const __grid_constant__ DescArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    __shared__ double red[4];
+    DescSmem S = carve_exact_smem(sm, a, a.raw_mode ? 1 : a.n_dsp);
 
     const long long n = a.slow_list ? (long long)*a.n_slow : (a.n_host >= 0 ? a.n_host : (long long)*a.n_dev);
     const int tid = threadIdx.x;
@@ -1079,9 +1085,10 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     __shared__ double red[4];
     __shared__ int misc[16];
     const int SP = a.max_span;
-    const int RP = (SP + 1) & ~1;
+    const int RP = (SP - 6) & ~1;   // >= the widest ring row 2*ceil(2.5 bw) + 1 (host: SP = that + 7)
     StreamSmem S;
     unsigned char* pbuf = sm;
+    S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * a.n_dsp;
     S.ax = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.cysu = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
@@ -1091,7 +1098,6 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     S.wp = reinterpret_cast<float2*>(pbuf); pbuf += sizeof(float2) * SP;
     S.ew = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * SP;
     S.ring = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kSRing * RP;
-    S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * a.n_dsp;
     S.lanelsb = reinterpret_cast<int*>(pbuf);
     S.misc = misc;
     stream_misc_init(misc);
@@ -1103,11 +1109,22 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     for (long long k = blockIdx.x; k < (a.force_slow == -2 ? (blockIdx.x == 0 ? 1 : 0) : n); k += gridDim.x) {
         const DevKeypoint kp = a.kps[k];
         const double2 cs = a.trig[k];
-        bool ok = true;
-        for (int fi = 0; fi < a.n_dsp; ++fi, ++call)
-            ok &= raw_descriptor_stream(a, S, kp, a.dsp[fi], cs.x, cs.y, S.raw + fi * kDescDim, RP,
-                                        misc + 8 * (call & 1));
-        const bool all_ok = __syncthreads_and(ok);
+        bool all_ok = true;
+        for (int fi = 0; fi < a.n_dsp; ++fi, ++call) {
+            const bool ok = raw_descriptor_stream(a, S, kp, a.dsp[fi], cs.x, cs.y, S.raw + fi * kDescDim, RP,
+                                                  misc + 8 * (call & 1));
+            const bool sok = __syncthreads_and(ok);
+            if (!sok && a.force_slow == 0) {
+                // a bin the certificate could not prove: recompute this scale with
+                // the exact scan-order trees, in place (the stream working set is
+                // dead; the exact working set aliases it, raw[] is kept)
+                const DescSmem E = carve_exact_smem(sm, a, a.n_dsp);
+                raw_descriptor_cta(a, E, kp, a.dsp[fi], cs.x, cs.y, S.raw + fi * kDescDim);
+                if (tid == 0 && a.fix_count) atomicAdd(a.fix_count, 1u);
+            } else {
+                all_ok &= sok;
+            }
+        }
         if (!all_ok) {
             if (tid == 0) {
                 const unsigned slot = atomicAdd(a.slow_count, 1u);
@@ -1121,8 +1138,18 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     }
 }
 
+size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp) {
+    // carve_exact_smem: raw + working set (+16 alignment slack)
+    const size_t A = (size_t)max_axis;
+    const size_t PW = ((A + 31) / 32) * 32, NW = PW / 32;
+    return sizeof(float) * kDescDim * n_dsp + sizeof(double) * 6 * A + sizeof(float) * A + sizeof(int) * A +
+           sizeof(float) * (chunk_rows + 2) * A + sizeof(float) * 2 * chunk_rows * PW +
+           sizeof(unsigned) * chunk_rows * kDescOrients * NW + 16 + sizeof(double) * (kTreeDepth - 3) * kDescThreads +
+           sizeof(float) * kRing * kDescThreads;
+}
+
 size_t describe_stream_smem_bytes(int max_span, int n_dsp) {
-    const size_t SP = (size_t)max_span, RP = (SP + 1) & ~(size_t)1;
+    const size_t SP = (size_t)max_span, RP = (SP - 6) & ~(size_t)1;
     return sizeof(double) * 5 * SP + sizeof(double) * 32 * kSSlotStride + sizeof(float2) * SP + sizeof(int) * SP +
            sizeof(float) * kSRing * RP + sizeof(float) * kDescDim * n_dsp + sizeof(int) * kDescThreads;
 }
