@@ -210,6 +210,7 @@ struct dsift_ctx {
     Plan plan;
     int batch = 0;            // images in the current pyramid / result
     PyramidDesc pyr{};
+    DevBuf det_aux;
     DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
         pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow,
         ref_states, keep;
@@ -376,11 +377,6 @@ static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
     a.cap = cap;
     Counters* ctr = counters(c);
     a.err = &ctr->err;
-    c->det_states.ensure(sizeof(unsigned long long) * (size_t)std::max(1u, a.n_tiles));
-    cuda_check(cudaMemsetAsync(c->det_states.as<void>(), 0, sizeof(unsigned long long) * std::max(1u, a.n_tiles),
-                               c->stream), "memset");
-    a.scan.states = c->det_states.as<unsigned long long>();
-    a.scan.ticket = &ctr->det_ticket;
     a.scan.total = &ctr->n_det;
     a.scan.cap = (unsigned long long)cap;
     if (raw_mode) {
@@ -389,8 +385,20 @@ static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
     } else {
         a.cand_out = nullptr;
     }
+    {   // count -> scan -> emit scratch: masks, counts, offsets, CUB temp
+        const size_t nt = std::max(1u, a.n_tiles);
+        const size_t masks = (sizeof(unsigned short) * 256 * nt + 255) & ~size_t(255);
+        const size_t cnts = (sizeof(unsigned) * nt + 255) & ~size_t(255);
+        a.scan_temp_bytes = detect_scan_temp_bytes(a.n_tiles);
+        c->det_aux.ensure(masks + 2 * cnts + a.scan_temp_bytes + 256);
+        char* base = c->det_aux.as<char>();
+        a.hit_masks = reinterpret_cast<unsigned short*>(base);
+        a.tile_counts = reinterpret_cast<unsigned*>(base + masks);
+        a.tile_offsets = reinterpret_cast<unsigned*>(base + masks + cnts);
+        a.scan_temp = base + masks + 2 * cnts;
+    }
     cuda_check(launch_detect(a, c->stream), "detect");
-    ++c->launches;
+    c->launches += 3;
 }
 
 // K3: refine the compacted candidates (count n_det) into compacted keypoints

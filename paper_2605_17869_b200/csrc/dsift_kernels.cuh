@@ -39,7 +39,14 @@ struct DetectArgs {
     long long cap;
     unsigned* err;
     ScanState scan;
+    // count -> scan -> emit compaction of the extrema (no cross-tile waiting)
+    unsigned short* hit_masks;   // [n_tiles][256] per-thread (level, row) hit bits
+    unsigned* tile_counts;       // [n_tiles]
+    unsigned* tile_offsets;      // [n_tiles] exclusive scan of tile_counts
+    void* scan_temp;
+    size_t scan_temp_bytes;
 };
+size_t detect_scan_temp_bytes(unsigned n_tiles);
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st);
 cudaError_t launch_refine(const DetectArgs& a, const DevCandidate* cand, const unsigned long long* n_cand,
                           long long cap, int* keep, cudaStream_t st);

@@ -10,6 +10,7 @@
 // scan plus a decoupled look-back over ticket-ordered tiles.  Output order is
 // (image, octave, tile, thread, level, row) — fixed by construction, no
 // atomics on order; canonical order is restored later by the sort (K7).
+#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include "dsift_common.cuh"
@@ -87,14 +88,14 @@ __device__ bool refine_candidate(const DetectArgs& a, int b, int o, int x, int y
     return true;
 }
 
+// K2a: one CTA per (image, octave, 32x32 tile) in a fixed tile order; every
+// thread records which of its (level, row) positions are extrema as a 12-bit
+// mask and the tile publishes its count.  No tile ever waits on another.
 __global__ void __launch_bounds__(kDetThreads)
-detect_kernel(const __grid_constant__ DetectArgs a) {
+detect_count_kernel(const __grid_constant__ DetectArgs a) {
     extern __shared__ float lv_s[];   // [s+2][34][34]
-    __shared__ unsigned ticket_s;
-    __shared__ unsigned long long off_s;
     __shared__ int warp_tot[kDetThreads / 32];
-
-    const unsigned t = scan_ticket(a.scan, &ticket_s);
+    const unsigned t = blockIdx.x;
     const int b = (int)(t / a.tiles_per_image);
     const int rr = (int)(t % a.tiles_per_image);
     int o = 0;
@@ -105,18 +106,24 @@ detect_kernel(const __grid_constant__ DetectArgs a) {
     const int ys = 1 + (tile / od.tiles_x) * kDetTile;
     const int s = a.pyr.s, w = od.w, h = od.h;
     const int nlev = s + 2;
+    const int lane = threadIdx.x & 31;
 
+    // stage s+2 DoG levels (+1 halo) with asynchronous 4-byte copies: every
+    // load is in flight at once (a load->store chain per row serialises on
+    // memory latency); out-of-image positions are zero-filled
     const float* __restrict__ dogb = od.dog + (long long)b * a.pyr.dog_img_stride(o);
     for (int idx = threadIdx.x; idx < nlev * kDetHalo * kDetHalo; idx += kDetThreads) {
-        const int l = idx / (kDetHalo * kDetHalo), rem = idx % (kDetHalo * kDetHalo);
-        const int yy = ys - 1 + rem / kDetHalo, xx = xs - 1 + rem % kDetHalo;
-        float v = 0.0f;
-        if (xx < w && yy < h) v = __ldg(dogb + (long long)l * od.level_stride + (long long)yy * od.pitch + xx);
-        lv_s[idx] = v;
+        const int r = idx / kDetHalo, c = idx - r * kDetHalo;
+        const int l = r / kDetHalo, yy = ys - 1 + (r - l * kDetHalo), xx = xs - 1 + c;
+        const bool in = xx < w && yy < h;
+        const float* g = dogb + (in ? (long long)l * od.level_stride + (long long)yy * od.pitch + xx : 0);
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(lv_s + idx);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"(in ? 4 : 0));
     }
+    asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
-    const int lx = threadIdx.x & 31, ly0 = threadIdx.x >> 5;
+    const int lx = lane, ly0 = threadIdx.x >> 5;
     auto S = [&](int l, int xl, int yl) -> float {
         return lv_s[l * kDetHalo * kDetHalo + yl * kDetHalo + xl];
     };
@@ -134,11 +141,8 @@ detect_kernel(const __grid_constant__ DetectArgs a) {
             }
         return true;
     };
-
-    // pass 1 tests every (level, row) of this thread once and remembers hits in
-    // a bitmask (bit = level-major index); pass 2 only replays the hits.
-    unsigned long long hits = 0;
-    int count = 0;
+    // bit = level-major index (i - 1) * 4 + q  (detect.cpp:38-70 candidate tests)
+    unsigned hits = 0;
     {
         int bit = 0;
         for (int i = 1; i <= s; ++i) {
@@ -147,38 +151,70 @@ detect_kernel(const __grid_constant__ DetectArgs a) {
                 const int x = xs + lx, y = ys + ly;
                 if (x > w - 2 || y > h - 2) continue;
                 const float v = S(i, lx + 1, ly + 1);
-                if (!(fabsf(v) > a.pre_gate)) continue;
-                const bool is_max = v > 0.0f;
-                if (!extremal(i, lx + 1, ly + 1, v, is_max)) continue;
-                hits |= 1ull << bit;
-                ++count;
+                if (!(fabsf(v) > a.pre_gate)) continue;   // float pre-gate (detect.cpp:35)
+                if (!extremal(i, lx + 1, ly + 1, v, v > 0.0f)) continue;
+                hits |= 1u << bit;
             }
         }
     }
+    a.hit_masks[(size_t)t * kDetThreads + threadIdx.x] = (unsigned short)hits;
+    int cnt = __popc(hits);
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
+    if (lane == 0) warp_tot[ly0] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int wq = 0; wq < kDetThreads / 32; ++wq) tot += warp_tot[wq];
+        a.tile_counts[t] = (unsigned)tot;
+    }
+}
+
+// K2b: candidates of tile t go to [tile_offsets[t], +count) in (thread, level,
+// row) order -- the same deterministic order as a single-pass look-back.
+__global__ void __launch_bounds__(kDetThreads)
+detect_emit_kernel(const __grid_constant__ DetectArgs a) {
+    __shared__ int warp_tot[kDetThreads / 32];
+    const unsigned t = blockIdx.x;
+    const unsigned cnt_t = a.tile_counts[t];
+    const unsigned long long tile_off = a.tile_offsets[t];
+    if (t == a.n_tiles - 1 && threadIdx.x == 0) {
+        const unsigned long long total = tile_off + cnt_t;
+        if ((long long)total > a.cap) atomicOr(a.err, kErrCandidateCapacity);
+        *a.scan.total = min(total, (unsigned long long)a.cap);   // never more than was written
+    }
+    if (cnt_t == 0) return;
+    const int b = (int)(t / a.tiles_per_image);
+    const int rr = (int)(t % a.tiles_per_image);
+    int o = 0;
+    while (o + 1 < a.pyr.n_oct && a.oct_tile_base[o + 1] <= rr) ++o;
+    const OctaveDesc& od = a.pyr.oct[o];
+    const int tile = rr - a.oct_tile_base[o];
+    const int xs = 1 + (tile % od.tiles_x) * kDetTile;
+    const int ys = 1 + (tile / od.tiles_x) * kDetTile;
+    const int lane = threadIdx.x & 31, ly0 = threadIdx.x >> 5;
+    unsigned hits = a.hit_masks[(size_t)t * kDetThreads + threadIdx.x];
+    const int count = __popc(hits);
     int incl = count;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         const int nb = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lx >= d) incl += nb;
+        if (lane >= d) incl += nb;
     }
-    if (lx == 31) warp_tot[ly0] = incl;
+    if (lane == 31) warp_tot[ly0] = incl;
     __syncthreads();
-    int warp_off = 0, tile_total = 0;
-    for (int wq = 0; wq < kDetThreads / 32; ++wq) {
-        if (wq < ly0) warp_off += warp_tot[wq];
-        tile_total += warp_tot[wq];
-    }
-    const unsigned long long tile_off = scan_exclusive(a.scan, t, (unsigned long long)tile_total, a.n_tiles, &off_s);
-    if (threadIdx.x == 0 && (long long)(tile_off + tile_total) > a.cap) atomicOr(a.err, kErrCandidateCapacity);
+    int warp_off = 0;
+    for (int wq = 0; wq < ly0; ++wq) warp_off += warp_tot[wq];
     unsigned long long slot = tile_off + warp_off + (incl - count);
+    const float* __restrict__ dogb = od.dog + (long long)b * a.pyr.dog_img_stride(o);
     while (hits) {
-        const int bit = __ffsll(hits) - 1;
+        const int bit = __ffs(hits) - 1;
         hits &= hits - 1;
         const int i = 1 + bit / (kDetTile / 8), q = bit % (kDetTile / 8);
-        const int ly = ly0 + 8 * q;
-        const int x = xs + lx, y = ys + ly;
+        const int x = xs + lane, y = ys + ly0 + 8 * q;
         if ((long long)slot < a.cap) {
-            DevCandidate c = {b, o, i, y, x, S(i, lx + 1, ly + 1) > 0.0f ? 1 : 0};
+            const float v = __ldg(dogb + (long long)i * od.level_stride + (long long)y * od.pitch + x);
+            DevCandidate c = {b, o, i, y, x, v > 0.0f ? 1 : 0};
             a.cand_out[slot] = c;
         }
         ++slot;
@@ -235,12 +271,22 @@ cudaError_t launch_refine(const DetectArgs& a, const DevCandidate* cand, const u
     return cudaGetLastError();
 }
 
+size_t detect_scan_temp_bytes(unsigned n_tiles) {
+    size_t bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const unsigned*)nullptr, (unsigned*)nullptr, (int)n_tiles);
+    return bytes;
+}
+
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st) {
     if (a.n_tiles == 0) return cudaSuccess;
     const size_t smem = sizeof(float) * (size_t)(a.pyr.s + 2) * kDetHalo * kDetHalo;
-    cudaError_t e = cudaFuncSetAttribute(detect_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(detect_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    detect_kernel<<<a.n_tiles, kDetThreads, smem, st>>>(a);
+    detect_count_kernel<<<a.n_tiles, kDetThreads, smem, st>>>(a);
+    size_t tb = a.scan_temp_bytes;
+    e = cub::DeviceScan::ExclusiveSum(a.scan_temp, tb, a.tile_counts, a.tile_offsets, (int)a.n_tiles, st);
+    if (e != cudaSuccess) return e;
+    detect_emit_kernel<<<a.n_tiles, kDetThreads, 0, st>>>(a);
     return cudaGetLastError();
 }
 

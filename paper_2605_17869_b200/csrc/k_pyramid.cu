@@ -26,10 +26,22 @@
 //             writes those samples as this octave's G[0]      (seed + first blur)
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "dsift_common.cuh"
 #include "dsift_kernels.cuh"
 
 namespace dsift {
+
+// A/B switch for measurements: DSIFT_BLUR_V1=1 keeps the v1 LEVEL kernel.
+static bool blur_v1_forced() {
+    static const int v = [] {
+        const char* e = std::getenv("DSIFT_BLUR_V1");
+        return e ? std::atoi(e) : 0;
+    }();
+    return v != 0;
+}
 
 constexpr int kTileW = 64;
 constexpr int kTileH = 64;
@@ -230,9 +242,209 @@ static cudaError_t launch_mode(const BlurArgs& a, int R, int batch, cudaStream_t
     return cudaGetLastError();
 }
 
+
+// ---------------------------------------------------------------------------
+// LEVEL-mode blur, v2 (the 5 incremental levels of every octave).
+//
+// The FP64 tap sums and the f32->f64 conversions (XU pipe, 1/4 of the FP64
+// rate) bound this stage, not HBM.  v2 therefore
+//   * stages the (64+2R)^2 input tile with 16-byte coalesced loads (interior
+//     tiles; border tiles use reflect-101 per element), 16-byte aligned so the
+//     H pass can read its window with LDS.128;
+//   * computes 8 outputs per thread in both passes: each staged value is
+//     converted to FP64 once per 8-output window (v1: per 4) and feeds 8
+//     independent DFMA chains.
+// Each output is still Sum_t k[t] * x[t] accumulated left to right in FP64
+// and rounded to float once per pass (scalespace.cpp:63-109).
+// ---------------------------------------------------------------------------
+constexpr int kB2W = 64, kB2H = 64, kB2Seg = 8, kB2Threads = 256;
+
+template <int R>
+struct B2Geom {
+    static constexpr int kLen = 2 * R + 1;
+    static constexpr int kWin = kB2Seg + 2 * R;                 // inputs per 8 outputs
+    static constexpr int kHR = kB2H + 2 * R;                    // input / tmp rows
+    static constexpr int kM = (4 - (R & 3)) & 3;                // (x - R) mod 4 for x = 0 mod 8
+    static constexpr int kNV = (kWin + kM + 3) / 4;             // float4 per window
+    static constexpr int kInW = ((kB2W + 2 * R + kM + 3) / 4) * 4;
+    static constexpr int kInPitch = kInW + 4;                   // floats; +4 spreads LDS.128 rows over banks
+    static constexpr int kTmpPitch = kB2W + 1;
+    static constexpr int kItems = (kHR * (kB2W / kB2Seg) + kB2Threads - 1) / kB2Threads;   // H items per thread
+    // the float tmp overwrites the staged input once the H pass has read it
+    static constexpr size_t kSmem = sizeof(float) * (size_t)kHR * (kInPitch > kTmpPitch ? kInPitch : kTmpPitch);
+};
+
+// float -> double for a positive normal float, on the integer pipe: the
+// exponent is rebiased (+896) and the mantissa shifted into place.  Exact for
+// exactly those inputs; the XU conversion (a quarter of the FP64 rate) is the
+// stage's co-bottleneck otherwise.
+__device__ __forceinline__ double widen_pos_normal(float x) {
+    const unsigned b = __float_as_uint(x);
+    return __hiloint2double((int)((b >> 3) + 0x38000000u), (int)(b << 29));
+}
+
+template <int R, bool kAlu>
+__device__ __forceinline__ double b2_widen(float x) {
+    if (kAlu) return widen_pos_normal(x);
+    return (double)x;
+}
+
+// H pass of one tile: results stay in registers until every thread has read
+// the staged input, then overwrite it as the float tmp.
+template <int R, bool kAlu>
+__device__ __forceinline__ void b2_hpass(const BlurArgs& a, float* sm) {
+    using G = B2Geom<R>;
+    float hres[G::kItems][kB2Seg];
+#pragma unroll
+    for (int it = 0; it < G::kItems; ++it) {
+        const int item = threadIdx.x + it * kB2Threads;
+        if (item < G::kHR * (kB2W / kB2Seg)) {
+            const int r = item >> 3, sg = item & 7;
+            const float4* v4 = reinterpret_cast<const float4*>(sm + r * G::kInPitch + sg * kB2Seg);
+            float win[4 * G::kNV];
+#pragma unroll
+            for (int q = 0; q < G::kNV; ++q) {
+                const float4 t = v4[q];
+                win[4 * q] = t.x; win[4 * q + 1] = t.y; win[4 * q + 2] = t.z; win[4 * q + 3] = t.w;
+            }
+            double acc[kB2Seg];
+#pragma unroll
+            for (int j = 0; j < kB2Seg; ++j) acc[j] = 0.0;
+#pragma unroll
+            for (int e = 0; e < G::kWin; ++e) {
+                const double x = b2_widen<R, kAlu>(win[G::kM + e]);
+#pragma unroll
+                for (int j = 0; j < kB2Seg; ++j) {
+                    const int t = e - j;
+                    if (t >= 0 && t < G::kLen) acc[j] = __fma_rn(a.taps[t], x, acc[j]);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kB2Seg; ++j) hres[it][j] = (float)acc[j];   // float tmp (scalespace.cpp:86)
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < G::kItems; ++it) {
+        const int item = threadIdx.x + it * kB2Threads;
+        if (item < G::kHR * (kB2W / kB2Seg)) {
+            float* o = sm + (item >> 3) * G::kTmpPitch + (item & 7) * kB2Seg;
+#pragma unroll
+            for (int j = 0; j < kB2Seg; ++j) o[j] = hres[it][j];
+        }
+    }
+    __syncthreads();
+}
+
+// V pass: item = (column c, 8-row group), lanes along x; writes G and DoG.
+template <int R, bool kAlu>
+__device__ __forceinline__ void b2_vpass(const BlurArgs& a, const float* sm, int b, int x0, int y0) {
+    using G = B2Geom<R>;
+    const int w = a.w, h = a.h, pitch = a.pitch;
+    const float* __restrict__ src = a.src + b * a.src_img_stride;
+    float* __restrict__ dst = a.dst + b * a.dst_img_stride;
+    float* __restrict__ dog = a.dog ? a.dog + b * a.dog_img_stride : nullptr;
+    for (int item = threadIdx.x; item < kB2W * (kB2H / kB2Seg); item += kB2Threads) {
+        const int c = item & (kB2W - 1), rg = item >> 6;
+        const int x = x0 + c;
+        double acc[kB2Seg];
+#pragma unroll
+        for (int j = 0; j < kB2Seg; ++j) acc[j] = 0.0;
+        const float* col = sm + (rg * kB2Seg) * G::kTmpPitch + c;
+#pragma unroll
+        for (int e = 0; e < G::kWin; ++e) {
+            const double v = b2_widen<R, kAlu>(col[e * G::kTmpPitch]);
+#pragma unroll
+            for (int j = 0; j < kB2Seg; ++j) {
+                const int t = e - j;
+                if (t >= 0 && t < G::kLen) acc[j] = __fma_rn(a.taps[t], v, acc[j]);
+            }
+        }
+        if (x < w) {
+#pragma unroll
+            for (int j = 0; j < kB2Seg; ++j) {
+                const int y = y0 + rg * kB2Seg + j;
+                if (y < h) {
+                    const float g = (float)acc[j];
+                    const long long off = (long long)y * pitch + x;
+                    dst[off] = g;
+                    // DoG[i-1] = G[i] - G[i-1] (scalespace.cpp:209); G[i-1] was just read (L2)
+                    if (dog) dog[off] = g - __ldg(src + off);
+                }
+            }
+        }
+    }
+}
+
+template <int R>
+__global__ void __launch_bounds__(kB2Threads)
+blur_level2_kernel(const __grid_constant__ BlurArgs a) {
+    using G = B2Geom<R>;
+    extern __shared__ __align__(16) float sm2[];       // staged input [kHR][kInPitch], then tmp [kHR][kTmpPitch]
+    const int b = blockIdx.z;
+    const int x0 = blockIdx.x * kB2W, y0 = blockIdx.y * kB2H;
+    const int w = a.w, h = a.h, pitch = a.pitch;
+    const float* __restrict__ src = a.src + b * a.src_img_stride;
+    const int cx0 = x0 - R - G::kM;                    // 16-byte aligned global column of staged column 0
+
+    // ---- stage the input tile; note whether every value is a positive normal
+    //      float >= 2^-100 (then the tmp values are positive normals too: the
+    //      smallest tap is > 2^-20) so both passes may widen on the ALU pipe
+    bool alu_ok = true;
+    const bool interior = cx0 >= 0 && cx0 + G::kInW <= pitch && x0 + kB2W + R <= w && y0 - R >= 0 &&
+                          y0 + kB2H + R <= h;
+    if (interior) {
+        constexpr int kV = G::kInW / 4;
+        for (int i = threadIdx.x; i < G::kHR * kV; i += kB2Threads) {
+            const int r = i / kV, q = i - r * kV;
+            const float4 v = __ldg(reinterpret_cast<const float4*>(src + (long long)(y0 - R + r) * pitch + cx0) + q);
+            *reinterpret_cast<float4*>(sm2 + r * G::kInPitch + 4 * q) = v;
+            const int m = min(min(__float_as_int(v.x), __float_as_int(v.y)), min(__float_as_int(v.z), __float_as_int(v.w)));
+            const int M = max(max(__float_as_int(v.x), __float_as_int(v.y)), max(__float_as_int(v.z), __float_as_int(v.w)));
+            alu_ok &= (m >= 0x0d800000) & (M < 0x7f800000);
+        }
+    } else {   // border tile: reflect-101 per element (scalespace.cpp:41-48)
+        for (int r = threadIdx.x >> 5; r < G::kHR; r += kB2Threads / 32) {
+            const float* row = src + (long long)reflect101(y0 - R + r, h) * pitch;
+            for (int c = threadIdx.x & 31; c < G::kInW; c += 32) {
+                const float v = __ldg(row + reflect101(cx0 + c, w));
+                sm2[r * G::kInPitch + c] = v;
+                alu_ok &= (__float_as_int(v) >= 0x0d800000) & (__float_as_int(v) < 0x7f800000);
+            }
+        }
+    }
+    if (__syncthreads_and(alu_ok)) {
+        b2_hpass<R, true>(a, sm2);
+        b2_vpass<R, true>(a, sm2, b, x0, y0);
+    } else {
+        b2_hpass<R, false>(a, sm2);
+        b2_vpass<R, false>(a, sm2, b, x0, y0);
+    }
+}
+
+static cudaError_t launch_level2(const BlurArgs& a, int R, int batch, cudaStream_t st) {
+    const dim3 grid((a.w + kB2W - 1) / kB2W, (a.h + kB2H - 1) / kB2H, batch);
+    size_t smem = 0;
+    void (*fn)(BlurArgs) = nullptr;
+    switch (R) {
+#define DSIFT_R2(r) case r: fn = blur_level2_kernel<r>; smem = B2Geom<r>::kSmem; break;
+        DSIFT_R2(1) DSIFT_R2(2) DSIFT_R2(3) DSIFT_R2(4) DSIFT_R2(5) DSIFT_R2(6) DSIFT_R2(7) DSIFT_R2(8)
+        DSIFT_R2(9) DSIFT_R2(10) DSIFT_R2(11) DSIFT_R2(12) DSIFT_R2(13) DSIFT_R2(14) DSIFT_R2(15)
+        DSIFT_R2(16)
+#undef DSIFT_R2
+        default: return cudaErrorInvalidValue;
+    }
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kB2Threads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStream_t st) {
     switch (mode) {
-        case kModeLevel: return launch_mode<kModeLevel>(a, R, batch, st);
+        case kModeLevel:
+            if (R >= 1 && R <= 16 && a.src_pitch == a.pitch && !blur_v1_forced()) return launch_level2(a, R, batch, st);
+            return launch_mode<kModeLevel>(a, R, batch, st);
         case kModeRaw: return launch_mode<kModeRaw>(a, R, batch, st);
         case kModeUpsample: return launch_mode<kModeUpsample>(a, R, batch, st);
         default: return launch_mode<kModeDecimate>(a, R, batch, st);
