@@ -22,6 +22,7 @@ namespace dsift {
 constexpr int kDetTile = 32;
 constexpr int kDetThreads = 256;
 constexpr int kDetHalo = kDetTile + 2;
+constexpr int kDetPitch = 36;   // staged row pitch (floats): 16-byte aligned rows
 
 // refine_extremum (detect.cpp:73-156), bit-exact FP64 restatement.
 __device__ bool refine_candidate(const DetectArgs& a, int b, int o, int x, int y, int i,
@@ -93,7 +94,7 @@ __device__ bool refine_candidate(const DetectArgs& a, int b, int o, int x, int y
 // mask and the tile publishes its count.  No tile ever waits on another.
 __global__ void __launch_bounds__(kDetThreads)
 detect_count_kernel(const __grid_constant__ DetectArgs a) {
-    extern __shared__ float lv_s[];   // [s+2][34][34]
+    extern __shared__ __align__(16) float lv_s[];   // [s+2][34][kDetPitch]
     __shared__ int warp_tot[kDetThreads / 32];
     const unsigned t = blockIdx.x;
     const int b = (int)(t / a.tiles_per_image);
@@ -112,20 +113,26 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
     // load is in flight at once (a load->store chain per row serialises on
     // memory latency); out-of-image positions are zero-filled
     const float* __restrict__ dogb = od.dog + (long long)b * a.pyr.dog_img_stride(o);
-    for (int idx = threadIdx.x; idx < nlev * kDetHalo * kDetHalo; idx += kDetThreads) {
-        const int r = idx / kDetHalo, c = idx - r * kDetHalo;
-        const int l = r / kDetHalo, yy = ys - 1 + (r - l * kDetHalo), xx = xs - 1 + c;
-        const bool in = xx < w && yy < h;
-        const float* g = dogb + (in ? (long long)l * od.level_stride + (long long)yy * od.pitch + xx : 0);
-        const unsigned sa = (unsigned)__cvta_generic_to_shared(lv_s + idx);
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"(in ? 4 : 0));
+    // a staged row = 32 aligned floats (8 x 16 B, xs - 1 = 32k) + 2 halo floats
+    for (int idx = threadIdx.x; idx < nlev * kDetHalo * 10; idx += kDetThreads) {
+        const int r = idx / 10, q = idx - r * 10;
+        const int l = r / kDetHalo, yy = ys - 1 + (r - l * kDetHalo);
+        const int xx = xs - 1 + (q < 8 ? 4 * q : 24 + q);   // q = 8, 9 -> columns 32, 33
+        const int cols = q < 8 ? 4 : 1;
+        const int nin = yy < h ? max(0, min(cols, w - xx)) : 0;
+        const float* g = dogb + (nin ? (long long)l * od.level_stride + (long long)yy * od.pitch + xx : 0);
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(lv_s + r * kDetPitch + (xx - (xs - 1)));
+        if (q < 8)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(4 * nin));
+        else
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"(4 * nin));
     }
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
     const int lx = lane, ly0 = threadIdx.x >> 5;
     auto S = [&](int l, int xl, int yl) -> float {
-        return lv_s[l * kDetHalo * kDetHalo + yl * kDetHalo + xl];
+        return lv_s[(l * kDetHalo + yl) * kDetPitch + xl];
     };
     // strictly_extremal (detect.cpp:11-28) on the staged tile
     auto extremal = [&](int i, int xl, int yl, float v, bool is_max) -> bool {
@@ -171,14 +178,16 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
 }
 
 // K2b: candidates of tile t go to [tile_offsets[t], +count) in (thread, level,
-// row) order -- the same deterministic order as a single-pass look-back.
-__global__ void __launch_bounds__(kDetThreads)
+// row) order -- the same deterministic order as a single-pass look-back.  One
+// warp per tile (8 tiles per CTA): lane j replays count-kernel threads 8j..8j+7.
+__global__ void __launch_bounds__(256)
 detect_emit_kernel(const __grid_constant__ DetectArgs a) {
-    __shared__ int warp_tot[kDetThreads / 32];
-    const unsigned t = blockIdx.x;
+    const int lane = threadIdx.x & 31;
+    const unsigned t = blockIdx.x * 8 + (threadIdx.x >> 5);
+    if (t >= a.n_tiles) return;
     const unsigned cnt_t = a.tile_counts[t];
     const unsigned long long tile_off = a.tile_offsets[t];
-    if (t == a.n_tiles - 1 && threadIdx.x == 0) {
+    if (t == a.n_tiles - 1 && lane == 0) {
         const unsigned long long total = tile_off + cnt_t;
         if ((long long)total > a.cap) atomicOr(a.err, kErrCandidateCapacity);
         *a.scan.total = min(total, (unsigned long long)a.cap);   // never more than was written
@@ -192,32 +201,36 @@ detect_emit_kernel(const __grid_constant__ DetectArgs a) {
     const int tile = rr - a.oct_tile_base[o];
     const int xs = 1 + (tile % od.tiles_x) * kDetTile;
     const int ys = 1 + (tile / od.tiles_x) * kDetTile;
-    const int lane = threadIdx.x & 31, ly0 = threadIdx.x >> 5;
-    unsigned hits = a.hit_masks[(size_t)t * kDetThreads + threadIdx.x];
-    const int count = __popc(hits);
+    const uint4 m4 = reinterpret_cast<const uint4*>(a.hit_masks + (size_t)t * kDetThreads)[lane];   // 8 x u16
+    const unsigned mw[4] = {m4.x, m4.y, m4.z, m4.w};
+    int count = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) count += __popc(mw[k]);
     int incl = count;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
         const int nb = __shfl_up_sync(0xffffffffu, incl, d);
         if (lane >= d) incl += nb;
     }
-    if (lane == 31) warp_tot[ly0] = incl;
-    __syncthreads();
-    int warp_off = 0;
-    for (int wq = 0; wq < ly0; ++wq) warp_off += warp_tot[wq];
-    unsigned long long slot = tile_off + warp_off + (incl - count);
+    unsigned long long slot = tile_off + (incl - count);
     const float* __restrict__ dogb = od.dog + (long long)b * a.pyr.dog_img_stride(o);
-    while (hits) {
-        const int bit = __ffs(hits) - 1;
-        hits &= hits - 1;
-        const int i = 1 + bit / (kDetTile / 8), q = bit % (kDetTile / 8);
-        const int x = xs + lane, y = ys + ly0 + 8 * q;
-        if ((long long)slot < a.cap) {
-            const float v = __ldg(dogb + (long long)i * od.level_stride + (long long)y * od.pitch + x);
-            DevCandidate c = {b, o, i, y, x, v > 0.0f ? 1 : 0};
-            a.cand_out[slot] = c;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int th = lane * 8 + k;                 // the count kernel's thread index
+        const int lx = th & 31, ly0 = th >> 5;
+        unsigned hits = (mw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+        while (hits) {
+            const int bit = __ffs(hits) - 1;
+            hits &= hits - 1;
+            const int i = 1 + bit / (kDetTile / 8), q = bit % (kDetTile / 8);
+            const int x = xs + lx, y = ys + ly0 + 8 * q;
+            if ((long long)slot < a.cap) {
+                const float v = __ldg(dogb + (long long)i * od.level_stride + (long long)y * od.pitch + x);
+                DevCandidate c = {b, o, i, y, x, v > 0.0f ? 1 : 0};
+                a.cand_out[slot] = c;
+            }
+            ++slot;
         }
-        ++slot;
     }
 }
 
@@ -279,14 +292,14 @@ size_t detect_scan_temp_bytes(unsigned n_tiles) {
 
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st) {
     if (a.n_tiles == 0) return cudaSuccess;
-    const size_t smem = sizeof(float) * (size_t)(a.pyr.s + 2) * kDetHalo * kDetHalo;
+    const size_t smem = sizeof(float) * (size_t)(a.pyr.s + 2) * kDetHalo * kDetPitch;
     cudaError_t e = cudaFuncSetAttribute(detect_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     detect_count_kernel<<<a.n_tiles, kDetThreads, smem, st>>>(a);
     size_t tb = a.scan_temp_bytes;
     e = cub::DeviceScan::ExclusiveSum(a.scan_temp, tb, a.tile_counts, a.tile_offsets, (int)a.n_tiles, st);
     if (e != cudaSuccess) return e;
-    detect_emit_kernel<<<a.n_tiles, kDetThreads, 0, st>>>(a);
+    detect_emit_kernel<<<(a.n_tiles + 7) / 8, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 

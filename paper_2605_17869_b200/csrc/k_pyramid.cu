@@ -336,14 +336,16 @@ __device__ __forceinline__ void b2_hpass(const BlurArgs& a, float* sm) {
     __syncthreads();
 }
 
-// V pass: item = (column c, 8-row group), lanes along x; writes G and DoG.
-template <int R, bool kAlu>
+// V pass: item = (column c, 8-row group), lanes along x; writes G and, for
+// LEVEL / DECIMATE, DoG (and the DECIMATE seed = this octave's G[0]).
+template <int R, int MODE, bool kAlu>
 __device__ __forceinline__ void b2_vpass(const BlurArgs& a, const float* sm, int b, int x0, int y0) {
     using G = B2Geom<R>;
     const int w = a.w, h = a.h, pitch = a.pitch;
     const float* __restrict__ src = a.src + b * a.src_img_stride;
     float* __restrict__ dst = a.dst + b * a.dst_img_stride;
     float* __restrict__ dog = a.dog ? a.dog + b * a.dog_img_stride : nullptr;
+    float* __restrict__ seed = (MODE == kModeDecimate) ? a.seed + b * a.seed_img_stride : nullptr;
     for (int item = threadIdx.x; item < kB2W * (kB2H / kB2Seg); item += kB2Threads) {
         const int c = item & (kB2W - 1), rg = item >> 6;
         const int x = x0 + c;
@@ -369,14 +371,21 @@ __device__ __forceinline__ void b2_vpass(const BlurArgs& a, const float* sm, int
                     const long long off = (long long)y * pitch + x;
                     dst[off] = g;
                     // DoG[i-1] = G[i] - G[i-1] (scalespace.cpp:209); G[i-1] was just read (L2)
-                    if (dog) dog[off] = g - __ldg(src + off);
+                    if (MODE == kModeLevel) {
+                        if (dog) dog[off] = g - __ldg(src + off);
+                    } else if (MODE == kModeDecimate) {
+                        // G[0] of this octave = even samples of G[s] of the previous one (scalespace.cpp:133-142)
+                        const float prev = __ldg(src + (long long)(2 * y) * a.src_pitch + 2 * x);
+                        seed[off] = prev;
+                        if (dog) dog[off] = g - prev;
+                    }
                 }
             }
         }
     }
 }
 
-template <int R>
+template <int R, int MODE>
 __global__ void __launch_bounds__(kB2Threads)
 blur_level2_kernel(const __grid_constant__ BlurArgs a) {
     using G = B2Geom<R>;
@@ -385,49 +394,58 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
     const int x0 = blockIdx.x * kB2W, y0 = blockIdx.y * kB2H;
     const int w = a.w, h = a.h, pitch = a.pitch;
     const float* __restrict__ src = a.src + b * a.src_img_stride;
-    const int cx0 = x0 - R - G::kM;                    // 16-byte aligned global column of staged column 0
+    const int cx0 = x0 - R - G::kM;                    // 16-byte aligned column of staged column 0
 
     // ---- stage the input tile; note whether every value is a positive normal
     //      float >= 2^-100 (then the tmp values are positive normals too: the
     //      smallest tap is > 2^-20) so both passes may widen on the ALU pipe
     bool alu_ok = true;
-    const bool interior = cx0 >= 0 && cx0 + G::kInW <= pitch && x0 + kB2W + R <= w && y0 - R >= 0 &&
-                          y0 + kB2H + R <= h;
+    const bool interior = MODE == kModeLevel && cx0 >= 0 && cx0 + G::kInW <= pitch && x0 + kB2W + R <= w &&
+                          y0 - R >= 0 && y0 + kB2H + R <= h;
     if (interior) {
+        // asynchronous 16-byte copies: the whole tile is in flight at once
         constexpr int kV = G::kInW / 4;
+        const float* gsrc = src + (long long)(y0 - R) * pitch + cx0;
         for (int i = threadIdx.x; i < G::kHR * kV; i += kB2Threads) {
             const int r = i / kV, q = i - r * kV;
-            const float4 v = __ldg(reinterpret_cast<const float4*>(src + (long long)(y0 - R + r) * pitch + cx0) + q);
-            *reinterpret_cast<float4*>(sm2 + r * G::kInPitch + 4 * q) = v;
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(sm2 + r * G::kInPitch + 4 * q);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc + (long long)r * pitch + 4 * q));
+        }
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
+        for (int i = threadIdx.x; i < G::kHR * kV; i += kB2Threads) {
+            const int r = i / kV, q = i - r * kV;
+            const float4 v = *reinterpret_cast<const float4*>(sm2 + r * G::kInPitch + 4 * q);
             const int m = min(min(__float_as_int(v.x), __float_as_int(v.y)), min(__float_as_int(v.z), __float_as_int(v.w)));
             const int M = max(max(__float_as_int(v.x), __float_as_int(v.y)), max(__float_as_int(v.z), __float_as_int(v.w)));
             alu_ok &= (m >= 0x0d800000) & (M < 0x7f800000);
         }
-    } else {   // border tile: reflect-101 per element (scalespace.cpp:41-48)
-        for (int r = threadIdx.x >> 5; r < G::kHR; r += kB2Threads / 32) {
-            const float* row = src + (long long)reflect101(y0 - R + r, h) * pitch;
-            for (int c = threadIdx.x & 31; c < G::kInW; c += 32) {
-                const float v = __ldg(row + reflect101(cx0 + c, w));
-                sm2[r * G::kInPitch + c] = v;
-                alu_ok &= (__float_as_int(v) >= 0x0d800000) & (__float_as_int(v) < 0x7f800000);
-            }
+    } else {   // gather with reflect-101 (scalespace.cpp:41-48) through the mode's input
+               // mapping: level / raw pixel, 2x upsample (:113-131), decimation (:133-142)
+#pragma unroll 4
+        for (int i = threadIdx.x; i < G::kHR * G::kInW; i += kB2Threads) {
+            const int r = i / G::kInW, c = i - r * G::kInW;
+            const float v = fetch_input<MODE>(a, src, reflect101(cx0 + c, w), reflect101(y0 - R + r, h));
+            sm2[r * G::kInPitch + c] = v;
+            alu_ok &= (__float_as_int(v) >= 0x0d800000) & (__float_as_int(v) < 0x7f800000);
         }
     }
     if (__syncthreads_and(alu_ok)) {
         b2_hpass<R, true>(a, sm2);
-        b2_vpass<R, true>(a, sm2, b, x0, y0);
+        b2_vpass<R, MODE, true>(a, sm2, b, x0, y0);
     } else {
         b2_hpass<R, false>(a, sm2);
-        b2_vpass<R, false>(a, sm2, b, x0, y0);
+        b2_vpass<R, MODE, false>(a, sm2, b, x0, y0);
     }
 }
 
-static cudaError_t launch_level2(const BlurArgs& a, int R, int batch, cudaStream_t st) {
+template <int MODE>
+static cudaError_t launch_v2(const BlurArgs& a, int R, int batch, cudaStream_t st) {
     const dim3 grid((a.w + kB2W - 1) / kB2W, (a.h + kB2H - 1) / kB2H, batch);
     size_t smem = 0;
     void (*fn)(BlurArgs) = nullptr;
     switch (R) {
-#define DSIFT_R2(r) case r: fn = blur_level2_kernel<r>; smem = B2Geom<r>::kSmem; break;
+#define DSIFT_R2(r) case r: fn = blur_level2_kernel<r, MODE>; smem = B2Geom<r>::kSmem; break;
         DSIFT_R2(1) DSIFT_R2(2) DSIFT_R2(3) DSIFT_R2(4) DSIFT_R2(5) DSIFT_R2(6) DSIFT_R2(7) DSIFT_R2(8)
         DSIFT_R2(9) DSIFT_R2(10) DSIFT_R2(11) DSIFT_R2(12) DSIFT_R2(13) DSIFT_R2(14) DSIFT_R2(15)
         DSIFT_R2(16)
@@ -441,13 +459,20 @@ static cudaError_t launch_level2(const BlurArgs& a, int R, int batch, cudaStream
 }
 
 cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStream_t st) {
+    const bool v2 = R >= 1 && R <= 16 && !blur_v1_forced();
     switch (mode) {
         case kModeLevel:
-            if (R >= 1 && R <= 16 && a.src_pitch == a.pitch && !blur_v1_forced()) return launch_level2(a, R, batch, st);
+            if (v2 && a.src_pitch == a.pitch) return launch_v2<kModeLevel>(a, R, batch, st);
             return launch_mode<kModeLevel>(a, R, batch, st);
-        case kModeRaw: return launch_mode<kModeRaw>(a, R, batch, st);
-        case kModeUpsample: return launch_mode<kModeUpsample>(a, R, batch, st);
-        default: return launch_mode<kModeDecimate>(a, R, batch, st);
+        case kModeRaw:
+            if (v2) return launch_v2<kModeRaw>(a, R, batch, st);
+            return launch_mode<kModeRaw>(a, R, batch, st);
+        case kModeUpsample:
+            if (v2) return launch_v2<kModeUpsample>(a, R, batch, st);
+            return launch_mode<kModeUpsample>(a, R, batch, st);
+        default:
+            if (v2) return launch_v2<kModeDecimate>(a, R, batch, st);
+            return launch_mode<kModeDecimate>(a, R, batch, st);
     }
 }
 
