@@ -749,7 +749,8 @@ struct StreamSmem {
     float* ring;    // [kSRing][ring_pitch] bilinear samples, -1 = undefined
     float* raw;     // [n_dsp][128]
     int* lanelsb;   // [128] per-lane lower bound on the leaves' lowest-bit exponent (+531: sum of 4 biased exponents)
-    int* misc;      // [2][8]: kmin, kmax, start of cell c = -1..3 (double-buffered per scale)
+    int* misc;      // [2][16]: kmin, kmax, start of cell c = -1..3, min weight exponent of
+                    // cell c = -1..3 (misc[8 + c + 1]); double-buffered per scale
 };
 
 // Biased exponent of x > 0 (floor(log2 x) + 127); denormals map to -22
@@ -764,13 +765,13 @@ __device__ __forceinline__ int efield1(float x) {
 
 __device__ __forceinline__ void stream_misc_init(int* misc) {
     const int t = threadIdx.x;
-    if (t < 16) misc[t] = ((t & 7) == 1) ? -(1 << 30) : (1 << 30);
+    if (t < 32) misc[t] = ((t & 15) == 1) ? -(1 << 30) : (1 << 30);
 }
 // Re-arm one misc buffer after its last read.  The buffer is next written two
 // scale calls later, with at least one CTA barrier in between.
 __device__ __forceinline__ void stream_misc_rearm(int* misc) {
     const int t = threadIdx.x;
-    if (t < 8) misc[t] = (t == 1) ? -(1 << 30) : (1 << 30);
+    if (t < 16) misc[t] = (t == 1) ? -(1 << 30) : (1 << 30);
 }
 
 // a[i] for a register array indexed by a runtime value (select chain, no local memory)
@@ -817,7 +818,8 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         const float gr = F_SUB(1.0f, fr);
         S.q2[i] = D_MUL(q, q);
         S.wp[i] = make_float2(gr, fr);
-        S.ew[i] = min(fr != 0.0f ? efield1(fr) : 255, gr != 0.0f ? efield1(gr) : 255);
+        const int ewk = min(fr != 0.0f ? efield1(fr) : 255, gr != 0.0f ? efield1(gr) : 255);
+        S.ew[i] = ewk;
         S.ax[i] = D_ADD(cx, D_MUL(cosa, (double)k));
         S.cysu[i] = D_ADD(cy, D_MUL(sina, (double)k));
         S.sv[i] = D_MUL(sina, (double)k);
@@ -1083,7 +1085,7 @@ __global__ void __launch_bounds__(kDescThreads, 4)
 describe_stream_kernel(const __grid_constant__ DescArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ double red[4];
-    __shared__ int misc[16];
+    __shared__ int misc[32];
     const int SP = a.max_span;
     const int RP = (SP - 6) & ~1;   // >= the widest ring row 2*ceil(2.5 bw) + 1 (host: SP = that + 7)
     StreamSmem S;
@@ -1112,7 +1114,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
         bool all_ok = true;
         for (int fi = 0; fi < a.n_dsp; ++fi, ++call) {
             const bool ok = raw_descriptor_stream(a, S, kp, a.dsp[fi], cs.x, cs.y, S.raw + fi * kDescDim, RP,
-                                                  misc + 8 * (call & 1));
+                                                  misc + 16 * (call & 1));
             const bool sok = __syncthreads_and(ok);
             if (!sok && a.force_slow == 0) {
                 // a bin the certificate could not prove: recompute this scale with
