@@ -302,6 +302,32 @@ def run_ours(args, rank, local_rank, world):
         e2e = {"value": B * world * nsteps / et_max, "unit": "images/s",
                "h2d_bytes_per_step": B * W * H * 4, "d2h_bytes_per_step": int(d2h / nsteps),
                "mpx_per_s": B * world * nsteps * W * H / 1e6 / et_max}
+        # the same, fed as 8-bit images (load_image's payload): the
+        # synthetic images quantised to uint8, converted on the device
+        host_u8 = torch.empty((B, H, W), dtype=torch.uint8, pin_memory=True)
+        host_u8.copy_(torch.clamp(torch.round(imgs * 255.0), 0, 255).to(torch.uint8).cpu())
+        u8_np = host_u8.numpy()
+
+        def e2e_u8_step():
+            _check = ds._check
+            _check(lib, lib.dsift_extract_batch_u8(ex.ctx, u8_np.ctypes.data, B, W, H, 1, 0))
+            total = ex.sync()
+            assert total <= cap
+            _check(lib, lib.dsift_result_copy(ex.ctx, out_k.ctypes.data, out_d.ctypes.data, None,
+                                              offs.ctypes.data))
+            return total
+
+        e2e_u8_step()
+        barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        d2h8 = 0
+        for _ in range(nsteps):
+            d2h8 += e2e_u8_step() * (28 + 512) + 8 * (B + 1)
+        torch.cuda.synchronize()
+        et8 = max_over_ranks(time.perf_counter() - t0)
+        e2e["u8_ingest"] = {"value": B * world * nsteps / et8, "unit": "images/s",
+                            "h2d_bytes_per_step": B * W * H, "d2h_bytes_per_step": int(d2h8 / nsteps)}
 
     # ---- roofline (per-stage, CUDA events inside the timed region) ------------------------
     k1, k2, px = stage_bytes(W, H)

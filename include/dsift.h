@@ -34,7 +34,8 @@ enum {
     DSIFT_ECUDA = 3,     /* CUDA runtime error / no device / extension absent */
     DSIFT_ENOMEM = 4,    /* device or host allocation failed                  */
     DSIFT_ESTATE = 5,    /* call order violated (e.g. no result yet)          */
-    DSIFT_ERANGE = 6     /* std::out_of_range in the reference (NaN input)   */
+    DSIFT_ERANGE = 6,    /* std::out_of_range in the reference (NaN input)   */
+    DSIFT_EIO = 7        /* std::runtime_error in the reference (image I/O)  */
 };
 
 /* detsift::SiftConfig (core.hpp:30-47).  dsp_scales is borrowed by the call. */
@@ -94,6 +95,23 @@ int dsift_set_capacity(dsift_ctx* ctx, int64_t max_keypoints_per_image);
  * per image in canonical order (core.cpp:116-170). */
 int dsift_extract_batch(dsift_ctx* ctx, const float* images, int n, int w, int h, int flags);
 int dsift_extract(dsift_ctx* ctx, const float* image, int w, int h, int flags);
+/* 8-bit ingest (replaces load_image's float conversion, io.cpp:49-81): n
+ * images of w x h pixels with channels = 1 (P5 gray) or 3 (P6 RGB,
+ * interleaved), host or device (flags).  The bytes are converted on the
+ * device with the reference's double arithmetic, then extracted exactly like
+ * dsift_extract_batch on the resulting GrayImages. */
+int dsift_extract_batch_u8(dsift_ctx* ctx, const uint8_t* pixels, int n, int w, int h, int channels,
+                           int flags);
+/* Reads a binary PNM (P5/P6, maxval 255) like detsift::load_image
+ * (io.cpp:49-81), with its error messages (DSIFT_EIO).  Pass pixels = NULL to
+ * query w, h, channels; otherwise pixels must hold w*h*channels bytes
+ * (capacity in bytes). */
+int dsift_load_image(const char* path, int32_t* w, int32_t* h, int32_t* channels, uint8_t* pixels,
+                     int64_t capacity);
+/* The float GrayImage load_image returns: n_px pixels of the given channel
+ * count converted on the device (dev_out must be a device pointer). */
+int dsift_ingest_u8(dsift_ctx* ctx, const uint8_t* pixels, int64_t n_px, int channels, int flags,
+                    float* dev_out);
 /* Waits for the last extract; *total = keypoints over all images. */
 int dsift_result_sync(dsift_ctx* ctx, int64_t* total);
 /* [begin, begin+count) of `image` inside the batch result (after sync). */

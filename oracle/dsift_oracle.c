@@ -17,6 +17,7 @@
  */
 #include "dsift_oracle.h"
 
+#include <ctype.h>
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -974,4 +975,84 @@ void dor_value_noise(int w, int h, uint64_t seed, int octaves, int cells, float*
         }
     const double span = hi > lo ? hi - lo : 1.0;
     for (size_t p = 0; p < (size_t)w * h; ++p) out[p] = (float)((out[p] - lo) / span);
+}
+
+/* ------------------------------------------------------------------------- */
+/* load_image (io.cpp:17-81): binary P5/P6, maxval 255.  Returns 0, or -2 with
+ * the reference's std::runtime_error message.  With out == NULL only *w, *h
+ * are set; out receives w*h floats. */
+static int pnm_token(FILE* f, char* tok, int cap) { /* io.cpp:17-35 */
+    int n = 0, ch;
+    while ((ch = fgetc(f)) != EOF) {
+        if (ch == '#') {
+            while ((ch = fgetc(f)) != EOF && ch != '\n') {
+            }
+            continue;
+        }
+        if (isspace(ch)) {
+            if (n) break;
+            continue;
+        }
+        if (n < cap - 1) tok[n++] = (char)ch;
+    }
+    tok[n] = 0;
+    return n;
+}
+
+static int pnm_dim(const char* tok, int* v) { /* io.cpp:37-45: std::stoi, > 0 */
+    const char* p = tok;
+    long long x = 0;
+    int sign = 1, digits = 0;
+    if (*p == '+' || *p == '-') sign = (*p++ == '-') ? -1 : 1;
+    while (*p >= '0' && *p <= '9') {
+        x = x * 10 + (*p++ - '0');
+        ++digits;
+        if (x > 2147483647LL) return 0;
+    }
+    x *= sign;
+    if (!digits || x <= 0) return 0;
+    *v = (int)x;
+    return 1;
+}
+
+int dor_load_image(const char* path, int* w, int* h, float* out) {
+    char tok[64], msg[200];
+    int width, height, maxval;
+    FILE* f = fopen(path, "rb");
+    if (!f) {
+        snprintf(msg, sizeof msg, "cannot open: %.150s", path);
+        return fail(-2, msg);
+    }
+    pnm_token(f, tok, sizeof tok);
+    const int color = strcmp(tok, "P6") == 0;
+    if (!color && strcmp(tok, "P5") != 0) {
+        snprintf(msg, sizeof msg, "image: unsupported format '%s' (want P5/P6)", tok);
+        fclose(f);
+        return fail(-2, msg);
+    }
+    pnm_token(f, tok, sizeof tok);
+    if (!pnm_dim(tok, &width)) { fclose(f); return fail(-2, "image: bad width"); }
+    pnm_token(f, tok, sizeof tok);
+    if (!pnm_dim(tok, &height)) { fclose(f); return fail(-2, "image: bad height"); }
+    pnm_token(f, tok, sizeof tok);
+    if (!pnm_dim(tok, &maxval)) { fclose(f); return fail(-2, "image: bad maxval"); }
+    if (maxval != 255) { fclose(f); return fail(-2, "image: maxval must be 255"); }
+    *w = width;
+    *h = height;
+    if (!out) { fclose(f); return 0; }
+    const size_t pixels = (size_t)width * height, payload = pixels * (color ? 3 : 1);
+    unsigned char* bytes = (unsigned char*)malloc(payload ? payload : 1);
+    const size_t got = fread(bytes, 1, payload, f);
+    fclose(f);
+    if (got != payload) { free(bytes); return fail(-2, "image: truncated payload"); }
+    for (size_t i = 0; i < pixels; ++i) {
+        if (color) { /* io.cpp:71-75 */
+            const double r = bytes[3 * i], g = bytes[3 * i + 1], b = bytes[3 * i + 2];
+            out[i] = (float)((0.299 * r + 0.587 * g + 0.114 * b) * (1.0 / 255.0));
+        } else { /* io.cpp:77-78 */
+            out[i] = (float)(bytes[i] * (1.0 / 255.0));
+        }
+    }
+    free(bytes);
+    return 0;
 }

@@ -90,6 +90,8 @@ int dor_root_sift(float* v, int n);
 int dor_extract(const float* img, int w, int h, const dor_config* c, dor_keypoint** kps,
                 float** desc, int64_t* n);
 void dor_free(void* p);
+/* load_image (io.cpp:49-81): 0, or -2 with the std::runtime_error message. */
+int dor_load_image(const char* path, int* w, int* h, float* out);
 void dor_canonical_sort(dor_keypoint* kps, float* desc, int64_t n);
 int64_t dor_serialize(const dor_keypoint* kps, const float* desc, int64_t n, uint8_t* out,
                       int64_t cap);

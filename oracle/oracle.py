@@ -147,6 +147,18 @@ class Oracle:
         self._f("value_noise")(w, h, C.c_uint64(seed), octaves, cells, out.ctypes.data)
         return out
 
+    # ---- image ingest (io.cpp:49-81) -------------------------------------
+    def load_image(self, path: str) -> np.ndarray:
+        w, h = C.c_int(), C.c_int()
+        fn = self._f("load_image")
+        fn.argtypes = [C.c_char_p, C.c_void_p, C.c_void_p, C.c_void_p]
+        if fn(os.fsencode(path), C.byref(w), C.byref(h), None):
+            raise OracleError(self.error())
+        out = np.empty((h.value, w.value), np.float32)
+        if fn(os.fsencode(path), C.byref(w), C.byref(h), out.ctypes.data):
+            raise OracleError(self.error())
+        return out
+
     # ---- full pipeline -----------------------------------------------------
     def extract(self, img: np.ndarray, cfg: Config | None = None, workers: int = 1):
         img = np.ascontiguousarray(img, np.float32)

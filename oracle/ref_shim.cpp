@@ -123,6 +123,17 @@ int oref_config_validate(const oref_config* c) {
     return guard([&] { to_cfg(c).validate(); return 0; });
 }
 
+// ---- image ingest: io.cpp:49-81 (w, h first with out = NULL) ---------------
+int oref_load_image(const char* path, int* w, int* h, float* out) {
+    return guard([&] {
+        const GrayImage img = load_image(path);
+        *w = img.width;
+        *h = img.height;
+        if (out) std::memcpy(out, img.data.data(), img.data.size() * sizeof(float));
+        return 0;
+    });
+}
+
 // ---- full pipeline: io.cpp:111-142 -----------------------------------------
 int oref_extract(const float* img, int w, int h, const oref_config* c, int workers,
                  void** out) {

@@ -30,7 +30,7 @@ KEYPOINT_DTYPE = np.dtype(
      ("response", "<f4"), ("octave", "<i4"), ("interval", "<i4")])
 DESC_DIM = 128
 
-DSIFT_OK, DSIFT_EINVAL, DSIFT_ECAPACITY, DSIFT_ECUDA, DSIFT_ENOMEM, DSIFT_ESTATE, DSIFT_ERANGE = range(7)
+DSIFT_OK, DSIFT_EINVAL, DSIFT_ECAPACITY, DSIFT_ECUDA, DSIFT_ENOMEM, DSIFT_ESTATE, DSIFT_ERANGE, DSIFT_EIO = range(8)
 INPUT_HOST, INPUT_DEVICE = 0, 1
 
 
@@ -42,6 +42,10 @@ class DsiftError(RuntimeError):
 
 class InvalidArgument(DsiftError, ValueError):
     """std::invalid_argument in the reference."""
+
+
+class ImageIOError(DsiftError, RuntimeError):
+    """std::runtime_error from load_image (io.cpp:49-81)."""
 
 
 class OutOfRange(DsiftError, IndexError):
@@ -134,6 +138,9 @@ def load_library():
         "dsift_set_capacity": ([vp, i64], C.c_int),
         "dsift_extract_batch": ([vp, vp, i32, i32, i32, i32], C.c_int),
         "dsift_extract": ([vp, vp, i32, i32, i32], C.c_int),
+        "dsift_extract_batch_u8": ([vp, vp, i32, i32, i32, i32, i32], C.c_int),
+        "dsift_load_image": ([C.c_char_p, vp, vp, vp, vp, i64], C.c_int),
+        "dsift_ingest_u8": ([vp, vp, i64, i32, i32, vp], C.c_int),
         "dsift_result_sync": ([vp, vp], C.c_int), "dsift_result_range": ([vp, i32, vp, vp], C.c_int),
         "dsift_result_copy": ([vp, vp, vp, vp, vp], C.c_int),
         "dsift_result_device": ([vp, vp, vp, vp, vp], C.c_int),
@@ -170,6 +177,8 @@ def _check(lib, rc: int) -> None:
             raise InvalidArgument(rc, msg)
         if rc == DSIFT_ERANGE:
             raise OutOfRange(rc, msg)
+        if rc == DSIFT_EIO:
+            raise ImageIOError(rc, msg)
         raise DsiftError(rc, f"{lib.dsift_strerror(rc).decode()}: {msg}")
 
 
@@ -253,6 +262,40 @@ class Extractor:
             s, e = int(offs[b]), int(offs[b + 1])
             out.append(FeatureSet(kps[s:e], desc[s:e], u8[s:e] if with_u8 else None))
         return out
+
+    def submit_u8(self, pixels) -> None:
+        """Enqueue 8-bit images converted on the device exactly as load_image does
+        (io.cpp:71-78): [h, w] or [n, h, w] gray (P5), [n, h, w, 3] RGB (P6)."""
+        a = np.ascontiguousarray(pixels, dtype=np.uint8)
+        if a.ndim == 2:
+            a = a[None]
+        if a.ndim == 3:
+            ch = 1
+        elif a.ndim == 4 and a.shape[-1] == 3:
+            ch = 3
+        else:
+            raise InvalidArgument(DSIFT_EINVAL, "pixels must be [n, h, w] or [n, h, w, 3] uint8")
+        self._pin = a
+        _check(self.lib, self.lib.dsift_extract_batch_u8(self.ctx, a.ctypes.data, a.shape[0], a.shape[2],
+                                                         a.shape[1], ch, INPUT_HOST))
+        self.batch = a.shape[0]
+
+    def extract_u8(self, pixels) -> list[FeatureSet]:
+        """extract(load_image(...)) for a batch of 8-bit images."""
+        self.submit_u8(pixels)
+        return self.results()
+
+    def ingest_u8(self, pixels) -> np.ndarray:
+        """The float GrayImage load_image builds from these bytes, converted on the device."""
+        import torch
+        a = np.ascontiguousarray(pixels, dtype=np.uint8)
+        ch = 3 if (a.ndim >= 3 and a.shape[-1] == 3) else 1
+        n_px = a.size // ch
+        out = torch.empty(n_px, dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(self.lib, self.lib.dsift_ingest_u8(self.ctx, a.ctypes.data, n_px, ch, INPUT_HOST,
+                                                  C.c_void_p(out.data_ptr())))
+        shape = a.shape[:-1] if ch == 3 else a.shape
+        return out.cpu().numpy().reshape(shape)
 
     def extract(self, img) -> FeatureSet:
         """detsift::extract (io.cpp:111-142) for one image."""
@@ -400,6 +443,19 @@ class Extractor:
         _check(self.lib, self.lib.dsift_dsp_descriptors(self.ctx, k.ctypes.data, len(k), out.ctypes.data,
                                                         u8.ctypes.data))
         return (out, u8) if with_u8 else out
+
+
+def load_image(path: str) -> np.ndarray:
+    """The 8-bit payload of a binary PNM, parsed like detsift::load_image
+    (io.cpp:49-81; same errors, raised as ImageIOError): [h, w] for P5,
+    [h, w, 3] for P6.  Convert with Extractor.ingest_u8 / extract_u8."""
+    lib = load_library()
+    w, h, ch = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(lib, lib.dsift_load_image(os.fsencode(path), C.byref(w), C.byref(h), C.byref(ch), None, 0))
+    out = np.empty((h.value, w.value, ch.value) if ch.value == 3 else (h.value, w.value), np.uint8)
+    _check(lib, lib.dsift_load_image(os.fsencode(path), C.byref(w), C.byref(h), C.byref(ch),
+                                     out.ctypes.data, out.size))
+    return out
 
 
 def extract(img, cfg: SiftConfig | None = None, device: int = 0) -> FeatureSet:

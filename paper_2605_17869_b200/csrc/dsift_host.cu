@@ -1,3 +1,4 @@
+#include <cctype>
 // dsift_host.cu — host orchestration and the C ABI (include/dsift.h).
 //
 // Replaces detsift::extract (io.cpp:111-142) and its parallel_for fan-out
@@ -210,7 +211,7 @@ struct dsift_ctx {
     Plan plan;
     int batch = 0;            // images in the current pyramid / result
     PyramidDesc pyr{};
-    DevBuf det_aux;
+    DevBuf det_aux, input_u8;
     DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
         pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow,
         ref_states, keep;
@@ -731,6 +732,7 @@ const char* dsift_strerror(int code) {
         case DSIFT_ENOMEM: return "out of memory";
         case DSIFT_ESTATE: return "invalid call order";
         case DSIFT_ERANGE: return "out of range";
+        case DSIFT_EIO: return "image I/O error";
         default: return "unknown error";
     }
 }
@@ -819,6 +821,114 @@ int dsift_extract_batch(dsift_ctx* c, const float* images, int n, int w, int h, 
 
 int dsift_extract(dsift_ctx* c, const float* image, int w, int h, int flags) {
     return dsift_extract_batch(c, image, 1, w, h, flags);
+}
+
+// ---- image ingest (io.cpp:49-81) ---------------------------------------------
+static const float* ingest_to_input(dsift_ctx* c, const uint8_t* pixels, long long n_px, int channels, int flags) {
+    if (channels != 1 && channels != 3) invalid("ingest: channels must be 1 (P5) or 3 (P6)");
+    if (!pixels) invalid("extract: null image pointer");
+    const size_t bytes = (size_t)n_px * channels;
+    const unsigned char* dev_bytes = reinterpret_cast<const unsigned char*>(pixels);
+    if (!(flags & DSIFT_INPUT_DEVICE)) {
+        c->input_u8.ensure(bytes);
+        cuda_check(cudaMemcpyAsync(c->input_u8.as<void>(), pixels, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+        dev_bytes = c->input_u8.as<unsigned char>();
+    }
+    c->input.ensure(sizeof(float) * (size_t)n_px);
+    cuda_check(launch_ingest_u8(dev_bytes, n_px, channels, c->input.as<float>(), c->stream), "ingest");
+    ++c->launches;
+    return c->input.as<float>();
+}
+
+int dsift_extract_batch_u8(dsift_ctx* c, const uint8_t* pixels, int n, int w, int h, int channels, int flags) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (n <= 0) invalid("extract: batch must contain at least one image");
+        if (w <= 0 || h <= 0) invalid("build_scale_space: empty image");
+        set_device(c);
+        const float* dev = ingest_to_input(c, pixels, (long long)n * w * h, channels, flags);
+        extract_batch(c, dev, n, w, h, DSIFT_INPUT_DEVICE);
+    });
+}
+
+int dsift_ingest_u8(dsift_ctx* c, const uint8_t* pixels, int64_t n_px, int channels, int flags, float* dev_out) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (!dev_out) invalid("ingest: null output");
+        set_device(c);
+        const float* dev = ingest_to_input(c, pixels, n_px, channels, flags);
+        cuda_check(cudaMemcpyAsync(dev_out, dev, sizeof(float) * (size_t)n_px, cudaMemcpyDeviceToDevice, c->stream),
+                   "D2D");
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+namespace {
+// next_token / parse_dim (io.cpp:17-45): whitespace-separated tokens, '#'
+// comments to end of line; std::stoi semantics (optional sign, leading
+// digits, trailing junk ignored), value must be > 0.
+std::string pnm_token(FILE* f) {
+    std::string tok;
+    int ch;
+    while ((ch = std::fgetc(f)) != EOF) {
+        if (ch == '#') {
+            while ((ch = std::fgetc(f)) != EOF && ch != '\n') {
+            }
+            continue;
+        }
+        if (std::isspace(ch)) {
+            if (!tok.empty()) return tok;
+            continue;
+        }
+        tok.push_back((char)ch);
+    }
+    return tok;
+}
+int pnm_dim(const std::string& tok, const char* what) {
+    const char* p = tok.c_str();
+    bool ok = false;
+    long long v = 0;
+    int sign = 1;
+    if (*p == '+' || *p == '-') sign = (*p++ == '-') ? -1 : 1;
+    while (*p >= '0' && *p <= '9') {
+        v = v * 10 + (*p++ - '0');
+        ok = true;
+        if (v > 2147483647LL) {
+            ok = false;
+            break;
+        }
+    }
+    v *= sign;
+    if (!ok || v <= 0) throw Error{DSIFT_EIO, std::string("image: bad ") + what};
+    return (int)v;
+}
+}  // namespace
+
+int dsift_load_image(const char* path, int32_t* w, int32_t* h, int32_t* channels, uint8_t* pixels, int64_t capacity) {
+    return guard([&] {
+        if (!path) invalid("load_image: null path");
+        FILE* f = std::fopen(path, "rb");
+        if (!f) throw Error{DSIFT_EIO, std::string("cannot open: ") + path};
+        struct Closer {
+            FILE* f;
+            ~Closer() { std::fclose(f); }
+        } closer{f};
+        const std::string magic = pnm_token(f);
+        if (magic != "P5" && magic != "P6")
+            throw Error{DSIFT_EIO, "image: unsupported format '" + magic + "' (want P5/P6)"};
+        const int ch = magic == "P6" ? 3 : 1;
+        const int ww = pnm_dim(pnm_token(f), "width");
+        const int hh = pnm_dim(pnm_token(f), "height");
+        const int maxval = pnm_dim(pnm_token(f), "maxval");
+        if (maxval != 255) throw Error{DSIFT_EIO, "image: maxval must be 255"};
+        if (w) *w = ww;
+        if (h) *h = hh;
+        if (channels) *channels = ch;
+        if (!pixels) return;
+        const size_t payload = (size_t)ww * hh * ch;
+        if ((int64_t)payload > capacity) invalid("load_image: pixel buffer too small");
+        if (std::fread(pixels, 1, payload, f) != payload) throw Error{DSIFT_EIO, "image: truncated payload"};
+    });
 }
 
 int dsift_result_sync(dsift_ctx* c, int64_t* total) {
