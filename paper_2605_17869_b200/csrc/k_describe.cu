@@ -849,6 +849,17 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
     const int sw = kmax - kmin + 3; // ring columns in use
     const double wm1 = (double)(w - 1), hm1 = (double)(h - 1);
     const int brow = tid >> 5, bcol = (tid >> 3) & 3, bori = tid & 7;
+    // the sample coordinates are monotone in u and in v (each rounding step is),
+    // so the lattice's 4 corners bound every sample: if they all lie in
+    // [0, w-2] x [0, h-2] no sample is undefined or needs the border clamp
+    bool interior = true;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int u = (q & 1) ? kmax + 1 : kmin - 1, v = (q & 2) ? kmax + 1 : kmin - 1;
+        const double px = D_SUB(S.ax[u - kA], S.sv[v - kA]);
+        const double py = D_ADD(S.cysu[u - kA], S.cv[v - kA]);
+        interior = interior && px >= 0.0 && px <= (double)(w - 2) && py >= 0.0 && py <= (double)(h - 2);
+    }
 
     double binacc = 0.0;
     int binlsb = 1 << 20;   // lowest-bit exponent bound of the bin's leaves, + 4*127 + 23
@@ -895,6 +906,40 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 // clamped pixel and are replaced by kUndef
                 const float inv_sw = 1.0f / (float)sw;   // exact row split for idx < 2^16
                 const int ns = (s1 - s0 + 1) * sw;
+                if (interior) {   // every lattice sample in [0, w-2] x [0, h-2]: no tests, no clamps
+                    for (int idx = tid; idx < ns; idx += 2 * kDescThreads) {
+                        int off[2], slot[2];
+                        float fx[2], fy[2];
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const int id = min(idx + j * kDescThreads, ns - 1);
+                            const int rr = (int)(((float)id + 0.5f) * inv_sw), cc = id - rr * sw;
+                            const int vv = s0 + rr, u = ub + cc;
+                            const double px = D_SUB(S.ax[u - kA], S.sv[vv - kA]);
+                            const double py = D_ADD(S.cysu[u - kA], S.cv[vv - kA]);
+                            const int ix = (int)px, iy = (int)py;   // px, py >= 0: truncation = floor
+                            fx[j] = (float)D_SUB(px, (double)ix);
+                            fy[j] = (float)D_SUB(py, (double)iy);
+                            off[j] = iy * pitch + ix;
+                            slot[j] = (vv & (kSRing - 1)) * ring_pitch + cc;
+                        }
+                        float v00[2], v10[2], v01[2], v11[2];
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const float* r0 = img + off[j];
+                            v00[j] = __ldg(r0);
+                            v10[j] = __ldg(r0 + 1);
+                            v01[j] = __ldg(r0 + pitch);
+                            v11[j] = __ldg(r0 + pitch + 1);
+                        }
+#pragma unroll
+                        for (int j = 0; j < 2; ++j) {
+                            const float top = F_ADD(v00[j], F_MUL(fx[j], F_SUB(v10[j], v00[j])));
+                            const float bot = F_ADD(v01[j], F_MUL(fx[j], F_SUB(v11[j], v01[j])));
+                            if (idx + j * kDescThreads < ns) S.ring[slot[j]] = F_ADD(top, F_MUL(fy[j], F_SUB(bot, top)));
+                        }
+                    }
+                } else
                 for (int idx = tid; idx < ns; idx += 2 * kDescThreads) {
                     int off[2], slot[2];
                     float fx[2], fy[2];
@@ -993,7 +1038,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float left = mid[-1], right = mid[1];
                 const float up = S.ring[((v - 1) & (kSRing - 1)) * ring_pitch + col];
                 const float down = S.ring[((v + 1) & (kSRing - 1)) * ring_pitch + col];
-                if (left == kUndef || right == kUndef || up == kUndef || down == kUndef) continue;
+                if (!interior && (left == kUndef || right == kUndef || up == kUndef || down == kUndef)) continue;
                 // describe.cpp:89-100
                 const float du = F_MUL(0.5f, F_SUB(right, left));
                 const float dv = F_MUL(0.5f, F_SUB(down, up));
