@@ -196,6 +196,8 @@ struct Counters {          // one small device block, cleared per batch
     unsigned ref_ticket;
     unsigned n_fixed;     // (keypoint, scale) pairs the stream kernel recomputed exactly in place
     unsigned long long n_kp;   // refined keypoints (compacted)
+    unsigned emit_ticket;      // orientation fan-out tiles
+    unsigned pad3;
 };
 
 }  // namespace dsift
@@ -211,7 +213,7 @@ struct dsift_ctx {
     Plan plan;
     int batch = 0;            // images in the current pyramid / result
     PyramidDesc pyr{};
-    DevBuf det_aux, input_u8;
+    DevBuf det_aux, input_u8, ori_aux;
     DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
         pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow,
         ref_states, keep;
@@ -461,15 +463,25 @@ static void run_orient(dsift_ctx* c, const DevKeypoint* kps, long long n_host, l
     a.hist_out = hist_out;
     const long long nk = n_host >= 0 ? n_host : cap_kp;
     a.n_tiles = (unsigned)((nk + orient_tile_size() - 1) / orient_tile_size());
-    c->ori_states.ensure(sizeof(unsigned long long) * (size_t)std::max(1u, a.n_tiles));
-    cuda_check(cudaMemsetAsync(c->ori_states.as<void>(), 0, sizeof(unsigned long long) * std::max(1u, a.n_tiles),
-                               c->stream), "memset");
-    a.scan.states = c->ori_states.as<unsigned long long>();
     a.scan.ticket = &ctr->ori_ticket;
-    a.scan.total = &ctr->n_ori;
-    a.scan.cap = (unsigned long long)cap_out;
+    // K4b fan-out: per-keypoint peak angles and counts, then a look-back over
+    // tiles of 256 keypoints
+    const size_t nkp = (size_t)std::max<long long>(1, nk);
+    const size_t ang_bytes = (sizeof(float) * nkp * (size_t)a.bins + 255) & ~size_t(255);
+    const size_t cnt_bytes = (sizeof(int) * nkp + 255) & ~size_t(255);
+    c->ori_aux.ensure(ang_bytes + cnt_bytes);
+    a.angles = c->ori_aux.as<float>();
+    a.counts = reinterpret_cast<int*>(c->ori_aux.as<char>() + ang_bytes);
+    const unsigned emit_tiles = (unsigned)((nkp + 255) / 256);
+    c->ori_states.ensure(sizeof(unsigned long long) * (size_t)emit_tiles);
+    cuda_check(cudaMemsetAsync(c->ori_states.as<void>(), 0, sizeof(unsigned long long) * emit_tiles, c->stream),
+               "memset");
+    a.emit_scan.states = c->ori_states.as<unsigned long long>();
+    a.emit_scan.ticket = &ctr->emit_ticket;
+    a.emit_scan.total = &ctr->n_ori;
+    a.emit_scan.cap = (unsigned long long)cap_out;
     cuda_check(launch_orient(a, c->stream), "orient");
-    ++c->launches;
+    c->launches += 2;
 }
 
 static int describe_axis(const dsift_config& cf, const std::vector<double>& dsp, double smax) {

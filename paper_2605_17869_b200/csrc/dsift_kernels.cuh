@@ -63,8 +63,11 @@ struct OrientArgs {
     long long cap;
     unsigned* err;
     float* hist_out;
-    ScanState scan;
+    ScanState scan;        // K4a: work tickets only
     unsigned n_tiles;
+    float* angles;         // [cap_kp][bins] peak angles per keypoint (K4a -> K4b)
+    int* counts;           // [cap_kp] oriented copies per keypoint
+    ScanState emit_scan;   // K4b: fan-out compaction in keypoint order
 };
 cudaError_t launch_orient(const OrientArgs& a, cudaStream_t st);
 int orient_tile_size();

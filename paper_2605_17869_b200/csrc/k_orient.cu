@@ -57,11 +57,10 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
     float* vals = reinterpret_cast<float*>(mask + bins);
     float* hist = vals + 32;
     float* hist2 = hist + bins;
-    // per-CTA: angles[kOriTile][bins], copies[kOriTile]
-    float* ang = reinterpret_cast<float*>(sm_raw + kOriWarps * per_warp_al);
-    int* ncopy = reinterpret_cast<int*>(ang + kOriTile * bins);
+    // peaks go straight to global: angles[k][bins], counts[k] (K4b emits them)
+    float* ang = a.angles;
+    int* ncopy = a.counts;
     __shared__ unsigned ticket_s;
-    __shared__ unsigned long long off_s;
 
     const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
     const unsigned n_tiles = (unsigned)((n + kOriTile - 1) / kOriTile);
@@ -76,8 +75,9 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
         const int slot = warp * kOriPerWarp + j;
         const long long k = k0 + slot;
         const DevKeypoint kp = a.kps[min(k, n - 1 >= 0 ? n - 1 : 0)];
-        if (k >= n || kp.octave < 0) {   // past the end, or a rejected candidate slot
-            if (lane == 0) ncopy[slot] = 0;
+        if (k >= n) continue;
+        if (kp.octave < 0) {   // a rejected candidate slot
+            if (lane == 0) ncopy[k] = 0;
             continue;
         }
         const PyramidDesc& p = a.pyr;
@@ -186,58 +186,73 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                     }
                 }
                 const unsigned pm = __ballot_sync(0xffffffffu, pk);
-                if (pk) ang[slot * bins + total + __popc(pm & ((1u << lane) - 1u))] = angf;
+                if (pk) ang[k * bins + total + __popc(pm & ((1u << lane) - 1u))] = angf;
                 total += __popc(pm);
             }
         }
         if (total == 0) {
-            if (lane == 0) ang[slot * bins] = 0.0f;
+            if (lane == 0) ang[k * bins] = 0.0f;
             total = 1;
         }
-        if (lane == 0) ncopy[slot] = total;
+        if (lane == 0) ncopy[k] = total;
         __syncwarp();
     }
-    __syncthreads();
+    __syncthreads();   // the ticket slot is reused by the next tile
+    }
+}
 
-    // tile fan-out offsets (decoupled look-back in keypoint order)
-    if (threadIdx.x < 32) {
-        int c = threadIdx.x < kOriTile ? ncopy[threadIdx.x] : 0;
+// K4b: oriented copies in keypoint order (the reference's flattened
+// per-candidate slots, io.cpp:117-125).  Tiles of 256 keypoints: a block scan
+// of the copy counts plus a decoupled look-back over ticket-ordered tiles --
+// uniform, tiny tiles, so the look-back never waits on heavy work.
+__global__ void __launch_bounds__(256)
+orient_emit_kernel(const __grid_constant__ OrientArgs a) {
+    __shared__ unsigned ticket_s;
+    __shared__ unsigned long long off_s;
+    __shared__ int warp_tot[8];
+    const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
+    const unsigned n_tiles = (unsigned)((n + 255) / 256);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (;;) {
+        const unsigned t = scan_ticket(a.emit_scan, &ticket_s);
+        if (t >= n_tiles) break;
+        const long long k = (long long)t * 256 + threadIdx.x;
+        const int c = k < n ? a.counts[k] : 0;
         int incl = c;
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const int v = __shfl_up_sync(0xffffffffu, incl, d);
-            if ((int)threadIdx.x >= d) incl += v;
+            if (lane >= d) incl += v;
         }
-        if (threadIdx.x < kOriTile) ncopy[kOriTile + threadIdx.x] = incl - c;   // exclusive
-        if (threadIdx.x == 31) ncopy[2 * kOriTile] = incl;
-    }
-    __syncthreads();
-    const int tile_total = ncopy[2 * kOriTile];
-    const unsigned long long off = scan_exclusive(a.scan, t, (unsigned long long)tile_total, n_tiles, &off_s);
-    if (threadIdx.x == 0 && (long long)(off + tile_total) > a.cap) atomicOr(a.err, kErrOrientedCapacity);
-    for (int slot = warp; slot < kOriTile; slot += kOriWarps) {
-        const long long k = k0 + slot;
-        if (k >= n) continue;
-        const DevKeypoint kp = a.kps[k];
-        if (kp.octave < 0) continue;
-        const int nc = ncopy[slot];
-        const long long dst0 = (long long)off + ncopy[kOriTile + slot];
-        for (int c = lane; c < nc; c += 32) {
-            if (dst0 + c >= a.cap) break;
-            DevKeypoint cp = kp;
-            cp.angle = ang[slot * bins + c];
-            a.out[dst0 + c] = cp;
+        if (lane == 31) warp_tot[warp] = incl;
+        __syncthreads();
+        int warp_off = 0, tile_total = 0;
+        for (int wq = 0; wq < 8; ++wq) {
+            if (wq < warp) warp_off += warp_tot[wq];
+            tile_total += warp_tot[wq];
         }
-    }
-    __syncthreads();   // smem (ang, ncopy, ticket) is reused by the next tile
+        const unsigned long long off = scan_exclusive(a.emit_scan, t, (unsigned long long)tile_total, n_tiles, &off_s);
+        if (threadIdx.x == 0 && (long long)(off + tile_total) > a.cap) atomicOr(a.err, kErrOrientedCapacity);
+        if (c > 0) {
+            const DevKeypoint kp = a.kps[k];
+            const long long dst0 = (long long)off + warp_off + (incl - c);
+            for (int i = 0; i < c; ++i) {
+                if (dst0 + i >= a.cap) break;
+                DevKeypoint cp = kp;
+                cp.angle = a.angles[k * a.bins + i];
+                a.out[dst0 + i] = cp;
+            }
+        }
+        __syncthreads();
     }
 }
+
 
 size_t orient_smem_bytes(int bins, int depth) {
     const size_t per_warp = sizeof(double) * bins * depth + sizeof(unsigned) * bins * 2 +
                             sizeof(float) * 32 + sizeof(float) * 2 * bins;
     const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
-    return kOriWarps * per_warp_al + sizeof(float) * kOriTile * bins + sizeof(int) * (2 * kOriTile + 1);
+    return kOriWarps * per_warp_al;
 }
 
 cudaError_t launch_orient(const OrientArgs& a, cudaStream_t st) {
@@ -252,6 +267,11 @@ cudaError_t launch_orient(const OrientArgs& a, cudaStream_t st) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const unsigned grid = (unsigned)std::min<long long>((long long)a.n_tiles, (long long)sms * std::max(1, per_sm));
     orient_kernel<<<std::max(1u, grid), kOriWarps * 32, smem, st>>>(a);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const long long nk = (long long)a.n_tiles * kOriTile;
+    const int grid2 = (int)std::max<long long>(1, std::min<long long>((nk + 255) / 256, (long long)sms * 8));
+    orient_emit_kernel<<<grid2, 256, 0, st>>>(a);
     return cudaGetLastError();
 }
 
