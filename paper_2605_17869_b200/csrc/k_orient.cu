@@ -46,16 +46,19 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
     const int bins = a.bins;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // per-warp: node[bins][depth] doubles | count[bins] | mask[bins] | vals[32] | hist[2][bins]
-    const size_t per_warp = sizeof(double) * bins * a.depth + sizeof(unsigned) * bins * 2 +
-                            sizeof(float) * 32 + sizeof(float) * 2 * bins;
-    const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
+    // per-warp: union{ acc[bins][32] doubles (certified pass) | node[bins][depth]
+    // doubles, count[bins], mask[bins], vals[32] (exact pass) } | hist[2][bins]
+    const size_t exact_bytes = sizeof(double) * bins * a.depth + sizeof(unsigned) * bins * 2 + sizeof(float) * 32;
+    const size_t acc_bytes = sizeof(double) * bins * 32;
+    const size_t uni = ((exact_bytes > acc_bytes ? exact_bytes : acc_bytes) + 15) & ~size_t(15);
+    const size_t per_warp_al = (uni + sizeof(float) * 2 * bins + 15) & ~size_t(15);
     unsigned char* wbase = sm_raw + warp * per_warp_al;
+    double* acc = reinterpret_cast<double*>(wbase);
     double* node = reinterpret_cast<double*>(wbase);
     unsigned* cnt = reinterpret_cast<unsigned*>(node + bins * a.depth);
     unsigned* mask = cnt + bins;
     float* vals = reinterpret_cast<float*>(mask + bins);
-    float* hist = vals + 32;
+    float* hist = reinterpret_cast<float*>(wbase + uni);
     float* hist2 = hist + bins;
     // peaks go straight to global: angles[k][bins], counts[k] (K4b emits them)
     float* ang = a.angles;
@@ -96,15 +99,10 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
         const int nx = xb - xa + 1, ny = yb - ya + 1;
         const int npx = (nx > 0 && ny > 0) ? nx * ny : 0;
 
-        for (int bb = lane; bb < bins; bb += 32) {
-            cnt[bb] = 0;
-            mask[bb] = 0;
-        }
-        __syncwarp();
-        for (int base = 0; base < npx; base += 32) {
-            const int q = base + lane;
-            int bin = -1;
-            float val = 0.0f;
+        // one window pixel q (row-major, orient.cpp:40-58): its bin and leaf value
+        auto pixel = [&](int q, int& bin, float& val) {
+            bin = -1;
+            val = 0.0f;
             if (q < npx) {
                 const int x = xa + q % nx, y = ya + q / nx;
                 const float* r0 = img + (long long)y * od.pitch;
@@ -124,24 +122,81 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 const float wgt = (float)dsift_exp_mid(arg);
                 val = F_MUL(mag, wgt);
             }
-            const unsigned grp = __match_any_sync(0xffffffffu, bin);
-            if (bin >= 0 && lane == __ffs(grp) - 1) mask[bin] = grp;
-            vals[lane] = val;
-            __syncwarp();
-            for (int bb = lane; bb < bins; bb += 32) {
-                unsigned m = mask[bb];
-                if (!m) continue;
-                mask[bb] = 0;
-                while (m) {
-                    const int l = __ffs(m) - 1;
-                    m &= m - 1;
-                    tree_push_smem(node + bb * a.depth, &cnt[bb], (double)vals[l]);
+        };
+
+        // Certified pass: each lane sums its pixels' leaves per bin in FP64
+        // (lane-private slots, no serialisation), the bins are folded over the
+        // 32 lanes in a fixed order, and each bin's float is proven equal to
+        // the reference's pairwise tree (detsum.cpp:19-31) by the exact-span or
+        // rounding-interval test of the descriptor kernels.  Any unproven bin
+        // sends the keypoint through the exact binary-counter pass below.
+        for (int bb = 0; bb < bins; ++bb) acc[bb * 32 + lane] = 0.0;
+        int emin = 1 << 20;   // lowest biased exponent of this lane's nonzero leaves
+        for (int base = 0; base < npx; base += 32) {
+            int bin;
+            float val;
+            pixel(base + lane, bin, val);
+            if (bin >= 0) {
+                double* slot = acc + bin * 32 + lane;
+                *slot = *slot + (double)val;
+                if (val > 0.0f) {
+                    const int e = (int)((__float_as_uint(val) >> 23) & 0xffu);
+                    emin = min(emin, e ? e : -22);
                 }
             }
-            __syncwarp();
         }
-        for (int bb = lane; bb < bins; bb += 32)
-            hist[bb] = (float)tree_result_smem(node + bb * a.depth, cnt[bb]);
+#pragma unroll
+        for (int d = 16; d; d >>= 1) emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, d));
+        __syncwarp();
+        bool ok = true;
+        {
+            const int steps = (npx + 31) / 32;
+            const double e = (double)(steps + 32 + a.depth + 64) * 0x1p-53;
+            for (int bb = lane; bb < bins; bb += 32) {
+                double sum = 0.0;
+                for (int l = 0; l < 32; ++l) sum = sum + acc[bb * 32 + l];
+                const int top = (int)((__double_as_longlong(sum) >> 52) & 0x7ff) - 1023;
+                float res;
+                if (sum == 0.0 || top - (emin - 150) <= 52) {   // every partial sum exact
+                    res = __double2float_rn(sum);
+                } else {
+                    res = __double2float_rn(sum * (1.0 - e));
+                    ok = ok && (res == __double2float_rn(sum * (1.0 + e)));
+                }
+                hist[bb] = res;
+            }
+        }
+        if (!__all_sync(0xffffffffu, ok)) {
+            // exact pass: bins fed in scan order through binary-counter trees
+            __syncwarp();
+            for (int bb = lane; bb < bins; bb += 32) {
+                cnt[bb] = 0;
+                mask[bb] = 0;
+            }
+            __syncwarp();
+            for (int base = 0; base < npx; base += 32) {
+                int bin;
+                float val;
+                pixel(base + lane, bin, val);
+                const unsigned grp = __match_any_sync(0xffffffffu, bin);
+                if (bin >= 0 && lane == __ffs(grp) - 1) mask[bin] = grp;
+                vals[lane] = val;
+                __syncwarp();
+                for (int bb = lane; bb < bins; bb += 32) {
+                    unsigned m = mask[bb];
+                    if (!m) continue;
+                    mask[bb] = 0;
+                    while (m) {
+                        const int l = __ffs(m) - 1;
+                        m &= m - 1;
+                        tree_push_smem(node + bb * a.depth, &cnt[bb], (double)vals[l]);
+                    }
+                }
+                __syncwarp();
+            }
+            for (int bb = lane; bb < bins; bb += 32)
+                hist[bb] = (float)tree_result_smem(node + bb * a.depth, cnt[bb]);
+        }
         __syncwarp();
         if (a.hist_out)
             for (int bb = lane; bb < bins; bb += 32) a.hist_out[k * bins + bb] = hist[bb];
@@ -249,9 +304,10 @@ orient_emit_kernel(const __grid_constant__ OrientArgs a) {
 
 
 size_t orient_smem_bytes(int bins, int depth) {
-    const size_t per_warp = sizeof(double) * bins * depth + sizeof(unsigned) * bins * 2 +
-                            sizeof(float) * 32 + sizeof(float) * 2 * bins;
-    const size_t per_warp_al = (per_warp + 15) & ~size_t(15);
+    const size_t exact_bytes = sizeof(double) * bins * depth + sizeof(unsigned) * bins * 2 + sizeof(float) * 32;
+    const size_t acc_bytes = sizeof(double) * bins * 32;
+    const size_t uni = ((exact_bytes > acc_bytes ? exact_bytes : acc_bytes) + 15) & ~size_t(15);
+    const size_t per_warp_al = (uni + sizeof(float) * 2 * bins + 15) & ~size_t(15);
     return kOriWarps * per_warp_al;
 }
 
