@@ -734,8 +734,11 @@ describe_fast_kernel(const __grid_constant__ DescArgs a) {
 constexpr int kSRing = 32;                 // sample rows resident (power of two)
 constexpr int kSMaxPassRows = kSRing - 2;  // lattice rows per pass (+2 guard rows)
 constexpr int kSLanes = 125;               // accumulation lanes: 5 cells x 25 parts ... 25 x 5
-constexpr int kSSlotStride = 129;          // doubles per slot-entry row (spreads the fold over banks)
-constexpr int kSSlotE = 8 * kSSlotStride;  // stride between (ri, ci) groups
+// Lane slots: double slot[lane >> 4][32 entries (ri, ci, o)][lane & 15].  A
+// lane's 32 entries all sit in bank pair (lane & 15), so the random-entry
+// read-modify-writes of a half-warp never conflict.
+constexpr int kSSlotE = 8 * 16;            // stride between (ri, ci) groups of one lane
+__device__ __forceinline__ int slot_index(int lane, int e) { return ((lane >> 4) * 32 + e) * 16 + (lane & 15); }
 
 struct StreamSmem {
     double* ax;     // cx + cos*k        [span] indexed k - kA
@@ -743,7 +746,7 @@ struct StreamSmem {
     double* sv;     // sin*k
     double* cv;     // cos*k
     double* q2;     // (k/bw)^2
-    double* slot;   // [32 entries (ri, ci, o)][kSSlotStride lanes]
+    double* slot;   // [8 half-warps][32 entries (ri, ci, o)][16 lanes]
     float2* wp;     // (1 - frac, frac): weight of histogram index floor(bin) + {0, 1}
     int* ew;        // min biased exponent (>= 1) of the nonzero weights in wp
     float* ring;    // [kSRing][ring_pitch] bilinear samples, -1 = undefined
@@ -993,17 +996,21 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                     const int Cc = bcol - 1 + dc;      // ci = 1 - dc
                     const int cell = (Rc - pRa) * 5 + (Cc + 1);
                     const int e = ((1 - dr) * 2 + (1 - dc)) * 8 + bori;
-                    const double* sp = S.slot + e * kSSlotStride + cell * pP;
-                    const int* lp = S.lanelsb + cell * pP;
+                    const int l0 = cell * pP;
+                    // lanes in a rotated (per-orientation) fixed order: the 8
+                    // orientations of one cell hit 8 different bank pairs
+                    int qq = bori % pP;
                     int q = 0;
                     for (; q + 1 < pP; q += 2) {
-                        se = se + sp[q];
-                        so = so + sp[q + 1];
-                        lm = min(lm, min(lp[q], lp[q + 1]));
+                        const int qa = qq, qb = (qq + 1 == pP) ? 0 : qq + 1;
+                        qq = (qb + 1 == pP) ? 0 : qb + 1;
+                        se = se + S.slot[slot_index(l0 + qa, e)];
+                        so = so + S.slot[slot_index(l0 + qb, e)];
+                        lm = min(lm, min(S.lanelsb[l0 + qa], S.lanelsb[l0 + qb]));
                     }
                     if (q < pP) {
-                        se = se + sp[q];
-                        lm = min(lm, lp[q]);
+                        se = se + S.slot[slot_index(l0 + qq, e)];
+                        lm = min(lm, S.lanelsb[l0 + qq]);
                     }
                 }
             }
@@ -1025,9 +1032,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 rv0 = r0;
                 if (r1 >= r0 && nc > 0) npts = (r1 - r0 + 1) * nc;
             }
-            double* my = S.slot + tid;
+            double* my = S.slot + slot_index(tid, 0);
 #pragma unroll
-            for (int e = 0; e < 32; ++e) my[e * kSSlotStride] = 0.0;
+            for (int e = 0; e < 32; ++e) my[e * 16] = 0.0;
             int lmin = 1 << 20;
             const float inv_nc = 1.0f / (float)max(nc, 1);
             for (int pi = part; pi < npts; pi += P) {
@@ -1061,8 +1068,8 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float a0 = F_MUL(val, wr.x), a1 = F_MUL(val, wr.y);
                 const float t00 = F_MUL(a0, wc.x), t01 = F_MUL(a0, wc.y);
                 const float t10 = F_MUL(a1, wc.x), t11 = F_MUL(a1, wc.y);
-                double* pa = my + (o0 & 7) * kSSlotStride;
-                double* pb = my + ((o0 + 1) & 7) * kSSlotStride;
+                double* pa = my + (o0 & 7) * 16;
+                double* pb = my + ((o0 + 1) & 7) * 16;
                 double x0 = pa[0], x1 = pb[0], x2 = pa[kSSlotE], x3 = pb[kSSlotE];
                 double x4 = pa[2 * kSSlotE], x5 = pb[2 * kSSlotE], x6 = pa[3 * kSSlotE], x7 = pb[3 * kSSlotE];
                 x0 = x0 + (double)F_MUL(t00, go);
@@ -1141,7 +1148,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.q2 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
-    S.slot = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * 32 * kSSlotStride;
+    S.slot = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * 32 * kDescThreads;
     S.wp = reinterpret_cast<float2*>(pbuf); pbuf += sizeof(float2) * SP;
     S.ew = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * SP;
     S.ring = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kSRing * RP;
@@ -1197,7 +1204,7 @@ size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp)
 
 size_t describe_stream_smem_bytes(int max_span, int n_dsp) {
     const size_t SP = (size_t)max_span, RP = (SP - 6) & ~(size_t)1;
-    return sizeof(double) * 5 * SP + sizeof(double) * 32 * kSSlotStride + sizeof(float2) * SP + sizeof(int) * SP +
+    return sizeof(double) * 5 * SP + sizeof(double) * 32 * kDescThreads + sizeof(float2) * SP + sizeof(int) * SP +
            sizeof(float) * kSRing * RP + sizeof(float) * kDescDim * n_dsp + sizeof(int) * kDescThreads;
 }
 
