@@ -739,6 +739,12 @@ constexpr int kSLanes = 125;               // accumulation lanes: 5 cells x 25 p
 // read-modify-writes of a half-warp never conflict.
 constexpr int kSSlotE = 8 * 16;            // stride between (ri, ci) groups of one lane
 __device__ __forceinline__ int slot_index(int lane, int e) { return ((lane >> 4) * 32 + e) * 16 + (lane & 15); }
+// Ring row pitch: >= the widest ring row 2*ceil(2.5 bw) + 1 (host: max_span = that
+// + 7), and = 16 (mod 32) so two adjacent rows fall in opposite bank halves.
+__host__ __device__ __forceinline__ int ring_pitch_for(int max_span) {
+    const int need = max_span - 7;
+    return need + ((16 - need % 32) + 32) % 32;
+}
 
 struct StreamSmem {
     double* ax;     // cx + cos*k        [span] indexed k - kA
@@ -1139,7 +1145,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     __shared__ double red[4];
     __shared__ int misc[32];
     const int SP = a.max_span;
-    const int RP = (SP - 6) & ~1;   // >= the widest ring row 2*ceil(2.5 bw) + 1 (host: SP = that + 7)
+    const int RP = ring_pitch_for(SP);
     StreamSmem S;
     unsigned char* pbuf = sm;
     S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * a.n_dsp;
@@ -1203,7 +1209,7 @@ size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp)
 }
 
 size_t describe_stream_smem_bytes(int max_span, int n_dsp) {
-    const size_t SP = (size_t)max_span, RP = (SP - 6) & ~(size_t)1;
+    const size_t SP = (size_t)max_span, RP = (size_t)ring_pitch_for(max_span);
     return sizeof(double) * 5 * SP + sizeof(double) * 32 * kDescThreads + sizeof(float2) * SP + sizeof(int) * SP +
            sizeof(float) * kSRing * RP + sizeof(float) * kDescDim * n_dsp + sizeof(int) * kDescThreads;
 }
