@@ -334,6 +334,12 @@ class Extractor:
     def libm_probe(self, mode: int, inputs: np.ndarray) -> np.ndarray:
         """Device restatements of atan2f (mode 0, inputs [n, 2] float32 (y, x)),
         exp (mode 1, float64) and sin/cos (mode 2, float64 -> [n, 2] (sin, cos))."""
+        if mode == 3:   # inputs = (seed, n): [mismatches, first failing (y << 32 | x) bits]
+            seed, n = inputs
+            a = np.array([seed], np.uint64)
+            out = np.zeros(2, np.uint64)
+            _check(self.lib, self.lib.dsift_libm_probe(self.ctx, 3, a.ctypes.data, int(n), out.ctypes.data))
+            return out
         if mode == 0:
             a = np.ascontiguousarray(inputs, np.float32).reshape(-1, 2)
             out = np.empty(len(a), np.float32)

@@ -1332,8 +1332,21 @@ int64_t dsift_kernel_launches(dsift_ctx* c) { return c ? c->launches : 0; }
 int dsift_libm_probe(dsift_ctx* c, int mode, const void* in, int64_t n, void* out) {
     return guard([&] {
         if (!c || !in || !out) invalid("null argument");
-        if (mode < 0 || mode > 2) invalid("libm_probe: mode must be 0 (atan2f), 1 (exp) or 2 (sincos)");
+        if (mode < 0 || mode > 3) invalid("libm_probe: mode must be 0 (atan2f), 1 (exp), 2 (sincos) or 3 (division)");
         set_device(c);
+        if (mode == 3) {   // in = uint64 seed, n = operand pairs, out = uint64[2] (mismatches, first)
+            void *din = nullptr, *dout = nullptr;
+            cuda_check(cudaMalloc(&din, 8), "cudaMalloc");
+            cuda_check(cudaMalloc(&dout, 16), "cudaMalloc");
+            cuda_check(cudaMemcpy(din, in, 8, cudaMemcpyHostToDevice), "H2D");
+            cuda_check(cudaMemset(dout, 0, 16), "memset");
+            cuda_check(launch_libm_probe(mode, din, n, dout, c->stream), "probe");
+            cuda_check(cudaStreamSynchronize(c->stream), "sync");
+            cuda_check(cudaMemcpy(out, dout, 16, cudaMemcpyDeviceToHost), "D2H");
+            cudaFree(din);
+            cudaFree(dout);
+            return;
+        }
         const size_t isz = mode == 0 ? 8 : 8, osz = mode == 0 ? 4 : (mode == 1 ? 8 : 16);
         void *din = nullptr, *dout = nullptr;
         cuda_check(cudaMalloc(&din, isz * (size_t)std::max<int64_t>(n, 1)), "cudaMalloc");

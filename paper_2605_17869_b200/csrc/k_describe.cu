@@ -27,6 +27,10 @@
 #include "dsift_math.cuh"
 #include "dsift_tree.cuh"
 
+#ifndef DSIFT_ABL
+#define DSIFT_ABL 0   // timing ablations of the stream kernel (never set in the product build)
+#endif
+
 namespace dsift {
 
 constexpr int kDescThreads = 128;
@@ -1056,7 +1060,11 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float du = F_MUL(0.5f, F_SUB(right, left));
                 const float dv = F_MUL(0.5f, F_SUB(down, up));
                 const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
+#if DSIFT_ABL == 2
+                float theta = fabsf(dv) + fabsf(du);
+#else
                 float theta = dsift_atan2f(dv, du);
+#endif
                 if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
                 if (isnan(theta)) {   // reference: negative bin -> std::out_of_range
                     atomicOr(a.err, kErrHistogramRange);
@@ -1065,7 +1073,11 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
                 if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
                 const double arg = D_MUL(-D_ADD(S.q2[u - kA], S.q2[v - kA]), 0.125);
+#if DSIFT_ABL == 3
+                const float val = F_MUL(mag, (float)arg);
+#else
                 const float val = F_MUL(mag, (float)dsift_exp_mid(arg));
+#endif
                 const int o0 = (int)floor(obin);
                 const float fo = (float)D_SUB(obin, (double)o0);
                 const float go = F_SUB(1.0f, fo);
@@ -1076,6 +1088,10 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float t10 = F_MUL(a1, wc.x), t11 = F_MUL(a1, wc.y);
                 double* pa = my + (o0 & 7) * 16;
                 double* pb = my + ((o0 + 1) & 7) * 16;
+#if DSIFT_ABL == 1
+                lmin += __float_as_int(F_MUL(t00, go)) ^ __float_as_int(F_MUL(t11, fo)) ^ __float_as_int(t01) ^ __float_as_int(t10);
+                continue;
+#endif
                 double x0 = pa[0], x1 = pb[0], x2 = pa[kSSlotE], x3 = pb[kSSlotE];
                 double x4 = pa[2 * kSSlotE], x5 = pb[2 * kSSlotE], x6 = pa[3 * kSSlotE], x7 = pb[3 * kSSlotE];
                 x0 = x0 + (double)F_MUL(t00, go);

@@ -149,6 +149,16 @@ def test_device_libm_matches_host():
         assert sc[:, 0].tobytes() == ts.tobytes() and sc[:, 1].tobytes() == tc.tobytes()
 
 
+def test_fast_division_exhaustive():
+    # ds_fdiv_inrange (the atan2f fast path's division, no FCHK) equals the IEEE
+    # __fdiv_rn on ~4e9 operand pairs of its domain (random exponents in
+    # [-100, 62] at most 60 apart, every 4th quotient near a multiple of 0.5)
+    with ds.Extractor() as ex:
+        for seed in (1, 2):
+            bad, first = ex.libm_probe(3, (seed, 2_000_000_000))
+            assert bad == 0, (int(bad), hex(int(first)))
+
+
 # ---- determinism, batching, export ----------------------------------------------------
 def test_determinism_batch_single_and_exact_path(port):
     imgs = np.stack([port.value_noise(320, 240, 100 + i, 5, 16) for i in range(4)])
