@@ -87,7 +87,8 @@ static void validate(const dsift_config& c) {
         invalid("config: orientation_peak_ratio must be in (0,1]");
     if (c.num_octaves < 0) invalid("config: num_octaves must be >= 0 (0 = auto)");
     // device-implementation limits (explicit, never silent)
-    if (c.intervals + 3 > kMaxLevels) invalid("config: intervals_per_octave too large for this build");
+    if (c.intervals + 3 > kMaxLevels || c.intervals > 8)   // K2 packs 4 rows x s levels per thread in 32 bits
+        invalid("config: intervals_per_octave too large for this build (max 8)");
     if (c.n_dsp_scales > kMaxDsp) invalid("config: too many dsp_scales for this build");
     if (c.orientation_bins > kMaxOriBins) invalid("config: orientation_bins too large for this build");
 }
@@ -390,12 +391,12 @@ static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
     }
     {   // count -> scan -> emit scratch: masks, counts, offsets, CUB temp
         const size_t nt = std::max(1u, a.n_tiles);
-        const size_t masks = (sizeof(unsigned short) * 256 * nt + 255) & ~size_t(255);
+        const size_t masks = (sizeof(unsigned) * 256 * nt + 255) & ~size_t(255);
         const size_t cnts = (sizeof(unsigned) * nt + 255) & ~size_t(255);
         a.scan_temp_bytes = detect_scan_temp_bytes(a.n_tiles);
         c->det_aux.ensure(masks + 2 * cnts + a.scan_temp_bytes + 256);
         char* base = c->det_aux.as<char>();
-        a.hit_masks = reinterpret_cast<unsigned short*>(base);
+        a.hit_masks = reinterpret_cast<unsigned*>(base);
         a.tile_counts = reinterpret_cast<unsigned*>(base + masks);
         a.tile_offsets = reinterpret_cast<unsigned*>(base + masks + cnts);
         a.scan_temp = base + masks + 2 * cnts;

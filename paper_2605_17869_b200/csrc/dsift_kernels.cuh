@@ -40,7 +40,7 @@ struct DetectArgs {
     unsigned* err;
     ScanState scan;
     // count -> scan -> emit compaction of the extrema (no cross-tile waiting)
-    unsigned short* hit_masks;   // [n_tiles][256] per-thread (level, row) hit bits
+    unsigned* hit_masks;         // [n_tiles][256] per-thread (level, row) hit bits (s <= 8)
     unsigned* tile_counts;       // [n_tiles]
     unsigned* tile_offsets;      // [n_tiles] exclusive scan of tile_counts
     void* scan_temp;

@@ -92,7 +92,7 @@ __device__ bool refine_candidate(const DetectArgs& a, int b, int o, int x, int y
 // K2a: one CTA per (image, octave, 32x32 tile) in a fixed tile order; every
 // thread records which of its (level, row) positions are extrema as a 12-bit
 // mask and the tile publishes its count.  No tile ever waits on another.
-__global__ void __launch_bounds__(kDetThreads)
+__global__ void __launch_bounds__(kDetThreads, 4)
 detect_count_kernel(const __grid_constant__ DetectArgs a) {
     extern __shared__ __align__(16) float lv_s[];   // [s+2][34][kDetPitch]
     __shared__ int warp_tot[kDetThreads / 32];
@@ -130,45 +130,73 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
 
-    const int lx = lane, ly0 = threadIdx.x >> 5;
-    auto S = [&](int l, int xl, int yl) -> float {
-        return lv_s[(l * kDetHalo + yl) * kDetPitch + xl];
-    };
-    // strictly_extremal (detect.cpp:11-28) on the staged tile
-    auto extremal = [&](int i, int xl, int yl, float v, bool is_max) -> bool {
+    // strictly_extremal (detect.cpp:11-28), branch-free: thread (lane, g) owns
+    // column lane and the 4 rows 4g..4g+3 of the tile.  Per level it keeps the
+    // max / min of each 3-pixel row segment of rows 4g-1..4g+4; a candidate's
+    // 26-neighbour max is max(its level's 8 neighbours, the 3x3 of the levels
+    // above and below), v > that (is_max) or v < the min (fmaxf/fminf ignore a
+    // NaN neighbour exactly like the reference's failed comparisons).
+    const int lx = lane, g = threadIdx.x >> 5;
+    float hx[3][6], hn[3][6];         // row-segment max / min of levels i-1, i, i+1
+    float cc[4], cl[4], cr[4];        // level i: centre, left, right of rows 4g..4g+3
+    auto load_level = [&](int l, float (&mx)[6], float (&mn)[6], bool keep_centre) {
+        const float* base = lv_s + (l * kDetHalo + 4 * g) * kDetPitch + lx;
 #pragma unroll
-        for (int dyy = -1; dyy <= 1; ++dyy)
-#pragma unroll
-            for (int dxx = -1; dxx <= 1; ++dxx) {
-                const float nb = S(i - 1, xl + dxx, yl + dyy), na = S(i + 1, xl + dxx, yl + dyy);
-                if (is_max ? (nb >= v || na >= v) : (nb <= v || na <= v)) return false;
-                if (dxx == 0 && dyy == 0) continue;
-                const float nm = S(i, xl + dxx, yl + dyy);
-                if (is_max ? nm >= v : nm <= v) return false;
+        for (int r = 0; r < 6; ++r) {
+            const float a0 = base[r * kDetPitch], a1 = base[r * kDetPitch + 1], a2 = base[r * kDetPitch + 2];
+            mx[r] = fmaxf(fmaxf(a0, a1), a2);
+            mn[r] = fminf(fminf(a0, a1), a2);
+            if (keep_centre && r >= 1 && r <= 4) {
+                cl[r - 1] = a0;
+                cc[r - 1] = a1;
+                cr[r - 1] = a2;
             }
-        return true;
+        }
     };
-    // bit = level-major index (i - 1) * 4 + q  (detect.cpp:38-70 candidate tests)
     unsigned hits = 0;
-    {
-        int bit = 0;
-        for (int i = 1; i <= s; ++i) {
-            for (int q = 0; q < kDetTile / 8; ++q, ++bit) {
-                const int ly = ly0 + 8 * q;
-                const int x = xs + lx, y = ys + ly;
-                if (x > w - 2 || y > h - 2) continue;
-                const float v = S(i, lx + 1, ly + 1);
-                if (!(fabsf(v) > a.pre_gate)) continue;   // float pre-gate (detect.cpp:35)
-                if (!extremal(i, lx + 1, ly + 1, v, v > 0.0f)) continue;
-                hits |= 1u << bit;
+    load_level(0, hx[0], hn[0], false);
+    load_level(1, hx[1], hn[1], true);
+    const int x = xs + lx;
+    for (int i = 1; i <= s; ++i) {
+        load_level(i + 1, hx[2], hn[2], false);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = q + 1;   // row in the 6-row window
+            const float v = cc[q];
+            const float m8 = fmaxf(fmaxf(hx[1][r - 1], hx[1][r + 1]), fmaxf(cl[q], cr[q]));
+            const float n8 = fminf(fminf(hn[1][r - 1], hn[1][r + 1]), fminf(cl[q], cr[q]));
+            const float mo = fmaxf(fmaxf(fmaxf(hx[0][r - 1], hx[0][r]), hx[0][r + 1]),
+                                   fmaxf(fmaxf(hx[2][r - 1], hx[2][r]), hx[2][r + 1]));
+            const float no = fminf(fminf(fminf(hn[0][r - 1], hn[0][r]), hn[0][r + 1]),
+                                   fminf(fminf(hn[2][r - 1], hn[2][r]), hn[2][r + 1]));
+            const bool ext = (v > 0.0f) ? (v > fmaxf(m8, mo)) : (v < fminf(n8, no));
+            const int y = ys + 4 * g + q;
+            // float pre-gate |v| > 0.5 * ct / s (detect.cpp:35); interior pixels only
+            const bool hit = ext && (fabsf(v) > a.pre_gate) && x <= w - 2 && y <= h - 2;
+            hits |= (hit ? 1u : 0u) << ((i - 1) * 4 + q);
+        }
+        if (i < s) {   // slide the level window: i -> i-1, i+1 -> i (+ its centres)
+#pragma unroll
+            for (int r = 0; r < 6; ++r) {
+                hx[0][r] = hx[1][r];
+                hn[0][r] = hn[1][r];
+                hx[1][r] = hx[2][r];
+                hn[1][r] = hn[2][r];
+            }
+            const float* base = lv_s + ((i + 1) * kDetHalo + 4 * g) * kDetPitch + lx;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                cl[q] = base[(q + 1) * kDetPitch];
+                cc[q] = base[(q + 1) * kDetPitch + 1];
+                cr[q] = base[(q + 1) * kDetPitch + 2];
             }
         }
     }
-    a.hit_masks[(size_t)t * kDetThreads + threadIdx.x] = (unsigned short)hits;
+    a.hit_masks[(size_t)t * kDetThreads + threadIdx.x] = hits;
     int cnt = __popc(hits);
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, d);
-    if (lane == 0) warp_tot[ly0] = cnt;
+    if (lane == 0) warp_tot[g] = cnt;
     __syncthreads();
     if (threadIdx.x == 0) {
         int tot = 0;
@@ -201,11 +229,12 @@ detect_emit_kernel(const __grid_constant__ DetectArgs a) {
     const int tile = rr - a.oct_tile_base[o];
     const int xs = 1 + (tile % od.tiles_x) * kDetTile;
     const int ys = 1 + (tile / od.tiles_x) * kDetTile;
-    const uint4 m4 = reinterpret_cast<const uint4*>(a.hit_masks + (size_t)t * kDetThreads)[lane];   // 8 x u16
-    const unsigned mw[4] = {m4.x, m4.y, m4.z, m4.w};
+    const uint4* mp = reinterpret_cast<const uint4*>(a.hit_masks + (size_t)t * kDetThreads) + 2 * lane;
+    const uint4 ma = mp[0], mb = mp[1];
+    const unsigned mw[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};   // count threads 8j..8j+7
     int count = 0;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) count += __popc(mw[k]);
+    for (int k = 0; k < 8; ++k) count += __popc(mw[k]);
     int incl = count;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -217,13 +246,13 @@ detect_emit_kernel(const __grid_constant__ DetectArgs a) {
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         const int th = lane * 8 + k;                 // the count kernel's thread index
-        const int lx = th & 31, ly0 = th >> 5;
-        unsigned hits = (mw[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+        const int lx = th & 31, g = th >> 5;
+        unsigned hits = mw[k];
         while (hits) {
             const int bit = __ffs(hits) - 1;
             hits &= hits - 1;
-            const int i = 1 + bit / (kDetTile / 8), q = bit % (kDetTile / 8);
-            const int x = xs + lx, y = ys + ly0 + 8 * q;
+            const int i = 1 + (bit >> 2), q = bit & 3;
+            const int x = xs + lx, y = ys + 4 * g + q;
             if ((long long)slot < a.cap) {
                 const float v = __ldg(dogb + (long long)i * od.level_stride + (long long)y * od.pitch + x);
                 DevCandidate c = {b, o, i, y, x, v > 0.0f ? 1 : 0};

@@ -55,6 +55,7 @@ def test_full_dumps_bitwise(golden):
 
 # ---- stage by stage ------------------------------------------------------------------
 STAGE_CASES = [(96, 64, 3, 6, {}), (160, 120, 7, 8, {"upsample_pixel_limit": 0}), (123, 77, 13, 9, {"intervals": 4}),
+               (140, 100, 21, 10, {"intervals": 7}),
                (250, 180, 31, 12, {"orientation_bins": 18})]
 
 
