@@ -27,9 +27,6 @@
 #include "dsift_math.cuh"
 #include "dsift_tree.cuh"
 
-#ifndef DSIFT_ABL
-#define DSIFT_ABL 0   // timing ablations of the stream kernel (never set in the product build)
-#endif
 
 namespace dsift {
 
@@ -755,7 +752,7 @@ struct StreamSmem {
     double* cysu;   // cy + sin*k
     double* sv;     // sin*k
     double* cv;     // cos*k
-    double* q2;     // (k/bw)^2
+    double* e8;     // exp(-(k/bw)^2 / 8): per-axis factor of the window weight
     double* slot;   // [8 half-warps][32 entries (ri, ci, o)][16 lanes]
     float2* wp;     // (1 - frac, frac): weight of histogram index floor(bin) + {0, 1}
     int* ew;        // min biased exponent (>= 1) of the nonzero weights in wp
@@ -774,6 +771,21 @@ struct StreamSmem {
 __device__ __forceinline__ int efield1(float x) {
     const int e = (int)((__float_as_uint(x) >> 23) & 0xffu);
     return e ? e : -22;
+}
+
+// float(D) for D = exp(a + b) from P = RN(exp(a) * exp(b)) (a, b <= 0, both
+// factors within 0.502 ulp): |P - D| <= 2^-50 D (factor errors, product
+// rounding, the reference's rounding of a + b, glibc's own error), so if P is
+// at least 2^-47 P inside the rounding interval of f = RN_float(P), D rounds to
+// f as well.  Returns false when that cannot be shown.
+__device__ __forceinline__ bool separable_weight(double P, float& f) {
+    f = __double2float_rn(P);
+    const double r = D_SUB(P, (double)f);   // exact: f is P's leading bits
+    const unsigned fb = __float_as_uint(f);
+    const int e = (int)((fb >> 23) & 0xffu);
+    // half an ulp of f; the interval below a power of two is half as wide
+    const double hu = __longlong_as_double((long long)(e - 127 - 24 + 1023) << 52) * ((fb & 0x7fffffu) ? 1.0 : 0.5);
+    return e > 0 && fabs(r) < D_SUB(hu, D_MUL(P, 0x1p-47));
 }
 
 __device__ __forceinline__ void stream_misc_init(int* misc) {
@@ -829,7 +841,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         const int c = (int)floor(bn);
         const float fr = (float)D_SUB(bn, (double)c);
         const float gr = F_SUB(1.0f, fr);
-        S.q2[i] = D_MUL(q, q);
+        S.e8[i] = dsift_exp_mid(D_MUL(-D_MUL(q, q), 0.125));
         S.wp[i] = make_float2(gr, fr);
         const int ewk = min(fr != 0.0f ? efield1(fr) : 255, gr != 0.0f ? efield1(gr) : 255);
         S.ew[i] = ewk;
@@ -1060,11 +1072,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float du = F_MUL(0.5f, F_SUB(right, left));
                 const float dv = F_MUL(0.5f, F_SUB(down, up));
                 const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
-#if DSIFT_ABL == 2
-                float theta = fabsf(dv) + fabsf(du);
-#else
                 float theta = dsift_atan2f(dv, du);
-#endif
                 if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
                 if (isnan(theta)) {   // reference: negative bin -> std::out_of_range
                     atomicOr(a.err, kErrHistogramRange);
@@ -1072,12 +1080,15 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 }
                 double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
                 if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
-                const double arg = D_MUL(-D_ADD(S.q2[u - kA], S.q2[v - kA]), 0.125);
-#if DSIFT_ABL == 3
-                const float val = F_MUL(mag, (float)arg);
-#else
-                const float val = F_MUL(mag, (float)dsift_exp_mid(arg));
-#endif
+                // window weight float(exp(-(uu^2 + vv^2) / 8)) (describe.cpp:96-98) as the
+                // product of the two per-axis factors, proven to round to the same
+                // float; otherwise (~1e-8 of points) evaluated as the reference does
+                float wgt;
+                if (!separable_weight(D_MUL(S.e8[u - kA], S.e8[v - kA]), wgt)) {
+                    const double qu = D_DIV((double)u, bw), qv = D_DIV((double)v, bw);
+                    wgt = (float)dsift_exp_mid(D_MUL(-D_ADD(D_MUL(qu, qu), D_MUL(qv, qv)), 0.125));
+                }
+                const float val = F_MUL(mag, wgt);
                 const int o0 = (int)floor(obin);
                 const float fo = (float)D_SUB(obin, (double)o0);
                 const float go = F_SUB(1.0f, fo);
@@ -1088,10 +1099,6 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float t10 = F_MUL(a1, wc.x), t11 = F_MUL(a1, wc.y);
                 double* pa = my + (o0 & 7) * 16;
                 double* pb = my + ((o0 + 1) & 7) * 16;
-#if DSIFT_ABL == 1
-                lmin += __float_as_int(F_MUL(t00, go)) ^ __float_as_int(F_MUL(t11, fo)) ^ __float_as_int(t01) ^ __float_as_int(t10);
-                continue;
-#endif
                 double x0 = pa[0], x1 = pb[0], x2 = pa[kSSlotE], x3 = pb[kSSlotE];
                 double x4 = pa[2 * kSSlotE], x5 = pb[2 * kSSlotE], x6 = pa[3 * kSSlotE], x7 = pb[3 * kSSlotE];
                 x0 = x0 + (double)F_MUL(t00, go);
@@ -1169,7 +1176,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     S.cysu = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
-    S.q2 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
+    S.e8 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.slot = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * 32 * kDescThreads;
     S.wp = reinterpret_cast<float2*>(pbuf); pbuf += sizeof(float2) * SP;
     S.ew = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * SP;
