@@ -773,21 +773,6 @@ __device__ __forceinline__ int efield1(float x) {
     return e ? e : -22;
 }
 
-// float(D) for D = exp(a + b) from P = RN(exp(a) * exp(b)) (a, b <= 0, both
-// factors within 0.502 ulp): |P - D| <= 2^-50 D (factor errors, product
-// rounding, the reference's rounding of a + b, glibc's own error), so if P is
-// at least 2^-47 P inside the rounding interval of f = RN_float(P), D rounds to
-// f as well.  Returns false when that cannot be shown.
-__device__ __forceinline__ bool separable_weight(double P, float& f) {
-    f = __double2float_rn(P);
-    const double r = D_SUB(P, (double)f);   // exact: f is P's leading bits
-    const unsigned fb = __float_as_uint(f);
-    const int e = (int)((fb >> 23) & 0xffu);
-    // half an ulp of f; the interval below a power of two is half as wide
-    const double hu = __longlong_as_double((long long)(e - 127 - 24 + 1023) << 52) * ((fb & 0x7fffffu) ? 1.0 : 0.5);
-    return e > 0 && fabs(r) < D_SUB(hu, D_MUL(P, 0x1p-47));
-}
-
 __device__ __forceinline__ void stream_misc_init(int* misc) {
     const int t = threadIdx.x;
     if (t < 32) misc[t] = ((t & 15) == 1) ? -(1 << 30) : (1 << 30);
@@ -1084,7 +1069,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 // product of the two per-axis factors, proven to round to the same
                 // float; otherwise (~1e-8 of points) evaluated as the reference does
                 float wgt;
-                if (!separable_weight(D_MUL(S.e8[u - kA], S.e8[v - kA]), wgt)) {
+                if (!ds_separable_weight(D_MUL(S.e8[u - kA], S.e8[v - kA]), 0x1p-47, wgt)) {
                     const double qu = D_DIV((double)u, bw), qv = D_DIV((double)v, bw);
                     wgt = (float)dsift_exp_mid(D_MUL(-D_ADD(D_MUL(qu, qu), D_MUL(qv, qv)), 0.125));
                 }

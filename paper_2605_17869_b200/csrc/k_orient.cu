@@ -26,6 +26,7 @@ namespace dsift {
 constexpr int kOriWarps = 4;
 constexpr int kOriPerWarp = 4;
 constexpr int kOriTile = kOriWarps * kOriPerWarp;
+constexpr int kOriAxis = 64;   // per-axis weight factors held (window side 2R+1 <= 64 uses them)
 
 __device__ __forceinline__ int nearest_level(const PyramidDesc& p, double sigma_rel) {
     // nearest_gauss_level (orient.cpp:13-24): strict < keeps the lower index on ties
@@ -51,7 +52,7 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
     const size_t exact_bytes = sizeof(double) * bins * a.depth + sizeof(unsigned) * bins * 2 + sizeof(float) * 32;
     const size_t acc_bytes = sizeof(double) * bins * 32;
     const size_t uni = ((exact_bytes > acc_bytes ? exact_bytes : acc_bytes) + 15) & ~size_t(15);
-    const size_t per_warp_al = (uni + sizeof(float) * 2 * bins + 15) & ~size_t(15);
+    const size_t per_warp_al = ((uni + sizeof(float) * 2 * bins + 15) & ~size_t(15)) + sizeof(double) * 2 * kOriAxis;
     unsigned char* wbase = sm_raw + warp * per_warp_al;
     double* acc = reinterpret_cast<double*>(wbase);
     double* node = reinterpret_cast<double*>(wbase);
@@ -60,6 +61,9 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
     float* vals = reinterpret_cast<float*>(mask + bins);
     float* hist = reinterpret_cast<float*>(wbase + uni);
     float* hist2 = hist + bins;
+    // per-axis window-weight factors exp(-d^2 / denom) for x and y
+    double* wx = reinterpret_cast<double*>(wbase + ((uni + sizeof(float) * 2 * bins + 15) & ~size_t(15)));
+    double* wy = wx + kOriAxis;
     // peaks go straight to global: angles[k][bins], counts[k] (K4b emits them)
     float* ang = a.angles;
     int* ncopy = a.counts;
@@ -99,6 +103,18 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
         const int nx = xb - xa + 1, ny = yb - ya + 1;
         const int npx = (nx > 0 && ny > 0) ? nx * ny : 0;
 
+        const bool sep = nx <= kOriAxis && ny <= kOriAxis;
+        if (sep) {
+            for (int j = lane; j < nx; j += 32) {
+                const double d = D_SUB((double)(xa + j), cx);
+                wx[j] = dsift_exp_mid(D_DIV(-D_MUL(d, d), denom));
+            }
+            for (int j = lane; j < ny; j += 32) {
+                const double d = D_SUB((double)(ya + j), cy);
+                wy[j] = dsift_exp_mid(D_DIV(-D_MUL(d, d), denom));
+            }
+            __syncwarp();
+        }
         // one window pixel q (row-major, orient.cpp:40-58): its bin and leaf value
         auto pixel = [&](int q, int& bin, float& val) {
             bin = -1;
@@ -117,9 +133,15 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 }
                 bin = (int)ds_div_2pi((double)F_MUL(theta, (float)bins));
                 if (bin >= bins) bin -= bins;
-                const double ddx = D_SUB((double)x, cx), ddy = D_SUB((double)y, cy);
-                const double arg = D_DIV(-D_ADD(D_MUL(ddx, ddx), D_MUL(ddy, ddy)), denom);
-                const float wgt = (float)dsift_exp_mid(arg);
+                // float(exp(-(ddx^2 + ddy^2) / denom)) (orient.cpp:54-55) from the
+                // per-axis factors, certified (|arg| <= 9: |P - D| <= 2^-48 D), else
+                // evaluated as the reference does
+                float wgt;
+                if (!(sep && ds_separable_weight(D_MUL(wx[x - xa], wy[y - ya]), 0x1p-45, wgt))) {
+                    const double ddx = D_SUB((double)x, cx), ddy = D_SUB((double)y, cy);
+                    const double arg = D_DIV(-D_ADD(D_MUL(ddx, ddx), D_MUL(ddy, ddy)), denom);
+                    wgt = (float)dsift_exp_mid(arg);
+                }
                 val = F_MUL(mag, wgt);
             }
         };
@@ -307,7 +329,7 @@ size_t orient_smem_bytes(int bins, int depth) {
     const size_t exact_bytes = sizeof(double) * bins * depth + sizeof(unsigned) * bins * 2 + sizeof(float) * 32;
     const size_t acc_bytes = sizeof(double) * bins * 32;
     const size_t uni = ((exact_bytes > acc_bytes ? exact_bytes : acc_bytes) + 15) & ~size_t(15);
-    const size_t per_warp_al = (uni + sizeof(float) * 2 * bins + 15) & ~size_t(15);
+    const size_t per_warp_al = ((uni + sizeof(float) * 2 * bins + 15) & ~size_t(15)) + sizeof(double) * 2 * kOriAxis;
     return kOriWarps * per_warp_al;
 }
 
