@@ -1,0 +1,91 @@
+"""verify-determinism on the B200 path (reference: tools/detsift.cpp:170-200,
+acceptance criterion 1, acceptance.cpp:72-101).
+
+The reference extracts one image `runs` times for every worker count and exits
+0 iff all DSF1 SHA-256 digests (detsum.cpp:129-132) are identical, 3 otherwise.
+On the GPU the free variables are the run index and the batch composition: an
+image is extracted alone, inside batches of several sizes (its neighbours
+change the grid, the tile tickets and the compaction offsets).  Every digest
+must be the same (tests/test_gpu_parity.py::test_verify_determinism also
+checks it against the reference's own digest).
+
+    python -m paper_2605_17869_b200.verify IMAGE.pgm [--runs 10] [--batches 1,2,4,8]
+    python -m paper_2605_17869_b200.verify --synthetic 640x480 --seed 0x5EED0000
+
+Prints one line per extraction (run, batch, digest) and a summary; exit code 0
+(one digest) or 3 (several), like the reference.
+"""
+from __future__ import annotations
+
+import argparse
+import sys
+
+import numpy as np
+
+from . import Extractor, SiftConfig, load_image
+
+
+def digests_for(img: np.ndarray, runs: int, batches: list[int], cfg: SiftConfig | None = None,
+                device: int = 0, fillers: np.ndarray | None = None) -> dict[str, list[tuple[int, int]]]:
+    """{digest: [(run, batch size), ...]} for `img` extracted `runs` times at
+    every batch size (the image sits at a rotating position among fillers)."""
+    out: dict[str, list[tuple[int, int]]] = {}
+    with Extractor(cfg, device) as ex:
+        for run in range(runs):
+            for b in batches:
+                if b == 1:
+                    batch = img[None]
+                    pos = 0
+                else:
+                    pos = run % b
+                    fill = fillers if fillers is not None else np.stack([np.roll(img, k + 1, axis=1) for k in range(b)])
+                    batch = np.array(fill[:b], np.float32, copy=True)
+                    batch[pos] = img
+                ex.submit(batch)
+                ex.sync()
+                d = ex.sha256(pos)
+                out.setdefault(d, []).append((run, b))
+    return out
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
+    ap.add_argument("image", nargs="?", help="binary PNM (P5/P6)")
+    ap.add_argument("--synthetic", help="WxH value-noise image instead of a file (synth.cpp:44-66)")
+    ap.add_argument("--seed", type=lambda s: int(s, 0), default=0x5EED0000)
+    ap.add_argument("--runs", type=int, default=10)
+    ap.add_argument("--batches", default="1,2,4,8")
+    ap.add_argument("--device", type=int, default=0)
+    args = ap.parse_args(argv)
+    if args.synthetic:
+        w, h = (int(v) for v in args.synthetic.lower().split("x"))
+        import torch
+        ex = Extractor(device=args.device)
+        dev = torch.empty((1, h, w), dtype=torch.float32, device=f"cuda:{args.device}")
+        ex.synth_value_noise(dev.data_ptr(), 1, w, h, args.seed, 5, max(8, w // 20))
+        torch.cuda.synchronize()
+        img = dev[0].cpu().numpy()
+        ex.close()
+    elif args.image:
+        pix = load_image(args.image)
+        with Extractor(device=args.device) as ex:
+            img = ex.ingest_u8(pix)
+    else:
+        ap.error("an image path or --synthetic WxH is required")
+    batches = [int(b) for b in args.batches.split(",") if b]
+    table = digests_for(img, args.runs, batches, device=args.device)
+    total = 0
+    for d, occ in table.items():
+        for run, b in occ:
+            print(f"run={run} batch={b} sha256={d}")
+            total += 1
+    ok = len(table) == 1
+    if len(table) == 1:
+        print(f"1 unique digest over {total} runs")
+    else:
+        print(f"{len(table)} distinct digests over {total} runs")
+    return 0 if ok else 3
+
+
+if __name__ == "__main__":
+    sys.exit(main())

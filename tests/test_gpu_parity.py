@@ -298,3 +298,17 @@ def test_c3_full_size_properties_and_sampled_parity(port):
     idx = np.linspace(0, len(k) - 1, 48).astype(int)
     for i in idx:
         assert bits(port.dsp_descriptor(ss, k[i])).tobytes() == bits(fs.descriptors[i]).tobytes(), i
+
+
+# ---- verify-determinism (detsift.cpp:170-200) ------------------------------
+def test_verify_determinism(port, tmp_path):
+    from paper_2605_17869_b200 import verify
+    img = port.value_noise(160, 120, 0x5EED0003, 5, 8)
+    table = verify.digests_for(img, runs=2, batches=[1, 3, 5])
+    assert len(table) == 1, table
+    k, d = port.extract(img)
+    assert next(iter(table)) == port.hash_features(k, d)
+    pix = (np.clip(img, 0, 1) * 255).round().astype(np.uint8)
+    path = tmp_path / "v.pgm"
+    path.write_bytes(b"P5\n160 120\n255\n" + pix.tobytes())
+    assert verify.main([str(path), "--runs", "2", "--batches", "1,2"]) == 0
