@@ -363,6 +363,27 @@ def run_ours(args, rank, local_rank, world):
                      "share_of_step": stages["describe"] / max(1e-9, sum(stages.values())),
                      "exact_fallbacks_last_step": fallbacks, "desc_kernel": args.desc_kernel}
 
+    # ---- matching: ratio_match of the first two images' descriptors,
+    # device-resident (DLPack export, no host copy), CUDA events
+    match = None
+    if B >= 2:
+        ex.set_profiling(False)
+        ex.submit(None, n=B, w=W, h=H, device_ptr=imgs.data_ptr())
+        ex.sync()
+        d = ex.export_torch(1)
+        offs = ex.offsets()
+        da, db = d[offs[0]:offs[1]], d[offs[1]:offs[2]]
+        ex.ratio_match(da, db, 0.8)   # warm-up
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        pairs, pa, pb = ex.ratio_match(da, db, 0.8)
+        e1.record()
+        torch.cuda.synchronize()
+        match = {"what": "ratio_match(image 0, image 1), ratio 0.8, descriptors on device",
+                 "n_a": int(offs[1] - offs[0]), "n_b": int(offs[2] - offs[1]), "ms": e0.elapsed_time(e1),
+                 "pairs": int(len(pairs)), "putative_a": pa, "putative_b": pb}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         img = imgs[0].cpu().numpy()
@@ -388,6 +409,7 @@ def run_ours(args, rank, local_rank, world):
             "e2e": e2e,
             "roofline": roofline,
             "roofline_descriptor": roofline_desc,
+            "match": match,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": launches,

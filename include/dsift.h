@@ -102,6 +102,20 @@ int dsift_extract(dsift_ctx* ctx, const float* image, int w, int h, int flags);
  * dsift_extract_batch on the resulting GrayImages. */
 int dsift_extract_batch_u8(dsift_ctx* ctx, const uint8_t* pixels, int n, int w, int h, int channels,
                            int flags);
+/* ---- matching ---------------------------------------------- */
+/* detsift::Match (match.hpp:14-18). */
+typedef struct dsift_match {
+    int32_t a, b;
+    float distance;
+} dsift_match;
+/* detsift::ratio_match (match.hpp:34-38, match.cpp:77-119): symmetric ratio
+ * test with mutual-consistency filtering over two descriptor sets (row-major
+ * n x dim float32, host or device per flags), bit-identical distances (fixed
+ * tree dot products).  Pairs come sorted by a; *n_pairs may exceed cap (then
+ * only cap are written).  This build supports dim = 128. */
+int dsift_ratio_match(dsift_ctx* ctx, const float* desc_a, int64_t n_a, const float* desc_b, int64_t n_b,
+                      int dim_a, int dim_b, float ratio, int flags, dsift_match* out, int64_t cap,
+                      int64_t* n_pairs, int64_t* putative_a, int64_t* putative_b);
 /* Reads a binary PNM (P5/P6, maxval 255) like detsift::load_image
  * (io.cpp:49-81), with its error messages (DSIFT_EIO).  Pass pixels = NULL to
  * query w, h, channels; otherwise pixels must hold w*h*channels bytes

@@ -147,6 +147,35 @@ class Oracle:
         self._f("value_noise")(w, h, C.c_uint64(seed), octaves, cells, out.ctypes.data)
         return out
 
+    # ---- matching (match.cpp:71-119), reference only ----------------------
+    def ratio_match(self, da: np.ndarray, db: np.ndarray, ratio: float = 0.8, workers: int = 1):
+        """MatchSet ratio_match(a, b, ratio): (pairs [k, 3] int32 with the distance
+        bits in column 2, putative_a, putative_b)."""
+        if self.kind != "reference":
+            raise OracleError("ratio_match: the reference library only")
+        da = np.ascontiguousarray(da, np.float32)
+        db = np.ascontiguousarray(db, np.float32)
+        fn = self.lib.oref_ratio_match
+        fn.restype = C.c_int64
+        fn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int, C.c_float, C.c_int,
+                       C.c_void_p, C.c_int64, C.c_void_p]
+        cap = max(1, min(len(da), len(db)))
+        out = np.zeros((cap, 3), np.int32)
+        put = np.zeros(2, np.int64)
+        n = fn(da.ctypes.data, len(da), db.ctypes.data, len(db), da.shape[1] if da.ndim == 2 else 128,
+               C.c_float(ratio), workers, out.ctypes.data, cap, put.ctypes.data)
+        if n < 0:
+            raise OracleError(self.error())
+        return out[:n], int(put[0]), int(put[1])
+
+    def descriptor_distance(self, a: np.ndarray, b: np.ndarray) -> float:
+        fn = self.lib.oref_descriptor_distance
+        fn.restype = C.c_float
+        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
+        a = np.ascontiguousarray(a, np.float32)
+        b = np.ascontiguousarray(b, np.float32)
+        return fn(a.ctypes.data, b.ctypes.data, len(a))
+
     # ---- image ingest (io.cpp:49-81) -------------------------------------
     def load_image(self, path: str) -> np.ndarray:
         w, h = C.c_int(), C.c_int()

@@ -21,6 +21,7 @@
 #include "detsift/detsum.hpp"
 #include "detsift/geom.hpp"
 #include "detsift/io.hpp"
+#include "detsift/match.hpp"
 #include "detsift/orient.hpp"
 #include "detsift/scalespace.hpp"
 #include "support/oracles.hpp"
@@ -132,6 +133,35 @@ int oref_load_image(const char* path, int* w, int* h, float* out) {
         if (out) std::memcpy(out, img.data.data(), img.data.size() * sizeof(float));
         return 0;
     });
+}
+
+// ---- matching: match.cpp:77-119 (ratio_match), :71-75 (descriptor_distance)
+// out3 receives (a, b, distance-bits) triples; returns the pair count or < 0.
+int64_t oref_ratio_match(const float* da, int64_t na, const float* db, int64_t nb, int dim, float ratio,
+                         int workers, int32_t* out3, int64_t cap, int64_t* putative) {
+    int64_t n = -1;
+    const int rc = guard([&] {
+        FeatureSet a, b;
+        a.dim = b.dim = dim;
+        a.keypoints.resize((size_t)na);
+        b.keypoints.resize((size_t)nb);
+        a.descriptors.assign(da, da + na * dim);
+        b.descriptors.assign(db, db + nb * dim);
+        const MatchSet m = ratio_match(a, b, ratio, workers);
+        putative[0] = m.putative_a;
+        putative[1] = m.putative_b;
+        n = (int64_t)m.pairs.size();
+        for (int64_t i = 0; i < n && i < cap; ++i) {
+            out3[3 * i + 0] = m.pairs[i].a;
+            out3[3 * i + 1] = m.pairs[i].b;
+            std::memcpy(&out3[3 * i + 2], &m.pairs[i].distance, 4);
+        }
+        return 0;
+    });
+    return rc ? rc : n;
+}
+float oref_descriptor_distance(const float* a, const float* b, int dim) {
+    return descriptor_distance(std::span<const float>(a, dim), std::span<const float>(b, dim));
 }
 
 // ---- full pipeline: io.cpp:111-142 -----------------------------------------

@@ -28,6 +28,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 KEYPOINT_DTYPE = np.dtype(
     [("x", "<f4"), ("y", "<f4"), ("sigma", "<f4"), ("angle", "<f4"),
      ("response", "<f4"), ("octave", "<i4"), ("interval", "<i4")])
+MATCH_DTYPE = np.dtype([("a", np.int32), ("b", np.int32), ("distance", np.float32)])   # detsift::Match
 DESC_DIM = 128
 
 DSIFT_OK, DSIFT_EINVAL, DSIFT_ECAPACITY, DSIFT_ECUDA, DSIFT_ENOMEM, DSIFT_ESTATE, DSIFT_ERANGE, DSIFT_EIO = range(8)
@@ -140,6 +141,7 @@ def load_library():
         "dsift_extract": ([vp, vp, i32, i32, i32], C.c_int),
         "dsift_extract_batch_u8": ([vp, vp, i32, i32, i32, i32, i32], C.c_int),
         "dsift_load_image": ([C.c_char_p, vp, vp, vp, vp, i64], C.c_int),
+        "dsift_ratio_match": ([vp, vp, i64, vp, i64, i32, i32, C.c_float, i32, vp, i64, vp, vp, vp], C.c_int),
         "dsift_ingest_u8": ([vp, vp, i64, i32, i32, vp], C.c_int),
         "dsift_result_sync": ([vp, vp], C.c_int), "dsift_result_range": ([vp, i32, vp, vp], C.c_int),
         "dsift_result_copy": ([vp, vp, vp, vp, vp], C.c_int),
@@ -249,6 +251,16 @@ class Extractor:
         _check(self.lib, self.lib.dsift_result_sync(self.ctx, C.byref(total)))
         return total.value
 
+    def offsets(self) -> np.ndarray:
+        """Per-image result offsets [batch + 1] of the last batch (host copy)."""
+        self.sync()
+        out = np.zeros(self.batch + 1, np.int64)
+        for b in range(self.batch):
+            beg, cnt = C.c_int64(), C.c_int64()
+            _check(self.lib, self.lib.dsift_result_range(self.ctx, b, C.byref(beg), C.byref(cnt)))
+            out[b], out[b + 1] = beg.value, beg.value + cnt.value
+        return out
+
     def results(self, with_u8: bool = True) -> list[FeatureSet]:
         total = self.sync()
         kps = np.zeros(total, KEYPOINT_DTYPE)
@@ -296,6 +308,29 @@ class Extractor:
                                                   C.c_void_p(out.data_ptr())))
         shape = a.shape[:-1] if ch == 3 else a.shape
         return out.cpu().numpy().reshape(shape)
+
+    def ratio_match(self, desc_a, desc_b, ratio: float = 0.8):
+        """detsift::ratio_match (match.cpp:77-119) on the device: returns
+        (pairs structured [k] (a, b, distance), putative_a, putative_b).  Inputs are
+        host arrays [n, 128] float32 or torch CUDA tensors (zero copy)."""
+        flags = INPUT_HOST
+        if hasattr(desc_a, "data_ptr") and getattr(desc_a, "is_cuda", False):
+            pa, na, da = desc_a.data_ptr(), desc_a.shape[0], desc_a.shape[1]
+            pb, nb, db = desc_b.data_ptr(), desc_b.shape[0], desc_b.shape[1]
+            flags = INPUT_DEVICE
+        else:
+            a = np.ascontiguousarray(desc_a, np.float32)
+            b = np.ascontiguousarray(desc_b, np.float32)
+            self._pin_match = (a, b)
+            pa, na, da = a.ctypes.data, a.shape[0], a.shape[1] if a.ndim == 2 else DESC_DIM
+            pb, nb, db = b.ctypes.data, b.shape[0], b.shape[1] if b.ndim == 2 else DESC_DIM
+        cap = max(1, min(na, nb))
+        out = np.zeros(cap, MATCH_DTYPE)
+        n, put_a, put_b = C.c_int64(), C.c_int64(), C.c_int64()
+        _check(self.lib, self.lib.dsift_ratio_match(self.ctx, C.c_void_p(pa), na, C.c_void_p(pb), nb, da, db,
+                                                    C.c_float(ratio), flags, out.ctypes.data, cap, C.byref(n),
+                                                    C.byref(put_a), C.byref(put_b)))
+        return out[:n.value], put_a.value, put_b.value
 
     def extract(self, img) -> FeatureSet:
         """detsift::extract (io.cpp:111-142) for one image."""

@@ -214,7 +214,7 @@ struct dsift_ctx {
     Plan plan;
     int batch = 0;            // images in the current pyramid / result
     PyramidDesc pyr{};
-    DevBuf det_aux, input_u8, ori_aux;
+    DevBuf det_aux, input_u8, ori_aux, match_in, match_scratch, match_best;
     DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
         pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow,
         ref_states, keep;
@@ -834,6 +834,66 @@ int dsift_extract_batch(dsift_ctx* c, const float* images, int n, int w, int h, 
 
 int dsift_extract(dsift_ctx* c, const float* image, int w, int h, int flags) {
     return dsift_extract_batch(c, image, 1, w, h, flags);
+}
+
+// ---- matching (match.cpp:77-119) --------------------------------------------
+int dsift_ratio_match(dsift_ctx* c, const float* desc_a, int64_t n_a, const float* desc_b, int64_t n_b, int dim_a,
+                      int dim_b, float ratio, int flags, dsift_match* out, int64_t cap, int64_t* n_pairs,
+                      int64_t* putative_a, int64_t* putative_b) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (dim_a != dim_b) invalid("ratio_match: dimension mismatch");
+        if (!(ratio > 0.0f) || ratio > 1.0f) invalid("ratio_match: ratio must be in (0,1]");
+        if (dim_a != kDescDim) invalid("ratio_match: this build matches 128-d descriptors");
+        if (n_a < 0 || n_b < 0) invalid("ratio_match: negative size");
+        if (n_pairs) *n_pairs = 0;
+        if (putative_a) *putative_a = 0;
+        if (putative_b) *putative_b = 0;
+        if (n_a < 2 || n_b < 2) return;   // match.cpp:85
+        if ((!desc_a || !desc_b)) invalid("ratio_match: null descriptors");
+        set_device(c);
+        const float* A = desc_a;
+        const float* B = desc_b;
+        const size_t ba = sizeof(float) * kDescDim * (size_t)n_a, bb = sizeof(float) * kDescDim * (size_t)n_b;
+        if (!(flags & DSIFT_INPUT_DEVICE)) {
+            c->match_in.ensure(ba + bb + 256);
+            char* p = c->match_in.as<char>();
+            cuda_check(cudaMemcpyAsync(p, desc_a, ba, cudaMemcpyHostToDevice, c->stream), "H2D");
+            cuda_check(cudaMemcpyAsync(p + ((ba + 255) & ~size_t(255)), desc_b, bb, cudaMemcpyHostToDevice, c->stream),
+                       "H2D");
+            A = reinterpret_cast<const float*>(p);
+            B = reinterpret_cast<const float*>(p + ((ba + 255) & ~size_t(255)));
+        }
+        c->match_scratch.ensure(match_scratch_bytes(n_a, n_b));
+        c->match_best.ensure(sizeof(int) * (size_t)(n_a + n_b) + sizeof(float) * (size_t)n_a + 512);
+        int* best_a = c->match_best.as<int>();
+        int* best_b = best_a + n_a;
+        float* dist_a = reinterpret_cast<float*>(best_b + n_b);
+        cuda_check(launch_ratio_match(A, n_a, B, n_b, ratio, c->match_scratch.as<void>(), best_a, best_b, dist_a,
+                                      c->stream),
+                   "ratio_match");
+        c->launches += 5;
+        std::vector<int> ha((size_t)n_a), hb((size_t)n_b);
+        std::vector<float> hd((size_t)n_a);
+        cuda_check(cudaMemcpyAsync(ha.data(), best_a, sizeof(int) * n_a, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaMemcpyAsync(hb.data(), best_b, sizeof(int) * n_b, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaMemcpyAsync(hd.data(), dist_a, sizeof(float) * n_a, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        // putative counts and the mutual filter in index order (match.cpp:109-117)
+        int64_t pa = 0, pb = 0, np = 0;
+        for (int64_t i = 0; i < n_a; ++i) pa += ha[i] >= 0;
+        for (int64_t j = 0; j < n_b; ++j) pb += hb[j] >= 0;
+        for (int64_t i = 0; i < n_a; ++i) {
+            const int j = ha[i];
+            if (j >= 0 && hb[j] == (int)i) {
+                if (out && np < cap) out[np] = dsift_match{(int32_t)i, (int32_t)j, hd[i]};
+                ++np;
+            }
+        }
+        if (n_pairs) *n_pairs = np;
+        if (putative_a) *putative_a = pa;
+        if (putative_b) *putative_b = pb;
+    });
 }
 
 // ---- image ingest (io.cpp:49-81) ---------------------------------------------

@@ -125,6 +125,9 @@ cudaError_t launch_describe_stream(const DescArgs& a, int grid, cudaStream_t st)
 cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev, long long n_host, double2* trig,
                         long long cap, cudaStream_t st);
 
+size_t match_scratch_bytes(long long na, long long nb);
+cudaError_t launch_ratio_match(const float* A, long long na, const float* B, long long nb, float ratio, void* scratch,
+                               int* best_a, int* best_b, float* dist_a, cudaStream_t st);
 cudaError_t launch_ingest_u8(const unsigned char* in, long long n_px, int channels, float* out, cudaStream_t st);
 
 }  // namespace dsift

@@ -312,3 +312,42 @@ def test_verify_determinism(port, tmp_path):
     path = tmp_path / "v.pgm"
     path.write_bytes(b"P5\n160 120\n255\n" + pix.tobytes())
     assert verify.main([str(path), "--runs", "2", "--batches", "1,2"]) == 0
+
+
+# ---- ratio_match (match.cpp:77-119) -----------------------------------------
+def _match_sets(port):
+    from oracle.oracle import Oracle, available
+    if not available("reference"):
+        pytest.skip("oracle/_ref not built")
+    ref = Oracle("reference")
+    a = port.value_noise(320, 240, 0x5EED0011, 5, 16)
+    b = (np.roll(a, (7, -5), axis=(0, 1)) * np.float32(0.9) + np.float32(0.03)).astype(np.float32)
+    _, da = ref.extract(a, None, os.cpu_count() or 1)
+    _, db = ref.extract(b, None, os.cpu_count() or 1)
+    return ref, da, db
+
+
+def test_ratio_match_bit_exact(port):
+    ref, da, db = _match_sets(port)
+    with ds.Extractor() as ex:
+        for ratio in (0.8, 0.6, 1.0):
+            got, pa, pb = ex.ratio_match(da, db, ratio)
+            want, wa, wb = ref.ratio_match(da, db, ratio, 8)
+            assert (pa, pb) == (wa, wb), ratio
+            assert len(got) == len(want) > 10, ratio
+            assert np.array_equal(got["a"], want[:, 0]) and np.array_equal(got["b"], want[:, 1])
+            assert got["distance"].view(np.uint32).tobytes() == want[:, 2].view(np.uint32).tobytes()
+        # ties, duplicates and degenerate sets: identical rows in B, an all-zero row, sizes < 2
+        db2 = np.concatenate([db[:40], db[:40], np.zeros((1, 128), np.float32)])
+        got, pa, pb = ex.ratio_match(da[:60], db2, 0.8)
+        want, wa, wb = ref.ratio_match(da[:60], db2, 0.8, 1)
+        assert (len(got), pa, pb) == (len(want), wa, wb)
+        assert np.array_equal(got["a"], want[:, 0]) and np.array_equal(got["b"], want[:, 1])
+        assert len(ex.ratio_match(da[:1], db, 0.8)[0]) == 0
+        with pytest.raises(ds.InvalidArgument, match="ratio must be in"):
+            ex.ratio_match(da, db, 1.5)
+        # device tensors in, same result
+        import torch
+        got_t, _, _ = ex.ratio_match(torch.from_numpy(da).cuda(), torch.from_numpy(db).cuda(), 0.8)
+        want, _, _ = ref.ratio_match(da, db, 0.8, 8)
+        assert np.array_equal(got_t["b"], want[:, 1])
