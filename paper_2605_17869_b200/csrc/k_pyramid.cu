@@ -444,6 +444,18 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
             const double s4 = (((double)p0[0] + (double)p0[dx]) + (double)p1[0]) + (double)p1[dx];
             sm2[r * G::kInPitch + c] = (float)(0.25 * s4);
         }
+    } else if (MODE == kModeDecimate && cx0 >= 0 && cx0 + G::kInW <= w && y0 - R >= 0 && y0 + kB2H + R <= h) {
+        // interior seed tile: even samples of the previous octave's G[s]
+        // (decimate2x, scalespace.cpp:133-142), no reflection needed
+        const float* gsrc = src + (long long)(2 * (y0 - R)) * a.src_pitch + 2 * cx0;
+#pragma unroll 4
+        for (int i = threadIdx.x; i < G::kHR * (G::kInW / 2); i += kB2Threads) {
+            const int r = i / (G::kInW / 2), c2 = i - r * (G::kInW / 2);
+            const float4 v = __ldg(reinterpret_cast<const float4*>(gsrc + (long long)(2 * r) * a.src_pitch) + c2);
+            *reinterpret_cast<float2*>(sm2 + r * G::kInPitch + 2 * c2) = make_float2(v.x, v.z);
+            alu_ok &= (__float_as_int(v.x) >= 0x0d800000) & (__float_as_int(v.x) < 0x7f800000) &
+                      (__float_as_int(v.z) >= 0x0d800000) & (__float_as_int(v.z) < 0x7f800000);
+        }
     } else {   // gather with reflect-101 (scalespace.cpp:41-48) through the mode's input
                // mapping: level / raw pixel, 2x upsample (:113-131), decimation (:133-142)
 #pragma unroll 4
