@@ -118,7 +118,8 @@ _LIB = None
 
 
 def library_path() -> str:
-    return os.path.join(HERE, "libdsift.so")
+    # DSIFT_LIBRARY: an alternative in-tree build (A/B measurements)
+    return os.environ.get("DSIFT_LIBRARY") or os.path.join(HERE, "libdsift.so")
 
 
 def load_library():

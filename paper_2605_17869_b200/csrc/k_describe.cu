@@ -747,20 +747,26 @@ __host__ __device__ __forceinline__ int ring_pitch_for(int max_span) {
     return need + ((16 - need % 32) + 32) % 32;
 }
 
+// per-axis weights of lattice index k, one 16-byte load
+struct __align__(16) AxisW {
+    double e8;      // exp(-(k/bw)^2 / 8): per-axis factor of the window weight
+    float g, fr;    // (1 - frac, frac): weight of histogram index floor(bin) + {0, 1}
+};
+
 struct StreamSmem {
     double* ax;     // cx + cos*k        [span] indexed k - kA
     double* cysu;   // cy + sin*k
     double* sv;     // sin*k
     double* cv;     // cos*k
-    double* e8;     // exp(-(k/bw)^2 / 8): per-axis factor of the window weight
+    AxisW* aw;      // [span]
     double* slot;   // [8 half-warps][32 entries (ri, ci, o)][16 lanes]
-    float2* wp;     // (1 - frac, frac): weight of histogram index floor(bin) + {0, 1}
-    int* ew;        // min biased exponent (>= 1) of the nonzero weights in wp
+    int* ew;        // min biased exponent (>= 1) of the nonzero weights in aw[k].{g, fr}
     float* ring;    // [kSRing][ring_pitch] bilinear samples, -1 = undefined
     float* raw;     // [n_dsp][128]
-    int* lanelsb;   // [128] per-lane lower bound on the leaves' lowest-bit exponent (+531: sum of 4 biased exponents)
-    int* misc;      // [2][16]: kmin, kmax, start of cell c = -1..3, min weight exponent of
-                    // cell c = -1..3 (misc[8 + c + 1]); double-buffered per scale
+    int* cellmin;   // [2][32]: per pass (double-buffered), per cell: lower bound on the lowest-bit
+                    // exponent of the cell's leaves (+531: sum of 4 biased exponents)
+    int* misc;      // [2][16]: kmin, kmax, start of cell c = -1..3 (misc[2 + c + 1]);
+                    // double-buffered per scale
 };
 
 // Biased exponent of x > 0 (floor(log2 x) + 127); denormals map to -22
@@ -826,8 +832,11 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         const int c = (int)floor(bn);
         const float fr = (float)D_SUB(bn, (double)c);
         const float gr = F_SUB(1.0f, fr);
-        S.e8[i] = dsift_exp_mid(D_MUL(-D_MUL(q, q), 0.125));
-        S.wp[i] = make_float2(gr, fr);
+        AxisW w;
+        w.e8 = dsift_exp_mid(D_MUL(-D_MUL(q, q), 0.125));
+        w.g = gr;
+        w.fr = fr;
+        S.aw[i] = w;
         const int ewk = min(fr != 0.0f ? efield1(fr) : 255, gr != 0.0f ? efield1(gr) : 255);
         S.ew[i] = ewk;
         S.ax[i] = D_ADD(cx, D_MUL(cosa, (double)k));
@@ -1013,12 +1022,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                         qq = (qb + 1 == pP) ? 0 : qb + 1;
                         se = se + S.slot[slot_index(l0 + qa, e)];
                         so = so + S.slot[slot_index(l0 + qb, e)];
-                        lm = min(lm, min(S.lanelsb[l0 + qa], S.lanelsb[l0 + qb]));
                     }
-                    if (q < pP) {
-                        se = se + S.slot[slot_index(l0 + qq, e)];
-                        lm = min(lm, S.lanelsb[l0 + qq]);
-                    }
+                    if (q < pP) se = se + S.slot[slot_index(l0 + qq, e)];
+                    lm = min(lm, S.cellmin[((npass - 1) & 1) * 32 + cell]);
                 }
             }
             binacc = binacc + (se + so);
@@ -1039,14 +1045,24 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 rv0 = r0;
                 if (r1 >= r0 && nc > 0) npts = (r1 - r0 + 1) * nc;
             }
+            if (tid < 32) S.cellmin[((npass + 1) & 1) * 32 + tid] = 1 << 20;   // next pass's buffer (read two passes ago)
             double* my = S.slot + slot_index(tid, 0);
 #pragma unroll
             for (int e = 0; e < 32; ++e) my[e * 16] = 0.0;
             int lmin = 1 << 20;
-            const float inv_nc = 1.0f / (float)max(nc, 1);
+            // point pi = part + j*P of the cell in row-major order: (rr, cc),
+            // advanced incrementally (dq rows + dr columns per step)
+            const int ncs = max(nc, 1);
+            int rr = part / ncs, cc = part - rr * ncs;
+            const int dq = P / ncs, dr = P - dq * ncs;
             for (int pi = part; pi < npts; pi += P) {
-                const int rr = (int)(((float)pi + 0.5f) * inv_nc), cc = pi - rr * nc;
                 const int v = rv0 + rr, u = cu0 + cc;
+                cc += dr;
+                rr += dq;
+                if (cc >= ncs) {
+                    cc -= ncs;
+                    ++rr;
+                }
                 const int col = u - ub;
                 const float* mid = S.ring + (v & (kSRing - 1)) * ring_pitch + col;
                 const float left = mid[-1], right = mid[1];
@@ -1065,11 +1081,12 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 }
                 double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
                 if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
+                const AxisW wu = S.aw[u - kA], wv = S.aw[v - kA];
                 // window weight float(exp(-(uu^2 + vv^2) / 8)) (describe.cpp:96-98) as the
                 // product of the two per-axis factors, proven to round to the same
                 // float; otherwise (~1e-8 of points) evaluated as the reference does
                 float wgt;
-                if (!ds_separable_weight(D_MUL(S.e8[u - kA], S.e8[v - kA]), 0x1p-47, wgt)) {
+                if (!ds_separable_weight<47>(D_MUL(wu.e8, wv.e8), wgt)) {
                     const double qu = D_DIV((double)u, bw), qv = D_DIV((double)v, bw);
                     wgt = (float)dsift_exp_mid(D_MUL(-D_ADD(D_MUL(qu, qu), D_MUL(qv, qv)), 0.125));
                 }
@@ -1078,10 +1095,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float fo = (float)D_SUB(obin, (double)o0);
                 const float go = F_SUB(1.0f, fo);
                 // leaves value*wr*wc*wo (describe.cpp:102-124), FP64 slot accumulation
-                const float2 wr = S.wp[v - kA], wc = S.wp[u - kA];
-                const float a0 = F_MUL(val, wr.x), a1 = F_MUL(val, wr.y);
-                const float t00 = F_MUL(a0, wc.x), t01 = F_MUL(a0, wc.y);
-                const float t10 = F_MUL(a1, wc.x), t11 = F_MUL(a1, wc.y);
+                const float a0 = F_MUL(val, wv.g), a1 = F_MUL(val, wv.fr);
+                const float t00 = F_MUL(a0, wu.g), t01 = F_MUL(a0, wu.fr);
+                const float t10 = F_MUL(a1, wu.g), t11 = F_MUL(a1, wu.fr);
                 double* pa = my + (o0 & 7) * 16;
                 double* pb = my + ((o0 + 1) & 7) * 16;
                 double x0 = pa[0], x1 = pb[0], x2 = pa[kSSlotE], x3 = pb[kSSlotE];
@@ -1109,7 +1125,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                     lmin = min(lmin, efield1(val) + eo + S.ew[v - kA] + S.ew[u - kA]);
                 }
             }
-            S.lanelsb[tid] = lmin;
+            if (cell < ncells && lmin < (1 << 20)) atomicMin(&S.cellmin[(npass & 1) * 32 + cell], lmin);
         }
         kchain = max(kchain, ((vb - va + 1) * maxnc + P - 1) / P);
         ++npass;
@@ -1120,6 +1136,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         pP = P;
     }
     stream_misc_rearm(misc);   // every thread read misc before the pass barriers
+    if (tid < 32) S.cellmin[((npass - 1) & 1) * 32 + tid] = 1 << 20;   // folded before the last barrier
     // certificate (see the fast path): chain <= kchain in a lane slot, <= 51 in
     // the fold, <= npass across passes; the reference tree is <= 13 deep
     bool ok;
@@ -1152,6 +1169,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     __shared__ double red[4];
     __shared__ int misc[32];
+    __shared__ int cellmin[64];
     const int SP = a.max_span;
     const int RP = ring_pitch_for(SP);
     StreamSmem S;
@@ -1161,14 +1179,14 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     S.cysu = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
-    S.e8 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
+    S.aw = reinterpret_cast<AxisW*>(pbuf); pbuf += sizeof(AxisW) * SP;
     S.slot = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * 32 * kDescThreads;
-    S.wp = reinterpret_cast<float2*>(pbuf); pbuf += sizeof(float2) * SP;
     S.ew = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * SP;
-    S.ring = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kSRing * RP;
-    S.lanelsb = reinterpret_cast<int*>(pbuf);
+    S.ring = reinterpret_cast<float*>(pbuf);
+    S.cellmin = cellmin;
     S.misc = misc;
     stream_misc_init(misc);
+    if (threadIdx.x < 64) cellmin[threadIdx.x] = 1 << 20;
     __syncthreads();
 
     const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
@@ -1218,8 +1236,8 @@ size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp)
 
 size_t describe_stream_smem_bytes(int max_span, int n_dsp) {
     const size_t SP = (size_t)max_span, RP = (size_t)ring_pitch_for(max_span);
-    return sizeof(double) * 5 * SP + sizeof(double) * 32 * kDescThreads + sizeof(float2) * SP + sizeof(int) * SP +
-           sizeof(float) * kSRing * RP + sizeof(float) * kDescDim * n_dsp + sizeof(int) * kDescThreads;
+    return sizeof(float) * kDescDim * n_dsp + sizeof(double) * 4 * SP + sizeof(AxisW) * SP +
+           sizeof(double) * 32 * kDescThreads + sizeof(int) * SP + sizeof(float) * kSRing * RP;
 }
 
 int describe_stream_blocks_per_sm(size_t smem) {

@@ -137,7 +137,7 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 // per-axis factors, certified (|arg| <= 9: |P - D| <= 2^-48 D), else
                 // evaluated as the reference does
                 float wgt;
-                if (!(sep && ds_separable_weight(D_MUL(wx[x - xa], wy[y - ya]), 0x1p-45, wgt))) {
+                if (!(sep && ds_separable_weight<45>(D_MUL(wx[x - xa], wy[y - ya]), wgt))) {
                     const double ddx = D_SUB((double)x, cx), ddy = D_SUB((double)y, cy);
                     const double arg = D_DIV(-D_ADD(D_MUL(ddx, ddx), D_MUL(ddy, ddy)), denom);
                     wgt = (float)dsift_exp_mid(arg);
