@@ -732,6 +732,13 @@ describe_fast_kernel(const __grid_constant__ DescArgs a) {
 // rounding-interval test against the reference's pairwise tree); keypoints
 // with an uncertified bin go to the exact kernel.
 // ------------------------------------------------------------------------------
+#ifndef DSIFT_P1_TH
+#define DSIFT_P1_TH 4
+#endif
+#ifndef DSIFT_P1_ILP
+#define DSIFT_P1_ILP 2
+#endif
+constexpr int kP1Ilp = DSIFT_P1_ILP;   // interior samples in flight per thread
 constexpr int kSRing = 32;                 // sample rows resident (power of two)
 constexpr int kSMaxPassRows = kSRing - 2;  // lattice rows per pass (+2 guard rows)
 constexpr int kSLanes = 125;               // accumulation lanes: 5 cells x 25 parts ... 25 x 5
@@ -926,13 +933,35 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float inv_sw = 1.0f / (float)sw;   // exact row split for idx < 2^16
                 const int ns = (s1 - s0 + 1) * sw;
                 if (interior) {   // every lattice sample in [0, w-2] x [0, h-2]: no tests, no clamps
-                    for (int idx = tid; idx < ns; idx += 2 * kDescThreads) {
-                        int off[2], slot[2];
-                        float fx[2], fy[2];
+#if DSIFT_P1_TH > 1
+                    // warp = TH x TW block of samples: its bilinear footprints
+                    // share fewer cache lines than a 32-sample row segment
+                    constexpr int TH = DSIFT_P1_TH, TW = 32 / DSIFT_P1_TH;
+                    const int tpr = (sw + TW - 1) / TW, nr = s1 - s0 + 1;
+                    const float inv_tpr = 1.0f / (float)tpr;
+                    const int nsb = ((nr + TH - 1) / TH) * tpr * 32;
+#else
+                    const int nsb = ns;
+#endif
+                    for (int idx = tid; idx < nsb; idx += kP1Ilp * kDescThreads) {
+                        int off[kP1Ilp], slot[kP1Ilp];
+                        float fx[kP1Ilp], fy[kP1Ilp];
+                        bool ok[kP1Ilp];
 #pragma unroll
-                        for (int j = 0; j < 2; ++j) {
+                        for (int j = 0; j < kP1Ilp; ++j) {
+#if DSIFT_P1_TH > 1
+                            const int id = idx + j * kDescThreads;
+                            const int t = id >> 5, l = id & 31;
+                            const int tr = (int)(((float)t + 0.5f) * inv_tpr), tc = t - tr * tpr;
+                            int rr = tr * TH + l / TW, cc = tc * TW + (l & (TW - 1));
+                            ok[j] = id < nsb && rr < nr && cc < sw;
+                            rr = min(rr, nr - 1);
+                            cc = min(cc, sw - 1);
+#else
                             const int id = min(idx + j * kDescThreads, ns - 1);
+                            ok[j] = idx + j * kDescThreads < ns;
                             const int rr = (int)(((float)id + 0.5f) * inv_sw), cc = id - rr * sw;
+#endif
                             const int vv = s0 + rr, u = ub + cc;
                             const double px = D_SUB(S.ax[u - kA], S.sv[vv - kA]);
                             const double py = D_ADD(S.cysu[u - kA], S.cv[vv - kA]);
@@ -942,9 +971,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                             off[j] = iy * pitch + ix;
                             slot[j] = (vv & (kSRing - 1)) * ring_pitch + cc;
                         }
-                        float v00[2], v10[2], v01[2], v11[2];
+                        float v00[kP1Ilp], v10[kP1Ilp], v01[kP1Ilp], v11[kP1Ilp];
 #pragma unroll
-                        for (int j = 0; j < 2; ++j) {
+                        for (int j = 0; j < kP1Ilp; ++j) {
                             const float* r0 = img + off[j];
                             v00[j] = __ldg(r0);
                             v10[j] = __ldg(r0 + 1);
@@ -952,10 +981,10 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                             v11[j] = __ldg(r0 + pitch + 1);
                         }
 #pragma unroll
-                        for (int j = 0; j < 2; ++j) {
+                        for (int j = 0; j < kP1Ilp; ++j) {
                             const float top = F_ADD(v00[j], F_MUL(fx[j], F_SUB(v10[j], v00[j])));
                             const float bot = F_ADD(v01[j], F_MUL(fx[j], F_SUB(v11[j], v01[j])));
-                            if (idx + j * kDescThreads < ns) S.ring[slot[j]] = F_ADD(top, F_MUL(fy[j], F_SUB(bot, top)));
+                            if (ok[j]) S.ring[slot[j]] = F_ADD(top, F_MUL(fy[j], F_SUB(bot, top)));
                         }
                     }
                 } else

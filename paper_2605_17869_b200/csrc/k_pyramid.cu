@@ -404,21 +404,48 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
                           y0 - R >= 0 && y0 + kB2H + R <= h;
     if (interior) {
         // asynchronous 16-byte copies: the whole tile is in flight at once
+        // (chunk i = r * kV + q of thread t: t, t + 256, ...; the row / column
+        // and both addresses advance incrementally)
         constexpr int kV = G::kInW / 4;
-        const float* gsrc = src + (long long)(y0 - R) * pitch + cx0;
-        for (int i = threadIdx.x; i < G::kHR * kV; i += kB2Threads) {
-            const int r = i / kV, q = i - r * kV;
-            const unsigned sa = (unsigned)__cvta_generic_to_shared(sm2 + r * G::kInPitch + 4 * q);
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc + (long long)r * pitch + 4 * q));
+        constexpr int kDr = kB2Threads / kV, kDq = kB2Threads % kV;
+        const int r0 = threadIdx.x / kV, q0 = threadIdx.x - r0 * kV;
+        {
+            int r = r0, q = q0;
+            const float* gp = src + (long long)(y0 - R + r) * pitch + cx0 + 4 * q;
+            unsigned sa = (unsigned)__cvta_generic_to_shared(sm2 + r * G::kInPitch + 4 * q);
+            while (r < G::kHR) {
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gp));
+                r += kDr;
+                q += kDq;
+                gp += kDr * pitch + 4 * kDq;
+                sa += 4 * (kDr * G::kInPitch + 4 * kDq);
+                if (q >= kV) {
+                    q -= kV;
+                    ++r;
+                    gp += pitch - 4 * kV;
+                    sa += 4 * (G::kInPitch - 4 * kV);
+                }
+            }
         }
         asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
-        for (int i = threadIdx.x; i < G::kHR * kV; i += kB2Threads) {
-            const int r = i / kV, q = i - r * kV;
-            const float4 v = *reinterpret_cast<const float4*>(sm2 + r * G::kInPitch + 4 * q);
-            const int m = min(min(__float_as_int(v.x), __float_as_int(v.y)), min(__float_as_int(v.z), __float_as_int(v.w)));
-            const int M = max(max(__float_as_int(v.x), __float_as_int(v.y)), max(__float_as_int(v.z), __float_as_int(v.w)));
-            alu_ok &= (m >= 0x0d800000) & (M < 0x7f800000);
+        {
+            int r = r0, q = q0, m = 0x7fffffff, M = 0;
+            const float* sp = sm2 + r * G::kInPitch + 4 * q;
+            while (r < G::kHR) {
+                const int4 v = *reinterpret_cast<const int4*>(sp);
+                m = min(m, min(min(v.x, v.y), min(v.z, v.w)));
+                M = max(M, max(max(v.x, v.y), max(v.z, v.w)));
+                r += kDr;
+                q += kDq;
+                sp += kDr * G::kInPitch + 4 * kDq;
+                if (q >= kV) {
+                    q -= kV;
+                    ++r;
+                    sp += G::kInPitch - 4 * kV;
+                }
+            }
+            alu_ok = (m >= 0x0d800000) & (M < 0x7f800000);
         }
     } else if (MODE == kModeUpsample && cx0 >= 0 && cx0 + G::kInW <= w - 1 && y0 - R >= 0 &&
                y0 + kB2H + R <= h - 1) {
