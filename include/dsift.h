@@ -35,7 +35,9 @@ enum {
     DSIFT_ENOMEM = 4,    /* device or host allocation failed                  */
     DSIFT_ESTATE = 5,    /* call order violated (e.g. no result yet)          */
     DSIFT_ERANGE = 6,    /* std::out_of_range in the reference (NaN input)   */
-    DSIFT_EIO = 7        /* std::runtime_error in the reference (image I/O)  */
+    DSIFT_EIO = 7,       /* std::runtime_error in the reference (image I/O)  */
+    DSIFT_EGEOM = 8      /* std::runtime_error in the reference (geometry:
+                            degenerate DLT, point at infinity)               */
 };
 
 /* detsift::SiftConfig (core.hpp:30-47).  dsp_scales is borrowed by the call. */
@@ -116,6 +118,30 @@ typedef struct dsift_match {
 int dsift_ratio_match(dsift_ctx* ctx, const float* desc_a, int64_t n_a, const float* desc_b, int64_t n_b,
                       int dim_a, int dim_b, float ratio, int flags, dsift_match* out, int64_t cap,
                       int64_t* n_pairs, int64_t* putative_a, int64_t* putative_b);
+/* ---- robust homography ------------------------------------ */
+/* detsift::MagsacResult (geom.hpp:55-61) without the mask vector. */
+typedef struct dsift_magsac_result {
+    int32_t success;
+    int32_t best_iteration; /* -1 when no hypothesis was valid            */
+    double score;           /* winning hypothesis score (0 on failure)    */
+    double h[9];            /* refit model, row-major (identity on failure) */
+} dsift_magsac_result;
+/* detsift::magsac_lite (geom.hpp:63-67, geom.cpp:181-320): seeded hypotheses
+ * (host SplitMix64 stream, as the reference draws them), minimal-sample DLT,
+ * soft truncated-quadratic scores (detsum tree) and the weighted refit on the
+ * device; bit-identical to the reference.  matches: host n x 4 doubles
+ * (x1, y1, x2, y2) = detsift::Correspondence.  inlier_mask (n bytes, may be
+ * NULL) is all zero on failure.  DSIFT_EINVAL for the reference's
+ * std::invalid_argument cases (n < 4, tau <= 0, iterations < 1). */
+int dsift_magsac_lite(dsift_ctx* ctx, const double* matches, int64_t n, int32_t iterations, double tau,
+                      uint64_t seed, dsift_magsac_result* result, uint8_t* inlier_mask);
+/* detsift::dlt_homography (geom.hpp:47-52, geom.cpp:108-161): normalized DLT
+ * on the device, optional per-correspondence weights (NULL = 1).  DSIFT_EGEOM
+ * where the reference throws std::runtime_error (degenerate / non-finite). */
+int dsift_dlt_homography(dsift_ctx* ctx, const double* matches, int64_t n, const double* weights, double* h_out);
+/* detsift::corner_error (geom.hpp:69-71, geom.cpp:322-333); DSIFT_EGEOM if a
+ * corner maps to infinity. */
+int dsift_corner_error(const double* h_est, const double* h_gt, double width, double height, double* out);
 /* Reads a binary PNM (P5/P6, maxval 255) like detsift::load_image
  * (io.cpp:49-81), with its error messages (DSIFT_EIO).  Pass pixels = NULL to
  * query w, h, channels; otherwise pixels must hold w*h*channels bytes

@@ -168,6 +168,49 @@ class Oracle:
             raise OracleError(self.error())
         return out[:n], int(put[0]), int(put[1])
 
+    # ---- geometry (geom.cpp:108-333), reference only ----------------------
+    def _geom_rc(self, rc):
+        if rc == 1:
+            raise ValueError(self.error())
+        if rc == 2:
+            raise RuntimeError(self.error())
+
+    def magsac_lite(self, matches, iterations: int, tau: float, seed: int, workers: int = 1):
+        """(success, best_iteration, score, h [9], inlier_mask [n]) of
+        detsift::magsac_lite."""
+        if self.kind != "reference":
+            raise OracleError("magsac_lite: the reference library only")
+        m = np.ascontiguousarray(matches, np.float64).reshape(-1, 4)
+        fn = self.lib.oref_magsac_lite
+        fn.argtypes = [C.c_void_p, C.c_int64, C.c_int, C.c_double, C.c_uint64, C.c_int, C.c_void_p,
+                       C.c_void_p, C.c_void_p]
+        sb = np.zeros(2, np.int32)
+        sh = np.zeros(10, np.float64)
+        mask = np.zeros(len(m), np.uint8)
+        self._geom_rc(fn(m.ctypes.data, len(m), int(iterations), C.c_double(tau), C.c_uint64(seed), workers,
+                         sb.ctypes.data, sh.ctypes.data, mask.ctypes.data))
+        return bool(sb[0]), int(sb[1]), float(sh[0]), sh[1:].copy(), mask
+
+    def dlt_homography(self, matches, weights=None) -> np.ndarray:
+        if self.kind != "reference":
+            raise OracleError("dlt_homography: the reference library only")
+        m = np.ascontiguousarray(matches, np.float64).reshape(-1, 4)
+        fn = self.lib.oref_dlt_homography
+        fn.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]
+        w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        out = np.zeros(9, np.float64)
+        self._geom_rc(fn(m.ctypes.data, len(m), None if w is None else w.ctypes.data, out.ctypes.data))
+        return out
+
+    def corner_error(self, h_est, h_gt, width: float, height: float) -> float:
+        fn = self.lib.oref_corner_error
+        fn.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_void_p]
+        a = np.ascontiguousarray(h_est, np.float64).reshape(9)
+        b = np.ascontiguousarray(h_gt, np.float64).reshape(9)
+        out = C.c_double()
+        self._geom_rc(fn(a.ctypes.data, b.ctypes.data, float(width), float(height), C.byref(out)))
+        return out.value
+
     def descriptor_distance(self, a: np.ndarray, b: np.ndarray) -> float:
         fn = self.lib.oref_descriptor_distance
         fn.restype = C.c_float

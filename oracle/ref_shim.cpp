@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <functional>
+#include <stdexcept>
 #include <memory>
 #include <string>
 #include <vector>
@@ -162,6 +164,56 @@ int64_t oref_ratio_match(const float* da, int64_t na, const float* db, int64_t n
 }
 float oref_descriptor_distance(const float* a, const float* b, int dim) {
     return descriptor_distance(std::span<const float>(a, dim), std::span<const float>(b, dim));
+}
+
+// ---- geometry: geom.cpp:108-161 (dlt_homography), :181-320 (magsac_lite),
+// :322-333 (corner_error).  m = n x 4 doubles (x1, y1, x2, y2).
+// Returns 0, or 1 for std::invalid_argument, 2 for std::runtime_error.
+static std::vector<Correspondence> to_corr(const double* m, int64_t n) {
+    std::vector<Correspondence> v((size_t)n);
+    for (int64_t i = 0; i < n; ++i) v[(size_t)i] = {m[4 * i], m[4 * i + 1], m[4 * i + 2], m[4 * i + 3]};
+    return v;
+}
+static int geom_guard(const std::function<void()>& f) {
+    try {
+        f();
+        return 0;
+    } catch (const std::invalid_argument& e) {
+        g_err = e.what();
+        return 1;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 2;
+    }
+}
+int oref_dlt_homography(const double* m, int64_t n, const double* w, double* h_out) {
+    return geom_guard([&] {
+        const auto c = to_corr(m, n);
+        const Homography h = w ? dlt_homography(c, std::span<const double>(w, (size_t)n)) : dlt_homography(c);
+        for (int i = 0; i < 9; ++i) h_out[i] = h.h[i];
+    });
+}
+int oref_magsac_lite(const double* m, int64_t n, int iterations, double tau, uint64_t seed, int workers,
+                     int32_t* success_best, double* score_h /*[10]*/, uint8_t* mask) {
+    return geom_guard([&] {
+        const auto c = to_corr(m, n);
+        const MagsacResult r = magsac_lite(c, iterations, tau, seed, workers);
+        success_best[0] = r.success ? 1 : 0;
+        success_best[1] = r.best_iteration;
+        score_h[0] = r.score;
+        for (int i = 0; i < 9; ++i) score_h[1 + i] = r.h.h[i];
+        for (int64_t i = 0; i < n; ++i) mask[i] = r.success ? r.inlier_mask[(size_t)i] : 0;
+    });
+}
+int oref_corner_error(const double* he, const double* hg, double w, double h, double* out) {
+    return geom_guard([&] {
+        Homography a, b;
+        for (int i = 0; i < 9; ++i) {
+            a.h[i] = he[i];
+            b.h[i] = hg[i];
+        }
+        *out = corner_error(a, b, w, h);
+    });
 }
 
 // ---- full pipeline: io.cpp:111-142 -----------------------------------------

@@ -18,6 +18,7 @@ import os
 from dataclasses import dataclass, field
 
 import numpy as np
+from typing import NamedTuple
 
 __all__ = [
     "SiftConfig", "FeatureSet", "KEYPOINT_DTYPE", "DsiftError", "Extractor", "extract",
@@ -31,7 +32,8 @@ KEYPOINT_DTYPE = np.dtype(
 MATCH_DTYPE = np.dtype([("a", np.int32), ("b", np.int32), ("distance", np.float32)])   # detsift::Match
 DESC_DIM = 128
 
-DSIFT_OK, DSIFT_EINVAL, DSIFT_ECAPACITY, DSIFT_ECUDA, DSIFT_ENOMEM, DSIFT_ESTATE, DSIFT_ERANGE, DSIFT_EIO = range(8)
+(DSIFT_OK, DSIFT_EINVAL, DSIFT_ECAPACITY, DSIFT_ECUDA, DSIFT_ENOMEM, DSIFT_ESTATE, DSIFT_ERANGE, DSIFT_EIO,
+ DSIFT_EGEOM) = range(9)
 INPUT_HOST, INPUT_DEVICE = 0, 1
 
 
@@ -47,6 +49,11 @@ class InvalidArgument(DsiftError, ValueError):
 
 class ImageIOError(DsiftError, RuntimeError):
     """std::runtime_error from load_image (io.cpp:49-81)."""
+
+
+class GeometryError(DsiftError, RuntimeError):
+    """std::runtime_error from the geometry code (geom.cpp: degenerate DLT,
+    point mapped to infinity)."""
 
 
 class OutOfRange(DsiftError, IndexError):
@@ -144,6 +151,9 @@ def load_library():
         "dsift_load_image": ([C.c_char_p, vp, vp, vp, vp, i64], C.c_int),
         "dsift_ratio_match": ([vp, vp, i64, vp, i64, i32, i32, C.c_float, i32, vp, i64, vp, vp, vp], C.c_int),
         "dsift_ingest_u8": ([vp, vp, i64, i32, i32, vp], C.c_int),
+        "dsift_magsac_lite": ([vp, vp, i64, i32, C.c_double, C.c_uint64, vp, vp], C.c_int),
+        "dsift_dlt_homography": ([vp, vp, i64, vp, vp], C.c_int),
+        "dsift_corner_error": ([vp, vp, C.c_double, C.c_double, vp], C.c_int),
         "dsift_result_sync": ([vp, vp], C.c_int), "dsift_result_range": ([vp, i32, vp, vp], C.c_int),
         "dsift_result_copy": ([vp, vp, vp, vp, vp], C.c_int),
         "dsift_result_device": ([vp, vp, vp, vp, vp], C.c_int),
@@ -182,6 +192,8 @@ def _check(lib, rc: int) -> None:
             raise OutOfRange(rc, msg)
         if rc == DSIFT_EIO:
             raise ImageIOError(rc, msg)
+        if rc == DSIFT_EGEOM:
+            raise GeometryError(rc, msg)
         raise DsiftError(rc, f"{lib.dsift_strerror(rc).decode()}: {msg}")
 
 
@@ -332,6 +344,32 @@ class Extractor:
                                                     C.c_float(ratio), flags, out.ctypes.data, cap, C.byref(n),
                                                     C.byref(put_a), C.byref(put_b)))
         return out[:n.value], put_a.value, put_b.value
+
+    def magsac_lite(self, matches, iterations: int, tau: float, seed: int):
+        """detsift::magsac_lite (geom.cpp:181-320) on the device.  matches: [n, 4]
+        float64 (x1, y1, x2, y2) = detsift::Correspondence.  Returns a
+        MagsacResult (success, h [3, 3], inlier_mask uint8 [n], score,
+        best_iteration), bit-identical to the reference."""
+        m = np.ascontiguousarray(matches, np.float64).reshape(-1, 4)
+        res = _MagsacResult()
+        mask = np.zeros(len(m), np.uint8)
+        _check(self.lib, self.lib.dsift_magsac_lite(self.ctx, m.ctypes.data, len(m), int(iterations),
+                                                    C.c_double(tau), C.c_uint64(seed), C.byref(res),
+                                                    mask.ctypes.data))
+        return MagsacResult(bool(res.success), np.array(res.h, np.float64).reshape(3, 3),
+                            mask if res.success else np.zeros(0, np.uint8), float(res.score),
+                            int(res.best_iteration))
+
+    def dlt_homography(self, matches, weights=None) -> np.ndarray:
+        """detsift::dlt_homography (geom.cpp:108-161) on the device: [3, 3]."""
+        m = np.ascontiguousarray(matches, np.float64).reshape(-1, 4)
+        w = None if weights is None else np.ascontiguousarray(weights, np.float64)
+        if w is not None and len(w) != len(m):
+            raise InvalidArgument(DSIFT_EINVAL, "dlt: weight count mismatch")
+        out = np.zeros(9, np.float64)
+        _check(self.lib, self.lib.dsift_dlt_homography(self.ctx, m.ctypes.data, len(m),
+                                                       None if w is None else w.ctypes.data, out.ctypes.data))
+        return out.reshape(3, 3)
 
     def extract(self, img) -> FeatureSet:
         """detsift::extract (io.cpp:111-142) for one image."""
@@ -498,6 +536,30 @@ def load_image(path: str) -> np.ndarray:
     _check(lib, lib.dsift_load_image(os.fsencode(path), C.byref(w), C.byref(h), C.byref(ch),
                                      out.ctypes.data, out.size))
     return out
+
+
+class _MagsacResult(C.Structure):
+    _fields_ = [("success", C.c_int32), ("best_iteration", C.c_int32), ("score", C.c_double),
+                ("h", C.c_double * 9)]
+
+
+class MagsacResult(NamedTuple):
+    """detsift::MagsacResult (geom.hpp:55-61)."""
+    success: bool
+    h: np.ndarray
+    inlier_mask: np.ndarray
+    score: float
+    best_iteration: int
+
+
+def corner_error(h_est, h_gt, width: float, height: float) -> float:
+    """detsift::corner_error (geom.cpp:322-333): mean corner displacement."""
+    lib = load_library()
+    a = np.ascontiguousarray(h_est, np.float64).reshape(9)
+    b = np.ascontiguousarray(h_gt, np.float64).reshape(9)
+    out = C.c_double()
+    _check(lib, lib.dsift_corner_error(a.ctypes.data, b.ctypes.data, float(width), float(height), C.byref(out)))
+    return out.value
 
 
 def extract(img, cfg: SiftConfig | None = None, device: int = 0) -> FeatureSet:

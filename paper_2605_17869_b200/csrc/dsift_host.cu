@@ -214,7 +214,7 @@ struct dsift_ctx {
     Plan plan;
     int batch = 0;            // images in the current pyramid / result
     PyramidDesc pyr{};
-    DevBuf det_aux, input_u8, ori_aux, match_in, match_scratch, match_best;
+    DevBuf det_aux, input_u8, ori_aux, match_in, match_scratch, match_best, geom_in, geom_scratch, geom_out;
     DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
         pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow,
         ref_states, keep;
@@ -746,6 +746,7 @@ const char* dsift_strerror(int code) {
         case DSIFT_ESTATE: return "invalid call order";
         case DSIFT_ERANGE: return "out of range";
         case DSIFT_EIO: return "image I/O error";
+        case DSIFT_EGEOM: return "degenerate geometry";
         default: return "unknown error";
     }
 }
@@ -893,6 +894,158 @@ int dsift_ratio_match(dsift_ctx* c, const float* desc_a, int64_t n_a, const floa
         if (n_pairs) *n_pairs = np;
         if (putative_a) *putative_a = pa;
         if (putative_b) *putative_b = pb;
+    });
+}
+
+// ---- robust homography (geom.cpp:104-320) ------------------------
+// Hypothesis samples: the reference's sequential seeded stream (geom.cpp:193-232),
+// drawn here on the host exactly as the reference draws them.
+namespace {
+struct SplitMix64 {
+    uint64_t state;
+    uint64_t next() {
+        uint64_t z = (state += 0x9e3779b97f4a7c15ull);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+        return z ^ (z >> 31);
+    }
+};
+
+std::vector<int4> magsac_samples(const double* m, int64_t n, int iterations, uint64_t seed) {
+    SplitMix64 rng{seed};
+    std::vector<int4> out;
+    out.reserve((size_t)iterations);
+    for (int it = 0; it < iterations; ++it) {
+        int sample[4] = {-1, -1, -1, -1};
+        bool ok = false;
+        for (int attempt = 0; attempt < 64 && !ok; ++attempt) {
+            int filled = 0, guard = 0;
+            while (filled < 4 && guard < 256) {
+                ++guard;
+                const int idx = static_cast<int>(rng.next() % (uint64_t)n);
+                bool dup = false;
+                for (int k = 0; k < filled; ++k) dup |= (sample[k] == idx);
+                if (!dup) sample[filled++] = idx;
+            }
+            if (filled < 4) break;
+            double xs[4], ys[4], xd[4], yd[4];
+            for (int k = 0; k < 4; ++k) {
+                xs[k] = m[4 * sample[k]];
+                ys[k] = m[4 * sample[k] + 1];
+                xd[k] = m[4 * sample[k] + 2];
+                yd[k] = m[4 * sample[k] + 3];
+            }
+            double span = 1e-12;
+            for (int p = 0; p < 4; ++p)
+                for (int q = p + 1; q < 4; ++q)
+                    span = std::max({span, std::fabs(xs[p] - xs[q]), std::fabs(ys[p] - ys[q])});
+            bool degenerate = false;
+            for (int p = 0; p < 4 && !degenerate; ++p)
+                for (int q = p + 1; q < 4 && !degenerate; ++q)
+                    for (int r = q + 1; r < 4 && !degenerate; ++r) {
+                        const double area = (xs[q] - xs[p]) * (ys[r] - ys[p]) - (xs[r] - xs[p]) * (ys[q] - ys[p]);
+                        const double area_d = (xd[q] - xd[p]) * (yd[r] - yd[p]) - (xd[r] - xd[p]) * (yd[q] - yd[p]);
+                        if (std::fabs(area) < 1e-8 * span * span || std::fabs(area_d) < 1e-8 * span * span)
+                            degenerate = true;
+                    }
+            ok = !degenerate;
+        }
+        out.push_back(ok ? make_int4(sample[0], sample[1], sample[2], sample[3]) : make_int4(-1, -1, -1, -1));
+    }
+    return out;
+}
+}  // namespace
+
+int dsift_magsac_lite(dsift_ctx* c, const double* matches, int64_t n, int32_t iterations, double tau, uint64_t seed,
+                      dsift_magsac_result* res, uint8_t* inlier_mask) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (n < 4) invalid("magsac_lite: need at least 4 correspondences");
+        if (!(tau > 0.0)) invalid("magsac_lite: tau must be > 0");
+        if (iterations < 1) invalid("magsac_lite: iterations must be >= 1");
+        if (!matches || !res) invalid("magsac_lite: null argument");
+        if (n > (int64_t)INT32_MAX) invalid("magsac_lite: too many correspondences");
+        set_device(c);
+        const std::vector<int4> samples = magsac_samples(matches, n, iterations, seed);
+        const size_t bm = sizeof(double) * 4 * (size_t)n, bs = sizeof(int4) * (size_t)iterations;
+        c->geom_in.ensure(bm + bs + (size_t)n + 1024);
+        char* p = c->geom_in.as<char>();
+        double* dm = reinterpret_cast<double*>(p);
+        int4* ds = reinterpret_cast<int4*>(p + ((bm + 255) & ~size_t(255)));
+        unsigned char* dmask = reinterpret_cast<unsigned char*>(p + ((bm + 255) & ~size_t(255)) + ((bs + 255) & ~size_t(255)));
+        c->geom_scratch.ensure(magsac_scratch_bytes(n, iterations));
+        c->geom_out.ensure(256);
+        int* out_i = c->geom_out.as<int>();
+        double* out_d = reinterpret_cast<double*>(c->geom_out.as<char>() + 64);
+        cuda_check(cudaMemcpyAsync(dm, matches, bm, cudaMemcpyHostToDevice, c->stream), "H2D");
+        cuda_check(cudaMemcpyAsync(ds, samples.data(), bs, cudaMemcpyHostToDevice, c->stream), "H2D");
+        cuda_check(launch_magsac(dm, n, ds, iterations, tau * tau, c->geom_scratch.as<void>(), dmask, out_i, out_d,
+                                 c->stream),
+                   "magsac");
+        c->launches += 3;
+        int hi[2];
+        double hd[10];
+        cuda_check(cudaMemcpyAsync(hi, out_i, sizeof(hi), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaMemcpyAsync(hd, out_d, sizeof(hd), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        if (inlier_mask)
+            cuda_check(cudaMemcpyAsync(inlier_mask, dmask, (size_t)n, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        res->success = hi[0];
+        res->best_iteration = hi[1];
+        res->score = hi[0] ? hd[0] : 0.0;
+        const double ident[9] = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+        for (int i = 0; i < 9; ++i) res->h[i] = hi[0] ? hd[1 + i] : ident[i];
+        if (!hi[0]) res->best_iteration = hi[1] >= 0 ? hi[1] : -1;
+    });
+}
+
+int dsift_dlt_homography(dsift_ctx* c, const double* matches, int64_t n, const double* weights, double* h_out) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (n < 4) invalid("dlt: need at least 4 correspondences");
+        if (!matches || !h_out) invalid("dlt: null argument");
+        if (n > (int64_t)INT32_MAX) invalid("dlt: too many correspondences");
+        set_device(c);
+        const size_t bm = sizeof(double) * 4 * (size_t)n, bw = weights ? sizeof(double) * (size_t)n : 0;
+        c->geom_in.ensure(bm + bw + 1024);
+        char* p = c->geom_in.as<char>();
+        double* dm = reinterpret_cast<double*>(p);
+        double* dw = weights ? reinterpret_cast<double*>(p + ((bm + 255) & ~size_t(255))) : nullptr;
+        c->geom_scratch.ensure(dlt_scratch_bytes(n));
+        c->geom_out.ensure(256);
+        int* st = c->geom_out.as<int>();
+        double* out = reinterpret_cast<double*>(c->geom_out.as<char>() + 64);
+        cuda_check(cudaMemcpyAsync(dm, matches, bm, cudaMemcpyHostToDevice, c->stream), "H2D");
+        if (dw) cuda_check(cudaMemcpyAsync(dw, weights, bw, cudaMemcpyHostToDevice, c->stream), "H2D");
+        cuda_check(launch_dlt(dm, dw, (int)n, c->geom_scratch.as<void>(), st, out, c->stream), "dlt");
+        c->launches += 1;
+        int status = 0;
+        cuda_check(cudaMemcpyAsync(&status, st, sizeof(int), cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaMemcpyAsync(h_out, out, sizeof(double) * 9, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        if (!status) throw Error{DSIFT_EGEOM, "dlt: degenerate or non-finite solution"};
+    });
+}
+
+// corner_error (geom.cpp:322-333): four corners, host arithmetic (std::hypot).
+int dsift_corner_error(const double* h_est, const double* h_gt, double width, double height, double* out) {
+    return guard([&] {
+        if (!h_est || !h_gt || !out) invalid("corner_error: null argument");
+        const double corners[4][2] = {{0, 0}, {width, 0}, {width, height}, {0, height}};
+        auto apply = [](const double* h, double x, double y, double& ox, double& oy) {
+            const double w = h[6] * x + h[7] * y + h[8];
+            if (std::fabs(w) < 1e-12) throw Error{DSIFT_EGEOM, "homography: point maps to infinity"};
+            ox = (h[0] * x + h[1] * y + h[2]) / w;
+            oy = (h[3] * x + h[4] * y + h[5]) / w;
+        };
+        double sum = 0.0;
+        for (const auto& cn : corners) {
+            double ex, ey, gx, gy;
+            apply(h_est, cn[0], cn[1], ex, ey);
+            apply(h_gt, cn[0], cn[1], gx, gy);
+            sum += std::hypot(ex - gx, ey - gy);
+        }
+        *out = sum / 4.0;
     });
 }
 

@@ -126,6 +126,13 @@ cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev,
                         long long cap, cudaStream_t st);
 
 size_t match_scratch_bytes(long long na, long long nb);
+// k_geom.cu: m = n x 4 doubles (x1, y1, x2, y2)
+size_t magsac_scratch_bytes(long long n, int iters);
+cudaError_t launch_magsac(const double* m, long long n, const int4* samples, int iters, double tau_sq, void* scratch,
+                          unsigned char* mask, int* out_i, double* out_d, cudaStream_t st);
+size_t dlt_scratch_bytes(long long n);
+cudaError_t launch_dlt(const double* m, const double* w, int n, void* scratch, int* status, double* out,
+                       cudaStream_t st);
 cudaError_t launch_ratio_match(const float* A, long long na, const float* B, long long nb, float ratio, void* scratch,
                                int* best_a, int* best_b, float* dist_a, cudaStream_t st);
 cudaError_t launch_ingest_u8(const unsigned char* in, long long n_px, int channels, float* out, cudaStream_t st);

@@ -165,3 +165,46 @@ int64_t lc_div2pi_mismatch(float tmax) {
     return bad;
 }
 }
+
+extern "C" {
+// ds_hypot vs glibc hypot: mode 0 pixel-scale coordinates (Hartley
+// normalization inputs), mode 1 arbitrary finite doubles, mode 2 specials.
+int64_t lc_hypot_mismatch(uint64_t seed, int64_t n, int mode, double* first_bad /*[3]*/) {
+    Rng r{seed};
+    int64_t bad = 0;
+    const double specials[] = {0.0, -0.0, 1.0, -1.0, INFINITY, -INFINITY, NAN, 1e-320, 1.7e308,
+                               0x1p-511, 0x1p511, 0x1p-600, 3.0, 4.0};
+    const int ns = sizeof(specials) / sizeof(double);
+    for (int64_t i = 0; i < n; ++i) {
+        double x, y;
+        if (mode == 0) {
+            x = (r.uni() - 0.5) * 6000.0;
+            y = (r.uni() - 0.5) * 6000.0;
+            if (i % 3 == 1) y *= 1e-4;
+            if (i % 7 == 2) x = y * (1.0 + r.uni() * 1e-9);
+        } else if (mode == 1) {
+            do {
+                uint64_t u = r.next();
+                std::memcpy(&x, &u, 8);
+            } while (!std::isfinite(x));
+            do {
+                uint64_t u = r.next();
+                std::memcpy(&y, &u, 8);
+            } while (!std::isfinite(y));
+        } else {
+            x = specials[i % ns];
+            y = specials[(i / ns) % ns];
+        }
+        const double g = std::hypot(x, y), m = ds_hypot(x, y);
+        if (dbits(g) != dbits(m) && !(std::isnan(g) && std::isnan(m))) {
+            if (bad == 0 && first_bad) {
+                first_bad[0] = x;
+                first_bad[1] = y;
+                first_bad[2] = m;
+            }
+            ++bad;
+        }
+    }
+    return bad;
+}
+}

@@ -57,3 +57,13 @@ def test_div_2pi_exhaustive(lc):
     lc.lc_div2pi_mismatch.restype = C.c_int64
     lc.lc_div2pi_mismatch.argtypes = [C.c_float]
     assert lc.lc_div2pi_mismatch(512.0) == 0
+
+
+@pytest.mark.parametrize("mode,n", [(0, 2_000_000), (1, 1_000_000), (2, 196)])
+def test_hypot_bit_exact(lc, mode, n):
+    # Hartley normalization's std::hypot (geom.cpp:83-84) restated from glibc
+    lc.lc_hypot_mismatch.restype = C.c_int64
+    lc.lc_hypot_mismatch.argtypes = [C.c_uint64, C.c_int64, C.c_int, C.c_void_p]
+    first = (C.c_double * 3)()
+    bad = lc.lc_hypot_mismatch(4242 + mode, n, mode, first)
+    assert bad == 0, f"{bad} mismatches, first (x, y, got) = {list(first)}"
