@@ -160,6 +160,37 @@ def cpu_reference_time(img, workers):
     return time.perf_counter() - t0, kind, workers, len(kps)
 
 
+def magsac_cases():
+    """Correspondences for the f4 measurement: the reference's acceptance
+    configuration (acceptance.cpp:255-281: 60 inliers + 40 outliers, 1500
+    iterations) and a 2000-correspondence set (40% outliers)."""
+    def sm(seed):
+        s = [seed & 0xFFFFFFFFFFFFFFFF]
+
+        def nxt():
+            M = 0xFFFFFFFFFFFFFFFF
+            s[0] = (s[0] + 0x9E3779B97F4A7C15) & M
+            z = s[0]
+            z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+            z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+            return z ^ (z >> 31)
+        return lambda lo, hi: lo + (hi - lo) * float(nxt() >> 11) / 9007199254740992.0
+
+    def make(h, seed, n_in, n_out):
+        u = sm(seed)
+        pts = []
+        for _ in range(n_in):
+            x, y = u(10, 630), u(10, 470)
+            w = h[6] * x + h[7] * y + h[8]
+            pts.append((x, y, (h[0] * x + h[1] * y + h[2]) / w, (h[3] * x + h[4] * y + h[5]) / w))
+        for _ in range(n_out):
+            pts.append((u(0, 640), u(0, 480), u(0, 640), u(0, 480)))
+        return np.array(pts, np.float64)
+    h = [1.07, 0.03, -10.0, -0.04, 0.96, 8.0, 2e-5, -1e-5, 1.0]
+    return [("acceptance_100", make(h, 1234567, 60, 40), 1500, 3.0, 1),
+            ("n2000_40pct_outliers", make(h, 7, 1200, 800), 1500, 3.0, 11)]
+
+
 def host_image(w, h, seed):
     from oracle.oracle import Oracle
     return Oracle("port").value_noise(w, h, seed, 5, cells_for(w))
@@ -384,6 +415,21 @@ def run_ours(args, rank, local_rank, world):
                  "n_a": int(offs[1] - offs[0]), "n_b": int(offs[2] - offs[1]), "ms": e0.elapsed_time(e1),
                  "pairs": int(len(pairs)), "putative_a": pa, "putative_b": pb}
 
+    # ---- robust homography: magsac_lite through the C ABI with host
+    # buffers (host sampling + H2D + 3 kernels + D2H inside the wall-clock time)
+    magsac = None
+    if rank == 0:
+        magsac = {"what": "magsac_lite, host correspondences, wall clock per call (C ABI)", "cases": []}
+        for name, m, iters, tau, seed in magsac_cases():
+            ex.magsac_lite(m, iters, tau, seed)   # warm-up
+            reps = 5
+            t1 = time.perf_counter()
+            for _ in range(reps):
+                r = ex.magsac_lite(m, iters, tau, seed)
+            ms = (time.perf_counter() - t1) * 1e3 / reps
+            magsac["cases"].append({"case": name, "n": int(len(m)), "iterations": iters, "ms": ms,
+                                    "success": bool(r.success), "inliers": int(r.inlier_mask.sum())})
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         img = imgs[0].cpu().numpy()
@@ -391,6 +437,15 @@ def run_ours(args, rank, local_rank, world):
         dt, kind, used, nk = cpu_reference_time(img, workers)
         cpu = {"value": 1.0 / dt, "unit": "images/s", "cores": used, "kind": kind,
                "sample": f"1 image {W}x{H} (seed {SEED0:#x}), detsift::extract workers={used}, {nk} keypoints"}
+        if magsac is not None:   # the reference's own magsac_lite on the same correspondences
+            from oracle.oracle import Oracle, available
+            if available("reference"):
+                ref = Oracle("reference")
+                for case, (name, m, iters, tau, seed) in zip(magsac["cases"], magsac_cases()):
+                    t1 = time.perf_counter()
+                    ref.magsac_lite(m, iters, tau, seed, workers=workers)
+                    case["reference_cpu_ms"] = (time.perf_counter() - t1) * 1e3
+                    case["reference_cpu_workers"] = workers
 
     clocks = clk.summary()
     if rank == 0:
@@ -410,6 +465,7 @@ def run_ours(args, rank, local_rank, world):
             "roofline": roofline,
             "roofline_descriptor": roofline_desc,
             "match": match,
+            "magsac": magsac,
             "cpu_baseline": cpu,
             "clocks": clocks,
             "gpu_launches": launches,

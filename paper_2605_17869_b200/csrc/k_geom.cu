@@ -4,14 +4,16 @@
 //
 // The host draws the hypothesis samples from the seeded SplitMix64 stream
 // (geom.cpp:193-232, sequential by definition).  The device then
-//   G1  one thread per hypothesis: normalized 4-point DLT (Hartley scaling,
-//       A^T A, cyclic Jacobi, smallest eigenvector), det / inverse checks;
+//   G1  one warp per hypothesis: normalized 4-point DLT (Hartley scaling,
+//       A^T A, cyclic Jacobi sweeps with the rotations' row updates spread
+//       over the lanes, smallest eigenvector), det / inverse checks;
 //   G2  one CTA per hypothesis: the soft truncated-quadratic terms of every
 //       correspondence and their detsum tree sum (detsum.cpp:19-71);
 //   G3  one CTA: the winner (score descending, iteration ascending), the soft
-//       inliers of the winner, the weighted DLT refit (A^T A entries owned by
-//       45 threads, each summed in the reference's row order) and the final
-//       inlier mask.
+//       inliers of the winner (ordered compaction), the weighted DLT refit
+//       (order-defining sums sequential, elementwise work parallel, A^T A
+//       entries owned by 45 threads in the reference's row order, Jacobi on
+//       one warp) and the final inlier mask.
 // Every floating-point expression is the reference's, evaluated in the same
 // order in IEEE binary64 (no contraction: built with -fmad=false); std::hypot
 // is glibc's algorithm (ds_hypot).  Results are bit-identical to the
@@ -85,13 +87,18 @@ __device__ __forceinline__ double soft_term(double r2, double tau_sq) {
     return (0.0 < t) ? t : 0.0;
 }
 
-// jacobi_eigen_sym on a 9x9 row-major symmetric matrix (linalg.cpp:9-93);
-// writes the eigenvector of the smallest eigenvalue (row 8 of the result,
-// sign-normalized) to hn.  One thread; a and v are scratch [81].
-__device__ void jacobi9_smallest(double* a, double* v, double* hn) {
+// jacobi_eigen_sym on a 9x9 row-major symmetric matrix (linalg.cpp:9-93),
+// one warp: every lane forms the rotation scalars (same operations, same
+// values), lane k < 9 then updates row / column k of A and lane 16 + k row k
+// of V.  Within one rotation no lane reads an element another lane writes
+// (A(k,p), A(k,q) belong to lane k; lane p owns the 2x2 block), so the result
+// is the reference's sequential sweep.  Writes the eigenvector of the smallest
+// eigenvalue (row 8 of the result, sign-normalized) to hn.  a, v: shared [81].
+__device__ void jacobi9_smallest_warp(double* a, double* v, double* hn) {
     const int n = 9;
-    for (int i = 0; i < 81; ++i) v[i] = 0.0;
-    for (int i = 0; i < n; ++i) v[i * n + i] = 1.0;
+    const int lane = threadIdx.x & 31;
+    for (int i = lane; i < 81; i += 32) v[i] = (i % 10 == 0) ? 1.0 : 0.0;
+    __syncwarp();
     double norm = 0.0;
     for (int i = 0; i < n; ++i)
         for (int j = 0; j < n; ++j) norm += a[i * n + j] * a[i * n + j];
@@ -112,23 +119,35 @@ __device__ void jacobi9_smallest(double* a, double* v, double* hn) {
                 const double s = t * c;
                 const double tau = s / (1.0 + c);
                 const double app = a[p * n + p], aqq = a[q * n + q];
-                a[p * n + p] = app - t * apq;
-                a[q * n + q] = aqq + t * apq;
-                a[p * n + q] = 0.0;
-                a[q * n + p] = 0.0;
-                for (int k = 0; k < n; ++k) {
-                    if (k == p || k == q) continue;
-                    const double akp = a[k * n + p], akq = a[k * n + q];
-                    a[k * n + p] = akp - s * (akq + tau * akp);
-                    a[p * n + k] = a[k * n + p];
-                    a[k * n + q] = akq + s * (akp - tau * akq);
-                    a[q * n + k] = a[k * n + q];
+                double akp = 0.0, akq = 0.0, vkp = 0.0, vkq = 0.0;
+                const int k = lane & 15;
+                if (lane < 9 && k != p && k != q) {
+                    akp = a[k * n + p];
+                    akq = a[k * n + q];
+                } else if (lane >= 16 && k < 9) {
+                    vkp = v[k * n + p];
+                    vkq = v[k * n + q];
                 }
-                for (int k = 0; k < n; ++k) {
-                    const double vkp = v[k * n + p], vkq = v[k * n + q];
+                __syncwarp();
+                if (lane < 9) {
+                    if (k == p) {
+                        a[p * n + p] = app - t * apq;
+                        a[q * n + q] = aqq + t * apq;
+                        a[p * n + q] = 0.0;
+                        a[q * n + p] = 0.0;
+                    } else if (k != q) {
+                        const double nkp = akp - s * (akq + tau * akp);
+                        const double nkq = akq + s * (akp - tau * akq);
+                        a[k * n + p] = nkp;
+                        a[p * n + k] = nkp;
+                        a[k * n + q] = nkq;
+                        a[q * n + k] = nkq;
+                    }
+                } else if (lane >= 16 && k < 9) {
                     v[k * n + p] = vkp - s * (vkq + tau * vkp);
                     v[k * n + q] = vkq + s * (vkp - tau * vkq);
                 }
+                __syncwarp();
             }
         }
     }
@@ -156,7 +175,8 @@ __device__ void jacobi9_smallest(double* a, double* v, double* hn) {
         }
     }
     const double sign = v[arg * n + col] < 0.0 ? -1.0 : 1.0;
-    for (int r = 0; r < n; ++r) hn[r] = sign * v[r * n + col];
+    if (lane < n) hn[lane] = sign * v[lane * n + col];
+    __syncwarp();
 }
 
 struct NormT {
@@ -237,48 +257,79 @@ __device__ bool dlt_finish(const double* hn, const NormT& ts, const NormT& td, d
     return true;
 }
 
-// G1: minimal-sample model of every hypothesis (geom.cpp:236-252).
-__global__ void __launch_bounds__(64) magsac_hyp_kernel(const double* __restrict__ m, const int4* __restrict__ samples,
-                                                        int iters, double* __restrict__ models,
-                                                        unsigned char* __restrict__ valid) {
-    const int it = blockIdx.x * blockDim.x + threadIdx.x;
-    if (it >= iters) return;
-    valid[it] = 0;
-    const int4 s = samples[it];
-    if (s.x < 0) return;
-    const int idx[4] = {s.x, s.y, s.z, s.w};
-    double sx[4], sy[4], dx[4], dy[4];
-    for (int k = 0; k < 4; ++k) {
-        sx[k] = m[4 * idx[k] + 0];
-        sy[k] = m[4 * idx[k] + 1];
-        dx[k] = m[4 * idx[k] + 2];
-        dy[k] = m[4 * idx[k] + 3];
+// G1: minimal-sample model of every hypothesis (geom.cpp:236-252), one warp
+// per hypothesis: lane 0 normalizes the 4 points, the lanes own A^T A
+// entries, the warp runs the Jacobi sweeps, lane 0 denormalizes and checks.
+constexpr int kG1Warps = 4;
+__global__ void __launch_bounds__(32 * kG1Warps) magsac_hyp_kernel(const double* __restrict__ m,
+                                                                   const int4* __restrict__ samples, int iters,
+                                                                   double* __restrict__ models,
+                                                                   unsigned char* __restrict__ valid) {
+    __shared__ double sa[kG1Warps][81], sv[kG1Warps][81], shn[kG1Warps][9], spts[kG1Warps][16];
+    __shared__ NormT sts[kG1Warps], std_[kG1Warps];
+    __shared__ int sok[kG1Warps];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int it = blockIdx.x * kG1Warps + w;
+    if (it >= iters) return;   // warp-uniform
+    double* a = sa[w];
+    double* pts = spts[w];   // sx[4], sy[4], dx[4], dy[4], normalized
+    if (lane == 0) {
+        int ok = 0;
+        const int4 s = samples[it];
+        if (s.x >= 0) {
+            const int idx[4] = {s.x, s.y, s.z, s.w};
+            for (int k = 0; k < 4; ++k) {
+                pts[k] = m[4 * idx[k] + 0];
+                pts[4 + k] = m[4 * idx[k] + 1];
+                pts[8 + k] = m[4 * idx[k] + 2];
+                pts[12 + k] = m[4 * idx[k] + 3];
+            }
+            NormT ts, td;
+            ok = hartley(pts, pts + 4, 4, ts) && hartley(pts + 8, pts + 12, 4, td) &&
+                 !three_collinear(pts, pts + 4, 4) && !three_collinear(pts + 8, pts + 12, 4);
+            sts[w] = ts;
+            std_[w] = td;
+        }
+        sok[w] = ok;
     }
-    // copies of the raw target coordinates (rows use the normalized ones)
-    NormT ts, td;
-    if (!hartley(sx, sy, 4, ts) || !hartley(dx, dy, 4, td)) return;
-    if (three_collinear(sx, sy, 4) || three_collinear(dx, dy, 4)) return;
-    double a[81], v[81];
-    for (int i = 0; i < 81; ++i) a[i] = 0.0;
-    for (int i = 0; i < 4; ++i) {
-        double r1[9], r2[9];
-        dlt_rows(1.0, sx[i], sy[i], dx[i], dy[i], r1, r2);
-        ata_add_row(a, r1);
-        ata_add_row(a, r2);
+    __syncwarp();
+    if (!sok[w]) {
+        if (lane == 0) valid[it] = 0;
+        return;
     }
-    for (int p = 0; p < 9; ++p)
-        for (int q = 0; q < p; ++q) a[p * 9 + q] = a[q * 9 + p];
-    double hn[9], h[9], hi[9];
-    jacobi9_smallest(a, v, hn);
-    if (!dlt_finish(hn, ts, td, h)) return;
-    const double det = h_det(h);
-    if (!isfinite(det) || det == 0.0) return;
-    if (!h_inverse(h, hi)) return;
-    for (int i = 0; i < 9; ++i) {
-        models[18 * it + i] = h[i];
-        models[18 * it + 9 + i] = hi[i];
+    for (int e = lane; e < 45; e += 32) {   // entry (p, q), q >= p: rows in the reference's order
+        int p = 0, r = e;
+        while (r >= 9 - p) {
+            r -= 9 - p;
+            ++p;
+        }
+        const int q = p + r;
+        double acc = 0.0;
+        for (int i = 0; i < 4; ++i) {
+            double r1[9], r2[9];
+            dlt_rows(1.0, pts[i], pts[4 + i], pts[8 + i], pts[12 + i], r1, r2);
+            acc += r1[p] * r1[q];
+            acc += r2[p] * r2[q];
+        }
+        a[p * 9 + q] = acc;
+        a[q * 9 + p] = acc;
     }
-    valid[it] = 1;
+    __syncwarp();
+    jacobi9_smallest_warp(a, sv[w], shn[w]);
+    if (lane == 0) {
+        double h[9], hi[9];
+        bool ok = dlt_finish(shn[w], sts[w], std_[w], h);
+        if (ok) {
+            const double det = h_det(h);
+            ok = isfinite(det) && det != 0.0 && h_inverse(h, hi);
+        }
+        if (ok)
+            for (int i = 0; i < 9; ++i) {
+                models[18 * it + i] = h[i];
+                models[18 * it + 9 + i] = hi[i];
+            }
+        valid[it] = ok ? 1 : 0;
+    }
 }
 
 // Binary counter over aligned 2^level blocks (the detsum tree; see dsift_tree.cuh).
@@ -352,166 +403,60 @@ __global__ void __launch_bounds__(kG2Threads) magsac_score_kernel(const double* 
     }
 }
 
-struct G3Shared {
-    double h[9], hi[9], refit[9], refit_inv[9];
+// Weighted normalized DLT of n correspondences (geom.cpp:108-161) by one CTA
+// of kG3Threads: the order-defining sums (centroids, mean distances) are
+// sequential loops of one thread each; everything elementwise is parallel;
+// A^T A entries are owned by 45 threads; the Jacobi sweeps run on warp 0.
+// x1..y2: global scratch holding the raw coordinates (normalized in place);
+// hs, ht: scratch [n].  Returns (to every thread) whether the reference
+// would have returned a model; out = H on success.
+struct DltShared {
+    double ata[81], jv[81], hn[9];
     NormT ts, td;
-    int best;
-    int n_in;
+    double sum[4];
     int ok;
 };
-
-// G3: winner, soft inliers, weighted refit, final mask (geom.cpp:261-319).
-// out: [0] status (1 = success), [1] best iteration, then score (double) and
-// h[9] in out_d.  Scratch (device, 7 n doubles): r2, inlier x1 y1 x2 y2, w.
-__global__ void __launch_bounds__(kG3Threads) magsac_final_kernel(const double* __restrict__ m, long long n, int iters,
-                                                                  const double* __restrict__ models,
-                                                                  const unsigned char* __restrict__ valid,
-                                                                  const double* __restrict__ scores, double tau_sq,
-                                                                  double* __restrict__ scratch,
-                                                                  unsigned char* __restrict__ mask,
-                                                                  int* __restrict__ out_i, double* __restrict__ out_d) {
-    __shared__ G3Shared S;
-    __shared__ double ata[81];
-    __shared__ double jv[81];
-    __shared__ double hn[9];
+__device__ bool dlt_cta(DltShared& S, double* x1, double* y1, double* x2, double* y2, const double* w, int n,
+                        double* hs, double* ht, double* out) {
     const int tid = threadIdx.x;
-    double* r2 = scratch;
-    double* ix1 = scratch + n;
-    double* iy1 = ix1 + n;
-    double* ix2 = iy1 + n;
-    double* iy2 = ix2 + n;
-    double* iw = iy2 + n;
-    if (tid == 0) {
-        int best = -1;
-        for (int it = 0; it < iters; ++it) {
-            if (!valid[it]) continue;
-            if (best < 0 || scores[it] > scores[best]) best = it;
+    if (tid == 0) S.ok = 1;
+    if (tid == 0 || tid == 32) {   // hartley_normalize (geom.cpp:68-94): centroid sums
+        const double* xs = tid == 0 ? x1 : x2;
+        const double* ys = tid == 0 ? y1 : y2;
+        double sx = 0.0, sy = 0.0;
+        for (int i = 0; i < n; ++i) {
+            sx += xs[i];
+            sy += ys[i];
         }
-        S.best = best;
-        S.ok = 0;
-        out_i[0] = 0;
-        out_i[1] = best;
-        out_d[0] = 0.0;
-        if (best >= 0) {
-            for (int i = 0; i < 9; ++i) S.h[i] = models[18 * best + i];
-            // the winner's inverse is recomputed as the reference does (geom.cpp:270-274)
-            S.ok = h_inverse(S.h, S.hi) ? 1 : 0;
-        }
+        NormT& t = tid == 0 ? S.ts : S.td;
+        t.cx = sx / (double)n;
+        t.cy = sy / (double)n;
     }
     __syncthreads();
-    if (!S.ok) {
-        for (long long i = tid; i < n; i += kG3Threads) mask[i] = 0;
-        return;
-    }
-    for (long long i = tid; i < n; i += kG3Threads)
-        r2[i] = sym_err_sq(S.h, S.hi, m[4 * i], m[4 * i + 1], m[4 * i + 2], m[4 * i + 3]);
-    __syncthreads();
-    if (tid == 0) {   // ordered compaction of the soft inliers (geom.cpp:276-283)
-        int k = 0;
-        for (long long i = 0; i < n; ++i)
-            if (r2[i] < tau_sq) {
-                ix1[k] = m[4 * i];
-                iy1[k] = m[4 * i + 1];
-                ix2[k] = m[4 * i + 2];
-                iy2[k] = m[4 * i + 3];
-                iw[k] = 1.0 - r2[i] / tau_sq;
-                ++k;
-            }
-        S.n_in = k;
-        S.ok = k >= 4;
-    }
-    __syncthreads();
-    if (!S.ok) {
-        for (long long i = tid; i < n; i += kG3Threads) mask[i] = 0;
-        return;
-    }
-    const int nin = S.n_in;
-    // Hartley normalization of both sides: sequential sums (threads 0 and 32)
-    if (tid == 0 || tid == 32) {
-        double* xs = tid == 0 ? ix1 : ix2;
-        double* ys = tid == 0 ? iy1 : iy2;
-        NormT t;
-        const bool ok = hartley(xs, ys, nin, t);
-        if (tid == 0) S.ts = t; else S.td = t;
-        if (!ok) atomicAnd(&S.ok, 0);
-    }
-    __syncthreads();
-    if (!S.ok) {
-        for (long long i = tid; i < n; i += kG3Threads) mask[i] = 0;
-        return;
-    }
-    if (nin == 4 && tid == 0) {   // geom.cpp:116-118 (only for a 4-point refit)
-        if (three_collinear(ix1, iy1, 4) || three_collinear(ix2, iy2, 4)) S.ok = 0;
-    }
-    // A^T A: thread e < 45 owns entry (p, q), q >= p, summed over the rows in order
-    if (tid < 45) {
-        int p = 0, e = tid;
-        while (e >= 9 - p) {
-            e -= 9 - p;
-            ++p;
-        }
-        const int q = p + e;
-        double acc = 0.0;
-        for (int i = 0; i < nin; ++i) {
-            double r1[9], rr[9];
-            dlt_rows(iw[i], ix1[i], iy1[i], ix2[i], iy2[i], r1, rr);
-            acc += r1[p] * r1[q];
-            acc += rr[p] * rr[q];
-        }
-        ata[p * 9 + q] = acc;
-        ata[q * 9 + p] = acc;
-    }
-    __syncthreads();
-    if (tid == 0 && S.ok) {
-        jacobi9_smallest(ata, jv, hn);
-        bool ok = dlt_finish(hn, S.ts, S.td, S.refit);
-        if (ok) ok = h_inverse(S.refit, S.refit_inv);
-        S.ok = ok;
-        if (ok) {
-            out_i[0] = 1;
-            out_d[0] = scores[S.best];
-            for (int i = 0; i < 9; ++i) out_d[1 + i] = S.refit[i];
-        }
-    }
-    __syncthreads();
-    for (long long i = tid; i < n; i += kG3Threads) {
-        unsigned char v = 0;
-        if (S.ok) v = sym_err_sq(S.refit, S.refit_inv, m[4 * i], m[4 * i + 1], m[4 * i + 2], m[4 * i + 3]) < tau_sq;
-        mask[i] = v;
-    }
-}
-
-// Standalone weighted DLT (geom.cpp:108-161) for the C ABI: one CTA, the same
-// code path as the refit.  status: 1 ok, 0 degenerate.
-__global__ void __launch_bounds__(kG3Threads) dlt_kernel(const double* __restrict__ m, const double* __restrict__ w,
-                                                         int n, double* __restrict__ scratch, int* __restrict__ status,
-                                                         double* __restrict__ out) {
-    __shared__ double ata[81];
-    __shared__ double jv[81];
-    __shared__ double hn[9];
-    __shared__ NormT ts, td;
-    __shared__ int ok;
-    const int tid = threadIdx.x;
-    double* x1 = scratch;
-    double* y1 = x1 + n;
-    double* x2 = y1 + n;
-    double* y2 = x2 + n;
-    if (tid == 0) ok = 1;
     for (int i = tid; i < n; i += kG3Threads) {
-        x1[i] = m[4 * i];
-        y1[i] = m[4 * i + 1];
-        x2[i] = m[4 * i + 2];
-        y2[i] = m[4 * i + 3];
+        hs[i] = ds_hypot(x1[i] - S.ts.cx, y1[i] - S.ts.cy);
+        ht[i] = ds_hypot(x2[i] - S.td.cx, y2[i] - S.td.cy);
     }
     __syncthreads();
     if (tid == 0 || tid == 32) {
-        NormT t;
-        const bool good = tid == 0 ? hartley(x1, y1, n, t) : hartley(x2, y2, n, t);
-        if (tid == 0) ts = t; else td = t;
-        if (!good) atomicAnd(&ok, 0);
+        const double* hh = tid == 0 ? hs : ht;
+        NormT& t = tid == 0 ? S.ts : S.td;
+        double mean_dist = 0.0;
+        for (int i = 0; i < n; ++i) mean_dist += hh[i];
+        mean_dist /= (double)n;
+        if (mean_dist < 1e-12) atomicAnd(&S.ok, 0);
+        t.scale = ds_sqrt_d(2.0) / mean_dist;
     }
     __syncthreads();
-    if (tid == 0 && ok && n == 4 && (three_collinear(x1, y1, 4) || three_collinear(x2, y2, 4))) ok = 0;
+    if (!S.ok) return false;
+    for (int i = tid; i < n; i += kG3Threads) {
+        x1[i] = (x1[i] - S.ts.cx) * S.ts.scale;
+        y1[i] = (y1[i] - S.ts.cy) * S.ts.scale;
+        x2[i] = (x2[i] - S.td.cx) * S.td.scale;
+        y2[i] = (y2[i] - S.td.cy) * S.td.scale;
+    }
+    __syncthreads();
+    if (tid == 0 && n == 4 && (three_collinear(x1, y1, 4) || three_collinear(x2, y2, 4))) S.ok = 0;
     if (tid < 45) {
         int p = 0, e = tid;
         while (e >= 9 - p) {
@@ -526,25 +471,171 @@ __global__ void __launch_bounds__(kG3Threads) dlt_kernel(const double* __restric
             acc += r1[p] * r1[q];
             acc += rr[p] * rr[q];
         }
-        ata[p * 9 + q] = acc;
-        ata[q * 9 + p] = acc;
+        S.ata[p * 9 + q] = acc;
+        S.ata[q * 9 + p] = acc;
+    }
+    __syncthreads();
+    if (!S.ok) return false;
+    if (tid < 32) {
+        jacobi9_smallest_warp(S.ata, S.jv, S.hn);
+        if (tid == 0) S.ok = dlt_finish(S.hn, S.ts, S.td, out);
+    }
+    __syncthreads();
+    return S.ok != 0;
+}
+
+// G3: winner, soft inliers, weighted refit, final mask (geom.cpp:261-319).
+// out_i: [0] success, [1] best iteration; out_d: [0] score, [1..9] H.
+// scratch (device): r2, x1, y1, x2, y2, w, hs, ht — 8 n doubles.
+__global__ void __launch_bounds__(kG3Threads) magsac_final_kernel(const double* __restrict__ m, long long n, int iters,
+                                                                  const double* __restrict__ models,
+                                                                  const unsigned char* __restrict__ valid,
+                                                                  const double* __restrict__ scores, double tau_sq,
+                                                                  double* __restrict__ scratch,
+                                                                  unsigned char* __restrict__ mask,
+                                                                  int* __restrict__ out_i, double* __restrict__ out_d) {
+    __shared__ DltShared D;
+    __shared__ double h[9], hi[9], refit[9], refit_inv[9];
+    __shared__ double wsc[kG3Threads / 32];
+    __shared__ int wix[kG3Threads / 32], cnt[kG3Threads];
+    __shared__ int best_s, ok_s, nin_s;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    double* r2 = scratch;
+    double* x1 = r2 + n;
+    double* y1 = x1 + n;
+    double* x2 = y1 + n;
+    double* y2 = x2 + n;
+    double* wt = y2 + n;
+    double* hs = wt + n;
+    double* ht = hs + n;
+    // winner: highest score, lowest iteration on ties (geom.cpp:263-268)
+    double bs = 0.0;
+    int bi = -1;
+    for (int it = tid; it < iters; it += kG3Threads)
+        if (valid[it] && (bi < 0 || scores[it] > bs)) {
+            bs = scores[it];
+            bi = it;
+        }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double os = __shfl_down_sync(0xffffffffu, bs, o);
+        const int oi = __shfl_down_sync(0xffffffffu, bi, o);
+        if (oi >= 0 && (bi < 0 || os > bs || (os == bs && oi < bi))) {
+            bs = os;
+            bi = oi;
+        }
+    }
+    if (lane == 0) {
+        wsc[warp] = bs;
+        wix[warp] = bi;
     }
     __syncthreads();
     if (tid == 0) {
-        int good = ok;
-        if (good) {
-            jacobi9_smallest(ata, jv, hn);
-            good = dlt_finish(hn, ts, td, out);
+        int best = -1;
+        double b = 0.0;
+        for (int k = 0; k < kG3Threads / 32; ++k)
+            if (wix[k] >= 0 && (best < 0 || wsc[k] > b || (wsc[k] == b && wix[k] < best))) {
+                b = wsc[k];
+                best = wix[k];
+            }
+        best_s = best;
+        out_i[0] = 0;
+        out_i[1] = best;
+        out_d[0] = 0.0;
+        int ok = 0;
+        if (best >= 0) {
+            for (int i = 0; i < 9; ++i) h[i] = models[18 * best + i];
+            ok = h_inverse(h, hi) ? 1 : 0;   // the winner's inverse, as the reference recomputes it
         }
-        *status = good;
+        ok_s = ok;
     }
+    __syncthreads();
+    if (!ok_s) {
+        for (long long i = tid; i < n; i += kG3Threads) mask[i] = 0;
+        return;
+    }
+    // soft inliers in index order (geom.cpp:276-283): per-thread contiguous chunks
+    const long long chunk = (n + kG3Threads - 1) / kG3Threads;
+    const long long c0 = tid * chunk, c1 = min(n, c0 + chunk);
+    int c = 0;
+    for (long long i = c0; i < c1; ++i) {
+        const double e = sym_err_sq(h, hi, m[4 * i], m[4 * i + 1], m[4 * i + 2], m[4 * i + 3]);
+        r2[i] = e;
+        c += e < tau_sq;
+    }
+    cnt[tid] = c;
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int k = 0; k < kG3Threads; ++k) {
+            const int v = cnt[k];
+            cnt[k] = acc;
+            acc += v;
+        }
+        nin_s = acc;
+    }
+    __syncthreads();
+    {
+        int k = cnt[tid];
+        for (long long i = c0; i < c1; ++i)
+            if (r2[i] < tau_sq) {
+                x1[k] = m[4 * i];
+                y1[k] = m[4 * i + 1];
+                x2[k] = m[4 * i + 2];
+                y2[k] = m[4 * i + 3];
+                wt[k] = 1.0 - r2[i] / tau_sq;
+                ++k;
+            }
+    }
+    __syncthreads();
+    const int nin = nin_s;
+    bool ok = nin >= 4 && dlt_cta(D, x1, y1, x2, y2, wt, nin, hs, ht, refit);
+    if (ok) {
+        if (tid == 0) {
+            ok_s = h_inverse(refit, refit_inv) ? 1 : 0;
+            if (ok_s) {
+                out_i[0] = 1;
+                out_d[0] = scores[best_s];
+                for (int i = 0; i < 9; ++i) out_d[1 + i] = refit[i];
+            }
+        }
+        __syncthreads();
+        ok = ok_s != 0;
+    }
+    for (long long i = tid; i < n; i += kG3Threads) {
+        unsigned char v = 0;
+        if (ok) v = sym_err_sq(refit, refit_inv, m[4 * i], m[4 * i + 1], m[4 * i + 2], m[4 * i + 3]) < tau_sq;
+        mask[i] = v;
+    }
+}
+
+// Standalone weighted DLT (geom.cpp:108-161) for the C ABI: one CTA, the
+// refit's code path.  status: 1 ok, 0 where the reference throws.
+// scratch: x1, y1, x2, y2, hs, ht — 6 n doubles.
+__global__ void __launch_bounds__(kG3Threads) dlt_kernel(const double* __restrict__ m, const double* __restrict__ w,
+                                                         int n, double* __restrict__ scratch, int* __restrict__ status,
+                                                         double* __restrict__ out) {
+    __shared__ DltShared D;
+    double* x1 = scratch;
+    double* y1 = x1 + n;
+    double* x2 = y1 + n;
+    double* y2 = x2 + n;
+    for (int i = threadIdx.x; i < n; i += kG3Threads) {
+        x1[i] = m[4 * i];
+        y1[i] = m[4 * i + 1];
+        x2[i] = m[4 * i + 2];
+        y2[i] = m[4 * i + 3];
+    }
+    __syncthreads();
+    const bool ok = dlt_cta(D, x1, y1, x2, y2, w, n, y2 + n, y2 + 2 * (long long)n, out);
+    if (threadIdx.x == 0) *status = ok ? 1 : 0;
 }
 
 }  // namespace
 
 size_t magsac_scratch_bytes(long long n, int iters) {
     return sizeof(double) * 18 * (size_t)iters + (size_t)iters + 256 + sizeof(double) * (size_t)iters +
-           sizeof(double) * (size_t)iters * (size_t)((n >> 5) + 1) + sizeof(double) * 7 * (size_t)n + 1024;
+           sizeof(double) * (size_t)iters * (size_t)((n >> 5) + 1) + sizeof(double) * 8 * (size_t)n + 2048;
 }
 
 cudaError_t launch_magsac(const double* m, long long n, const int4* samples, int iters, double tau_sq, void* scratch,
@@ -559,15 +650,15 @@ cudaError_t launch_magsac(const double* m, long long n, const int4* samples, int
     unsigned char* valid = reinterpret_cast<unsigned char*>(take((size_t)iters));
     double* scores = reinterpret_cast<double*>(take(sizeof(double) * (size_t)iters));
     double* bsums = reinterpret_cast<double*>(take(sizeof(double) * (size_t)iters * (size_t)((n >> 5) + 1)));
-    double* fscr = reinterpret_cast<double*>(take(sizeof(double) * 6 * (size_t)n));
-    magsac_hyp_kernel<<<(iters + 63) / 64, 64, 0, st>>>(m, samples, iters, models, valid);
+    double* fscr = reinterpret_cast<double*>(take(sizeof(double) * 8 * (size_t)n));
+    magsac_hyp_kernel<<<(iters + kG1Warps - 1) / kG1Warps, 32 * kG1Warps, 0, st>>>(m, samples, iters, models, valid);
     magsac_score_kernel<<<iters, kG2Threads, 0, st>>>(m, n, models, valid, tau_sq, scores, bsums);
     magsac_final_kernel<<<1, kG3Threads, 0, st>>>(m, n, iters, models, valid, scores, tau_sq, fscr, mask, out_i,
                                                   out_d);
     return cudaGetLastError();
 }
 
-size_t dlt_scratch_bytes(long long n) { return sizeof(double) * 4 * (size_t)n + 256; }
+size_t dlt_scratch_bytes(long long n) { return sizeof(double) * 6 * (size_t)n + 256; }
 
 cudaError_t launch_dlt(const double* m, const double* w, int n, void* scratch, int* status, double* out,
                        cudaStream_t st) {
