@@ -11,6 +11,8 @@
 // std::invalid_argument for DSIFT_EINVAL, std::runtime_error otherwise.
 #pragma once
 
+#include <algorithm>
+#include <array>
 #include <cstdint>
 #include <memory>
 #include <span>
@@ -84,6 +86,22 @@ struct FeatureSet {   // core.hpp:66-78
     std::span<const float> row(size_t i) const { return {descriptors.data() + i * dim, size_t(dim)}; }
 };
 
+// detsift::Homography / Correspondence / MagsacResult (geom.hpp:14-61),
+// layout-compatible with the C ABI's double arrays.
+struct Homography {
+    std::array<double, 9> h = {1, 0, 0, 0, 1, 0, 0, 0, 1};
+};
+struct Correspondence {
+    double x1 = 0, y1 = 0, x2 = 0, y2 = 0;
+};
+struct MagsacResult {
+    bool success = false;
+    Homography h;
+    std::vector<uint8_t> inlier_mask;
+    double score = 0.0;
+    int best_iteration = -1;
+};
+
 [[noreturn]] inline void throw_status(int rc) {
     const std::string msg = dsift_last_error();
     if (rc == DSIFT_EINVAL) throw std::invalid_argument(msg);
@@ -92,6 +110,13 @@ struct FeatureSet {   // core.hpp:66-78
 }
 inline void check(int rc) {
     if (rc != DSIFT_OK) throw_status(rc);
+}
+
+// detsift::corner_error (geom.cpp:322-333).
+inline double corner_error(const Homography& est, const Homography& gt, double width, double height) {
+    double out = 0.0;
+    check(dsift_corner_error(est.h.data(), gt.h.data(), width, height, &out));
+    return out;
 }
 
 inline void SiftConfig::validate() const {
@@ -149,6 +174,31 @@ class Extractor {
         char hex[65];
         check(dsift_result_sha256(ctx_.get(), image, hex));
         return hex;
+    }
+    // detsift::magsac_lite (geom.cpp:181-320) on the device, bit-identical.
+    MagsacResult magsac_lite(std::span<const Correspondence> matches, int iterations, double tau, uint64_t seed) {
+        dsift_magsac_result r{};
+        MagsacResult out;
+        out.inlier_mask.assign(matches.size(), 0);
+        check(dsift_magsac_lite(ctx_.get(), reinterpret_cast<const double*>(matches.data()),
+                                static_cast<int64_t>(matches.size()), iterations, tau, seed, &r,
+                                out.inlier_mask.data()));
+        out.success = r.success != 0;
+        std::copy(r.h, r.h + 9, out.h.h.begin());
+        out.score = r.score;
+        out.best_iteration = r.best_iteration;
+        if (!out.success) out.inlier_mask.clear();
+        return out;
+    }
+    // detsift::dlt_homography (geom.cpp:108-161) on the device.
+    Homography dlt_homography(std::span<const Correspondence> pairs, std::span<const double> weights = {}) {
+        if (!weights.empty() && weights.size() != pairs.size())
+            throw std::invalid_argument("dlt: weight count mismatch");
+        Homography h;
+        check(dsift_dlt_homography(ctx_.get(), reinterpret_cast<const double*>(pairs.data()),
+                                   static_cast<int64_t>(pairs.size()), weights.empty() ? nullptr : weights.data(),
+                                   h.h.data()));
+        return h;
     }
     dsift_ctx* handle() { return ctx_.get(); }
 

@@ -32,6 +32,19 @@ int main(int argc, char** argv) {
         } catch (const std::invalid_argument& e) {
             std::cout << "invalid_argument: " << e.what() << "\n";
         }
+        // geometry face: exact correspondences of a translation, then corner error
+        std::vector<dsift::Correspondence> pairs;
+        for (int i = 0; i < 30; ++i) {
+            const double x = 17.0 * (i % 6) + 3.0 * i, y = 11.0 * (i / 6) + 0.5 * i * i;
+            pairs.push_back({x, y, x + 5.5, y - 2.25});
+        }
+        const dsift::MagsacResult r = ex.magsac_lite(pairs, 100, 3.0, 7);
+        size_t inl = 0;
+        for (uint8_t v : r.inlier_mask) inl += v;
+        dsift::Homography t;
+        t.h = {1, 0, 5.5, 0, 1, -2.25, 0, 0, 1};
+        std::cout << "magsac " << r.success << " " << inl << " " << (dsift::corner_error(r.h, t, 640, 480) < 1e-6)
+                  << "\n";
     } catch (const std::exception& e) {
         std::cerr << "error: " << e.what() << "\n";
         return 1;

@@ -235,6 +235,7 @@ def test_cpp_wrapper(golden, port):
     n, sha = lines[0].split()
     assert int(n) == case["n_keypoints"] and sha == case["sha256"]
     assert lines[1].startswith("invalid_argument: build_scale_space: image smaller than 8x8")
+    assert lines[2] == "magsac 1 30 1"
 
 
 def test_c2_pair_photometric(ref):
