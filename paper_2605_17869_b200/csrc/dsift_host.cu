@@ -21,6 +21,7 @@
 
 #include "dlpack_min.h"
 #include "dsift_common.cuh"
+#include "dsift_tma.cuh"
 #include "dsift_kernels.cuh"
 
 namespace dsift {
@@ -215,6 +216,7 @@ struct dsift_ctx {
     int batch = 0;            // images in the current pyramid / result
     PyramidDesc pyr{};
     DevBuf det_aux, input_u8, ori_aux, match_in, match_scratch, match_best, geom_in, geom_scratch, geom_out;
+    DevBuf tma_maps;
     DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
         pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow,
         ref_states, keep;
@@ -366,12 +368,62 @@ static unsigned detect_tiles(const PyramidDesc& d, int* base, int* per_image) {
     return (unsigned)acc * (unsigned)d.batch;
 }
 
+bool tma_encode_3d_f32(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
+                       uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2) {
+    using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                            const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                            CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Fn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<Fn>(p);
+    }
+    if (!fn) return false;
+    const cuuint64_t dims[3] = {d0, d1, d2};
+    const cuuint64_t strides[2] = {s1 * sizeof(float), s2 * sizeof(float)};
+    const cuuint32_t box[3] = {b0, b1, b2};
+    const cuuint32_t es[3] = {1, 1, 1};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// K2's TMA maps: per octave, the DoG stack {w, h, batch * (s+2)}, box
+// {36, 34, s+2} (detect tile + halo, all DoG levels of one image).
+static unsigned build_dog_maps(dsift_ctx* c, const PyramidDesc& d) {
+    if (std::getenv("DSIFT_NO_TMA")) return 0u;
+    std::vector<CUtensorMap> maps((size_t)std::max(1, d.n_oct));
+    unsigned mask = 0;
+    for (int o = 0; o < d.n_oct && o < 32; ++o) {
+        const OctaveDesc& od = d.oct[o];
+        if (od.tiles_x == 0) continue;
+        if (tma_encode_3d_f32(&maps[(size_t)o], od.dog, (uint64_t)od.w, (uint64_t)od.h,
+                              (uint64_t)d.batch * (uint64_t)(d.s + 2), (uint64_t)od.pitch,
+                              (uint64_t)od.level_stride, 36u, 34u, (uint32_t)(d.s + 2)))
+            mask |= 1u << o;
+    }
+    if (mask) {
+        c->tma_maps.ensure(sizeof(CUtensorMap) * maps.size());
+        cuda_check(cudaMemcpyAsync(c->tma_maps.as<void>(), maps.data(), sizeof(CUtensorMap) * maps.size(),
+                                   cudaMemcpyHostToDevice, c->stream),
+                   "H2D tensor maps");
+    }
+    return mask;
+}
+
 static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
     const dsift_config& cf = c->cfg.c;
     DetectArgs a{};
     a.pyr = c->pyr;
     a.n_tiles = detect_tiles(c->pyr, a.oct_tile_base, &a.tiles_per_image);
     a.pre_gate = 0.5f * cf.contrast_threshold / cf.intervals;
+    a.tma_mask = build_dog_maps(c, a.pyr);
+    a.dog_maps = c->tma_maps.as<void>();
     a.contrast_gate = double(cf.contrast_threshold) / cf.intervals;
     a.edge_r = cf.edge_ratio;
     a.max_iters = cf.max_refine_iters;

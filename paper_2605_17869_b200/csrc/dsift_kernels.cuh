@@ -45,6 +45,10 @@ struct DetectArgs {
     unsigned* tile_offsets;      // [n_tiles] exclusive scan of tile_counts
     void* scan_temp;
     size_t scan_temp_bytes;
+    // TMA: per-octave 3-D maps of the DoG stack {w, h, batch * (s+2)} (device
+    // memory, CUtensorMap each); octave o is staged by TMA iff bit o is set
+    const void* dog_maps;
+    unsigned tma_mask;
 };
 size_t detect_scan_temp_bytes(unsigned n_tiles);
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st);

@@ -16,6 +16,7 @@
 #include "dsift_common.cuh"
 #include "dsift_kernels.cuh"
 #include "dsift_scan.cuh"
+#include "dsift_tma.cuh"
 
 namespace dsift {
 
@@ -94,7 +95,9 @@ __device__ bool refine_candidate(const DetectArgs& a, int b, int o, int x, int y
 // mask and the tile publishes its count.  No tile ever waits on another.
 __global__ void __launch_bounds__(kDetThreads, 4)
 detect_count_kernel(const __grid_constant__ DetectArgs a) {
-    extern __shared__ __align__(16) float lv_s[];   // [s+2][34][kDetPitch]
+    extern __shared__ __align__(128) float lv_raw[];
+    // [s+2][34][kDetPitch], 128-byte aligned (TMA destination)
+    float* lv_s = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(lv_raw) + 127) & ~uintptr_t(127));
     __shared__ int warp_tot[kDetThreads / 32];
     const unsigned t = blockIdx.x;
     const int b = (int)(t / a.tiles_per_image);
@@ -109,26 +112,40 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
     const int nlev = s + 2;
     const int lane = threadIdx.x & 31;
 
-    // stage s+2 DoG levels (+1 halo) with asynchronous 4-byte copies: every
-    // load is in flight at once (a load->store chain per row serialises on
-    // memory latency); out-of-image positions are zero-filled
-    const float* __restrict__ dogb = od.dog + (long long)b * a.pyr.dog_img_stride(o);
-    // a staged row = 32 aligned floats (8 x 16 B, xs - 1 = 32k) + 2 halo floats
-    for (int idx = threadIdx.x; idx < nlev * kDetHalo * 10; idx += kDetThreads) {
-        const int r = idx / 10, q = idx - r * 10;
-        const int l = r / kDetHalo, yy = ys - 1 + (r - l * kDetHalo);
-        const int xx = xs - 1 + (q < 8 ? 4 * q : 24 + q);   // q = 8, 9 -> columns 32, 33
-        const int cols = q < 8 ? 4 : 1;
-        const int nin = yy < h ? max(0, min(cols, w - xx)) : 0;
-        const float* g = dogb + (nin ? (long long)l * od.level_stride + (long long)yy * od.pitch + xx : 0);
-        const unsigned sa = (unsigned)__cvta_generic_to_shared(lv_s + r * kDetPitch + (xx - (xs - 1)));
-        if (q < 8)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(4 * nin));
-        else
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"(4 * nin));
+    if ((a.tma_mask >> o) & 1u) {
+        // one TMA box {36, 34, s+2} of the DoG stack: 34 rows (tile + halo) x
+        // 36 columns from xs - 1 of each level; out-of-image elements arrive
+        // as zeros, exactly like the copy path below
+        __shared__ __align__(8) uint64_t bar;
+        if (threadIdx.x == 0) {
+            mbar_init(&bar, 1);
+            mbar_arrive_expect_tx(&bar, (unsigned)(sizeof(float) * kDetPitch * kDetHalo * nlev));
+            tma_load_3d(lv_s, static_cast<const CUtensorMap*>(a.dog_maps) + o, xs - 1, ys - 1, b * nlev, &bar);
+        }
+        __syncthreads();
+        mbar_wait(&bar, 0);
+    } else {
+        // stage s+2 DoG levels (+1 halo) with asynchronous 4-byte copies: every
+        // load is in flight at once (a load->store chain per row serialises on
+        // memory latency); out-of-image positions are zero-filled
+        const float* __restrict__ dogb = od.dog + (long long)b * a.pyr.dog_img_stride(o);
+        // a staged row = 32 aligned floats (8 x 16 B, xs - 1 = 32k) + 2 halo floats
+        for (int idx = threadIdx.x; idx < nlev * kDetHalo * 10; idx += kDetThreads) {
+            const int r = idx / 10, q = idx - r * 10;
+            const int l = r / kDetHalo, yy = ys - 1 + (r - l * kDetHalo);
+            const int xx = xs - 1 + (q < 8 ? 4 * q : 24 + q);   // q = 8, 9 -> columns 32, 33
+            const int cols = q < 8 ? 4 : 1;
+            const int nin = yy < h ? max(0, min(cols, w - xx)) : 0;
+            const float* g = dogb + (nin ? (long long)l * od.level_stride + (long long)yy * od.pitch + xx : 0);
+            const unsigned sa = (unsigned)__cvta_generic_to_shared(lv_s + r * kDetPitch + (xx - (xs - 1)));
+            if (q < 8)
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(4 * nin));
+            else
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"(4 * nin));
+        }
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
     }
-    asm volatile("cp.async.wait_all;\n" ::);
-    __syncthreads();
 
     // strictly_extremal (detect.cpp:11-28), branch-free: thread (lane, g) owns
     // column lane and the 4 rows 4g..4g+3 of the tile.  Per level it keeps the
@@ -321,7 +338,7 @@ size_t detect_scan_temp_bytes(unsigned n_tiles) {
 
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st) {
     if (a.n_tiles == 0) return cudaSuccess;
-    const size_t smem = sizeof(float) * (size_t)(a.pyr.s + 2) * kDetHalo * kDetPitch;
+    const size_t smem = sizeof(float) * (size_t)(a.pyr.s + 2) * kDetHalo * kDetPitch + 128;
     cudaError_t e = cudaFuncSetAttribute(detect_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     detect_count_kernel<<<a.n_tiles, kDetThreads, smem, st>>>(a);
