@@ -310,55 +310,73 @@ def run_ours(args, rank, local_rank, world):
         lib = ds.load_library()
         ex.set_profiling(False)
 
-        def e2e_step():
-            ex.submit(host_np)
-            total = ex.sync()
+        # Two contexts (two CUDA streams) in ping-pong, as a serving loop would
+        # run them: every step still copies its batch host->device, extracts and
+        # copies the result back into pinned host memory (all inside the timed
+        # region); batch k's copies overlap batch k+1's extraction.
+        ex2 = ds.Extractor(ds.SiftConfig(), local_rank)
+        ex2.set_profiling(False)
+        ctxs = [ex, ex2]
+        outs = [(out_k, out_d, offs),
+                (torch.empty((cap * 28,), dtype=torch.uint8, pin_memory=True).numpy(),
+                 torch.empty((cap * 512,), dtype=torch.uint8, pin_memory=True).numpy(), np.zeros(B + 1, np.int64))]
+
+        def finish(i):
+            e = ctxs[i]
+            total = e.sync()
             assert total <= cap
-            ds._check(lib, lib.dsift_result_copy(ex.ctx, out_k.ctypes.data, out_d.ctypes.data, None,
-                                                 offs.ctypes.data))
+            ok, od, oo = outs[i]
+            ds._check(lib, lib.dsift_result_copy(e.ctx, ok.ctypes.data, od.ctypes.data, None, oo.ctypes.data))
             return total
 
-        e2e_step()
-        nsteps = args.e2e_steps or args.steps
+        def run_pipelined(submit, nsteps):
+            pending, d2h = [], 0
+            for k in range(nsteps):
+                i = k % 2
+                if len(pending) == 2:
+                    d2h += finish(pending.pop(0)) * (28 + 512) + 8 * (B + 1)
+                submit(ctxs[i])
+                pending.append(i)
+            while pending:
+                d2h += finish(pending.pop(0)) * (28 + 512) + 8 * (B + 1)
+            return d2h
+
+        def sub_f32(e):
+            e.submit(host_np)
+
+        nsteps = max(2, args.e2e_steps or args.steps)
+        run_pipelined(sub_f32, 2)   # warm-up (both contexts)
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        d2h = 0
-        for _ in range(nsteps):
-            d2h += e2e_step() * (28 + 512) + 8 * (B + 1)
+        d2h = run_pipelined(sub_f32, nsteps)
         torch.cuda.synchronize()
         et = time.perf_counter() - t0
         barrier()
         et_max = max_over_ranks(et)
         e2e = {"value": B * world * nsteps / et_max, "unit": "images/s",
                "h2d_bytes_per_step": B * W * H * 4, "d2h_bytes_per_step": int(d2h / nsteps),
-               "mpx_per_s": B * world * nsteps * W * H / 1e6 / et_max}
+               "mpx_per_s": B * world * nsteps * W * H / 1e6 / et_max,
+               "pipeline": "2 contexts ping-pong (H2D + extract + D2H per step, copies overlap the other batch)"}
         # the same, fed as 8-bit images (load_image's payload): the
         # synthetic images quantised to uint8, converted on the device
         host_u8 = torch.empty((B, H, W), dtype=torch.uint8, pin_memory=True)
         host_u8.copy_(torch.clamp(torch.round(imgs * 255.0), 0, 255).to(torch.uint8).cpu())
         u8_np = host_u8.numpy()
 
-        def e2e_u8_step():
-            _check = ds._check
-            _check(lib, lib.dsift_extract_batch_u8(ex.ctx, u8_np.ctypes.data, B, W, H, 1, 0))
-            total = ex.sync()
-            assert total <= cap
-            _check(lib, lib.dsift_result_copy(ex.ctx, out_k.ctypes.data, out_d.ctypes.data, None,
-                                              offs.ctypes.data))
-            return total
+        def sub_u8(e):
+            ds._check(lib, lib.dsift_extract_batch_u8(e.ctx, u8_np.ctypes.data, B, W, H, 1, 0))
 
-        e2e_u8_step()
+        run_pipelined(sub_u8, 2)
         barrier()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        d2h8 = 0
-        for _ in range(nsteps):
-            d2h8 += e2e_u8_step() * (28 + 512) + 8 * (B + 1)
+        d2h8 = run_pipelined(sub_u8, nsteps)
         torch.cuda.synchronize()
         et8 = max_over_ranks(time.perf_counter() - t0)
         e2e["u8_ingest"] = {"value": B * world * nsteps / et8, "unit": "images/s",
                             "h2d_bytes_per_step": B * W * H, "d2h_bytes_per_step": int(d2h8 / nsteps)}
+        ex2.close()
 
     # ---- roofline (per-stage, CUDA events inside the timed region) ------------------------
     k1, k2, px = stage_bytes(W, H)
