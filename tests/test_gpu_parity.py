@@ -301,6 +301,22 @@ def test_c3_full_size_properties_and_sampled_parity(port):
         assert bits(port.dsp_descriptor(ss, k[i])).tobytes() == bits(fs.descriptors[i]).tobytes(), i
 
 
+def test_c3_full_size_sha_matches_reference(ref):
+    # the whole C3 output (1600x1200, ~14k keypoints with descriptors) against
+    # the unmodified reference run on the host: the DSF1 SHA-256 and every
+    # keypoint / descriptor bit
+    w, h = 1600, 1200
+    img = ref.value_noise(w, h, 0x5EED0000, 5, 80)
+    kps, desc = ref.extract(img, workers=os.cpu_count() or 1)
+    with ds.Extractor() as ex:
+        fs = ex.extract(img)
+        sha = ex.sha256(0)
+    assert len(fs) == len(kps)
+    assert fs.keypoints.tobytes() == np.ascontiguousarray(kps).tobytes()
+    assert bits(fs.descriptors).tobytes() == bits(desc).tobytes()
+    assert sha == ref.hash_features(kps, desc)
+
+
 # ---- verify-determinism (detsift.cpp:170-200) ------------------------------
 def test_verify_determinism(port, tmp_path):
     from paper_2605_17869_b200 import verify
