@@ -93,6 +93,9 @@ __device__ bool refine_candidate(const DetectArgs& a, int b, int o, int x, int y
 // K2a: one CTA per (image, octave, 32x32 tile) in a fixed tile order; every
 // thread records which of its (level, row) positions are extrema as a 12-bit
 // mask and the tile publishes its count.  No tile ever waits on another.
+// kS > 0: intervals known at compile time (the level loop unrolls and the
+// sliding window lives in renamed registers); kS = 0: any s.
+template <int kS>
 __global__ void __launch_bounds__(kDetThreads, 4)
 detect_count_kernel(const __grid_constant__ DetectArgs a) {
     extern __shared__ __align__(128) float lv_raw[];
@@ -108,7 +111,7 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
     const int tile = rr - a.oct_tile_base[o];
     const int xs = 1 + (tile % od.tiles_x) * kDetTile;
     const int ys = 1 + (tile / od.tiles_x) * kDetTile;
-    const int s = a.pyr.s, w = od.w, h = od.h;
+    const int s = kS > 0 ? kS : a.pyr.s, w = od.w, h = od.h;
     const int nlev = s + 2;
     const int lane = threadIdx.x & 31;
 
@@ -174,6 +177,7 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
     load_level(0, hx[0], hn[0], false);
     load_level(1, hx[1], hn[1], true);
     const int x = xs + lx;
+#pragma unroll (kS > 0 ? kS : 1)
     for (int i = 1; i <= s; ++i) {
         load_level(i + 1, hx[2], hn[2], false);
 #pragma unroll
@@ -339,9 +343,10 @@ size_t detect_scan_temp_bytes(unsigned n_tiles) {
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st) {
     if (a.n_tiles == 0) return cudaSuccess;
     const size_t smem = sizeof(float) * (size_t)(a.pyr.s + 2) * kDetHalo * kDetPitch + 128;
-    cudaError_t e = cudaFuncSetAttribute(detect_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    void (*fn)(DetectArgs) = a.pyr.s == 3 ? detect_count_kernel<3> : detect_count_kernel<0>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    detect_count_kernel<<<a.n_tiles, kDetThreads, smem, st>>>(a);
+    fn<<<a.n_tiles, kDetThreads, smem, st>>>(a);
     size_t tb = a.scan_temp_bytes;
     e = cub::DeviceScan::ExclusiveSum(a.scan_temp, tb, a.tile_counts, a.tile_offsets, (int)a.n_tiles, st);
     if (e != cudaSuccess) return e;
