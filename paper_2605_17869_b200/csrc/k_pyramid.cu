@@ -363,12 +363,14 @@ __device__ __forceinline__ void b2_vpass(const BlurArgs& a, const float* sm, int
             }
         }
         if (x < w) {
+            const int yb = y0 + rg * kB2Seg;
+            const long long ob = (long long)yb * pitch + x;
 #pragma unroll
             for (int j = 0; j < kB2Seg; ++j) {
-                const int y = y0 + rg * kB2Seg + j;
+                const int y = yb + j;
                 if (y < h) {
                     const float g = (float)acc[j];
-                    const long long off = (long long)y * pitch + x;
+                    const long long off = ob + j * pitch;
                     dst[off] = g;
                     // DoG[i-1] = G[i] - G[i-1] (scalespace.cpp:209); G[i-1] was just read (L2)
                     if (MODE == kModeLevel) {
