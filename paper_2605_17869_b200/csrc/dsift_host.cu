@@ -199,7 +199,7 @@ struct Counters {          // one small device block, cleared per batch
     unsigned n_fixed;     // (keypoint, scale) pairs the stream kernel recomputed exactly in place
     unsigned long long n_kp;   // refined keypoints (compacted)
     unsigned emit_ticket;      // orientation fan-out tiles
-    unsigned pad3;
+    unsigned desc_ticket;      // describe: dynamic keypoint claims
 };
 
 }  // namespace dsift
@@ -597,6 +597,7 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
     a.slow_out = c->slow.as<int>();
     a.slow_count = &ctr->n_slow;
     a.fix_count = &ctr->n_fixed;
+    a.ticket = &ctr->desc_ticket;
     a.slow_cap = cap_n;
     a.force_slow = c->force_exact;
     DescArgs af = a;
@@ -626,6 +627,7 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
         const int per_sm = std::max(1, describe_stream_blocks_per_sm(smem_s));
         int grid = c->sm_count * per_sm;
         if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
+        cuda_check(cudaMemsetAsync(af.ticket, 0, sizeof(unsigned), c->stream), "memset ticket");
         cuda_check(launch_describe_stream(af, grid, c->stream), "describe stream");
     }
     DescArgs b = a;

@@ -94,6 +94,7 @@ struct DescArgs {
     int* slow_out;         // fast kernel: keypoints it could not certify
     unsigned* slow_count;
     unsigned* fix_count;   // stream kernel: (keypoint, scale) pairs recomputed exactly in place
+    unsigned* ticket;      // stream kernel: next keypoint to claim (zeroed before the launch)
     long long slow_cap;
     int force_slow;        // test hook: fail every certificate
     int hot_pair;          // fast path: cache the (o0, o0+1) accumulators in registers

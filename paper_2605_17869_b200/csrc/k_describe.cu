@@ -1221,7 +1221,17 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
     const int tid = threadIdx.x;
     int call = 0;
-    for (long long k = blockIdx.x; k < (a.force_slow == -2 ? (blockIdx.x == 0 ? 1 : 0) : n); k += gridDim.x) {
+    // keypoints are claimed one at a time from a global ticket: a keypoint
+    // costs up to ~16x another (its DSP lattices scale with sigma^2), so a
+    // static stride would leave the slowest CTA ~10% behind the mean
+    __shared__ unsigned s_k;
+    const bool diag = a.force_slow == -2;   // diagnostic dump: block 0, keypoint 0 only
+    for (int it = 0;; ++it) {
+        __syncthreads();                   // everyone is done with the previous s_k
+        if (tid == 0) s_k = diag ? (blockIdx.x == 0 && it == 0 ? 0u : 0xffffffffu) : atomicAdd(a.ticket, 1u);
+        __syncthreads();
+        const long long k = (long long)s_k;
+        if (k >= n) break;
         const DevKeypoint kp = a.kps[k];
         const double2 cs = a.trig[k];
         bool all_ok = true;
