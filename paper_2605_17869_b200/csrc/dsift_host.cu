@@ -533,6 +533,7 @@ static void run_orient(dsift_ctx* c, const DevKeypoint* kps, long long n_host, l
     a.emit_scan.ticket = &ctr->emit_ticket;
     a.emit_scan.total = &ctr->n_ori;
     a.emit_scan.cap = (unsigned long long)cap_out;
+    cuda_check(cudaMemsetAsync(a.scan.ticket, 0, sizeof(unsigned), c->stream), "memset ticket");
     cuda_check(launch_orient(a, c->stream), "orient");
     c->launches += 2;
 }

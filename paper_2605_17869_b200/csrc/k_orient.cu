@@ -67,22 +67,16 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
     // peaks go straight to global: angles[k][bins], counts[k] (K4b emits them)
     float* ang = a.angles;
     int* ncopy = a.counts;
-    __shared__ unsigned ticket_s;
-
     const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
-    const unsigned n_tiles = (unsigned)((n + kOriTile - 1) / kOriTile);
-    // persistent: CTAs take ticket-ordered tiles until the device-side count
-    // is covered (no empty tiles, no capacity-sized grid)
+    // persistent: each warp claims keypoints one at a time from a global
+    // ticket (a keypoint's window area scales with sigma^2, so fixed groups
+    // would leave warps waiting for the slowest one)
     for (;;) {
-    const unsigned t = scan_ticket(a.scan, &ticket_s);
-    if (t >= n_tiles) break;
-    const long long k0 = (long long)t * kOriTile;
-
-    for (int j = 0; j < kOriPerWarp; ++j) {
-        const int slot = warp * kOriPerWarp + j;
-        const long long k = k0 + slot;
-        const DevKeypoint kp = a.kps[min(k, n - 1 >= 0 ? n - 1 : 0)];
-        if (k >= n) continue;
+        unsigned kt = 0;
+        if (lane == 0) kt = atomicAdd(a.scan.ticket, 1u);
+        const long long k = (long long)__shfl_sync(0xffffffffu, kt, 0);
+        if (k >= n) break;
+        const DevKeypoint kp = a.kps[k];
         if (kp.octave < 0) {   // a rejected candidate slot
             if (lane == 0) ncopy[k] = 0;
             continue;
@@ -273,8 +267,6 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
         }
         if (lane == 0) ncopy[k] = total;
         __syncwarp();
-    }
-    __syncthreads();   // the ticket slot is reused by the next tile
     }
 }
 
