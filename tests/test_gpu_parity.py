@@ -268,6 +268,52 @@ def test_c2_pair_photometric(ref):
         assert ex.sha256(0) == ref.hash_features(k, d)
 
 
+def test_c2_full_size_pairs(ref):
+    # C2 at its BASELINE size (1000x750): value-noise images A_i and their
+    # photometric twins B_i with the fixture constants cycled (synth.cpp:121-128,
+    # 158-160), extracted as one GPU batch; every image's DSF1 SHA-256 equals
+    # the reference's (or both raise the same error)
+    from oracle.oracle import OracleError
+    w, h = 1000, 750
+    consts = [(0.75, 1.15, -0.04), (0.9, 0.85, 0.05), (1.1, 1.05, -0.02), (1.3, 0.9, 0.03), (1.5, 0.8, 0.08)]
+    imgs = []
+    for i in range(3):
+        a = ref.value_noise(w, h, 0x5EED0000 + i, 5, max(8, w // 20))
+        g, gain, bias = consts[i % len(consts)]
+        b = np.empty_like(a)
+        ref.lib.oref_photometric(a.ctypes.data, w, h, g, gain, bias, b.ctypes.data)
+        imgs += [a, b]
+    ok = [i for i, im in enumerate(imgs) if np.isfinite(im).all()]
+    batch = np.stack([imgs[i] for i in ok])
+    with ds.Extractor() as ex:
+        ex.extract_batch(batch)
+        shas = [ex.sha256(j) for j in range(len(ok))]
+    for j, i in enumerate(ok):
+        try:
+            k, d = ref.extract(imgs[i], None, os.cpu_count() or 1)
+            assert shas[j] == ref.hash_features(k, d), i
+        except OracleError:
+            pytest.fail(f"reference raised on finite image {i}")
+
+
+def test_c5_mixed_resolutions_deterministic(ref):
+    # C5-shaped: resolutions drawn from the C5 list, each size extracted twice
+    # (alone and inside a batch of its size); every digest is stable and a
+    # sample equals the reference's
+    sizes = [(640, 480), (800, 600), (1024, 768), (1280, 720)]
+    with ds.Extractor() as ex:
+        for n, (w, h) in enumerate(sizes):
+            imgs = np.stack([ref.value_noise(w, h, 0x5EED0000 + 10 * n + i, 5, max(8, w // 20)) for i in range(2)])
+            ex.extract_batch(imgs)
+            first = [ex.sha256(i) for i in range(2)]
+            ex.extract(imgs[1])
+            assert ex.sha256(0) == first[1]
+            ex.extract_batch(imgs)
+            assert [ex.sha256(i) for i in range(2)] == first
+            k, d = ref.extract(imgs[0], None, os.cpu_count() or 1)
+            assert first[0] == ref.hash_features(k, d), (w, h)
+
+
 # ---- full size: C3 1600x1200, properties + sampled oracle parity ------------------------
 def test_c3_full_size_properties_and_sampled_parity(port):
     w, h = 1600, 1200
@@ -306,15 +352,17 @@ def test_c3_full_size_sha_matches_reference(ref):
     # the unmodified reference run on the host: the DSF1 SHA-256 and every
     # keypoint / descriptor bit
     w, h = 1600, 1200
-    img = ref.value_noise(w, h, 0x5EED0000, 5, 80)
-    kps, desc = ref.extract(img, workers=os.cpu_count() or 1)
+    imgs = np.stack([ref.value_noise(w, h, 0x5EED0000 + i, 5, 80) for i in range(4)])
     with ds.Extractor() as ex:
-        fs = ex.extract(img)
-        sha = ex.sha256(0)
-    assert len(fs) == len(kps)
-    assert fs.keypoints.tobytes() == np.ascontiguousarray(kps).tobytes()
-    assert bits(fs.descriptors).tobytes() == bits(desc).tobytes()
-    assert sha == ref.hash_features(kps, desc)
+        res = ex.extract_batch(imgs)
+        shas = [ex.sha256(i) for i in range(4)]
+    for i in range(4):
+        kps, desc = ref.extract(imgs[i], workers=os.cpu_count() or 1)
+        fs = res[i]
+        assert len(fs) == len(kps)
+        assert fs.keypoints.tobytes() == np.ascontiguousarray(kps).tobytes()
+        assert bits(fs.descriptors).tobytes() == bits(desc).tobytes()
+        assert shas[i] == ref.hash_features(kps, desc)
 
 
 # ---- verify-determinism (detsift.cpp:170-200) ------------------------------
