@@ -365,21 +365,24 @@ __device__ __forceinline__ void b2_vpass(const BlurArgs& a, const float* sm, int
         if (x < w) {
             const int yb = y0 + rg * kB2Seg;
             const long long ob = (long long)yb * pitch + x;
+            float* dp = dst + ob;                            // row bases of this item, once
+            const float* sp = src + ob;
+            float* gp = dog ? dog + ob : dst;
 #pragma unroll
             for (int j = 0; j < kB2Seg; ++j) {
                 const int y = yb + j;
                 if (y < h) {
                     const float g = (float)acc[j];
                     const long long off = ob + j * pitch;
-                    dst[off] = g;
+                    dp[j * pitch] = g;
                     // DoG[i-1] = G[i] - G[i-1] (scalespace.cpp:209); G[i-1] was just read (L2)
                     if (MODE == kModeLevel) {
-                        if (dog) dog[off] = g - __ldg(src + off);
+                        if (dog) gp[j * pitch] = g - __ldg(sp + j * pitch);
                     } else if (MODE == kModeDecimate) {
                         // G[0] of this octave = even samples of G[s] of the previous one (scalespace.cpp:133-142)
                         const float prev = __ldg(src + (long long)(2 * y) * a.src_pitch + 2 * x);
                         seed[off] = prev;
-                        if (dog) dog[off] = g - prev;
+                        if (dog) gp[j * pitch] = g - prev;
                     }
                 }
             }
