@@ -767,11 +767,10 @@ struct StreamSmem {
     double* cv;     // cos*k
     AxisW* aw;      // [span]
     double* slot;   // [8 half-warps][32 entries (ri, ci, o)][16 lanes]
-    int* ew;        // min biased exponent (>= 1) of the nonzero weights in aw[k].{g, fr}
     float* ring;    // [kSRing][ring_pitch] bilinear samples, -1 = undefined
     float* raw;     // [n_dsp][128]
     int* cellmin;   // [2][32]: per pass (double-buffered), per cell: lower bound on the lowest-bit
-                    // exponent of the cell's leaves (+531: sum of 4 biased exponents)
+                    // exponent of the cell's leaves (biased: lowest bit >= 2^(e - 127 - 23))
     int* misc;      // [2][16]: kmin, kmax, start of cell c = -1..3 (misc[2 + c + 1]);
                     // double-buffered per scale
 };
@@ -844,8 +843,6 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         w.g = gr;
         w.fr = fr;
         S.aw[i] = w;
-        const int ewk = min(fr != 0.0f ? efield1(fr) : 255, gr != 0.0f ? efield1(gr) : 255);
-        S.ew[i] = ewk;
         S.ax[i] = D_ADD(cx, D_MUL(cosa, (double)k));
         S.cysu[i] = D_ADD(cy, D_MUL(sina, (double)k));
         S.sv[i] = D_MUL(sina, (double)k);
@@ -888,7 +885,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
     }
 
     double binacc = 0.0;
-    int binlsb = 1 << 20;   // lowest-bit exponent bound of the bin's leaves, + 4*127 + 23
+    int binlsb = 1 << 20;   // biased exponent of the bin's smallest leaf (lowest bit >= 2^(binlsb - 150))
     int kchain = 0;         // longest in-lane addition chain of any pass
     int npass = 0;
     int pRa = 0, pRb = -1, pP = 1;
@@ -1148,10 +1145,13 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 pa[3 * kSSlotE] = x6;
                 pb[3 * kSSlotE] = x7;
                 if (val > 0.0f) {
-                    // lowest nonzero orientation weight: min(fo, 1-fo), or ~1 (>= 2^-1) if one is 0
-                    const float mo = fminf(fo, go);
-                    const int eo = mo > 0.0f ? efield1(mo) : 126;
-                    lmin = min(lmin, efield1(val) + eo + S.ew[v - kA] + S.ew[u - kA]);
+                    // the lane's smallest leaf: leaves are RN(t * wo), monotone in t and
+                    // wo, so it is RN(min t * min nonzero wo); its exponent bounds every
+                    // leaf's lowest bit (a zero t, from an exactly-integral spatial bin,
+                    // only makes the bound pessimistic)
+                    const float tmin = fminf(fminf(t00, t01), fminf(t10, t11));
+                    const float mo = fo > 0.0f ? fminf(fo, go) : go;
+                    lmin = min(lmin, efield1(F_MUL(tmin, mo)));
                 }
             }
             if (cell < ncells && lmin < (1 << 20)) atomicMin(&S.cellmin[(npass & 1) * 32 + cell], lmin);
@@ -1171,7 +1171,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
     bool ok;
     float res;
     const int top = (int)((__double_as_longlong(binacc) >> 52) & 0x7ff) - 1023;
-    if (binacc == 0.0 || top - (binlsb - 4 * 127 - 23) <= 52) {
+    if (binacc == 0.0 || top - (binlsb - 127 - 23) <= 52) {
         ok = true;
         res = __double2float_rn(binacc);
     } else {
@@ -1185,7 +1185,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
     if (a.force_slow == -2) {   // diagnostic dump (block 0, keypoint 0): rows fi*4 + field
         const int fi = (int)(raw_out - S.raw) / kDescDim;
         a.desc[(fi * 4 + 0) * kDescDim + tid] = (float)binacc;
-        a.desc[(fi * 4 + 1) * kDescDim + tid] = (float)(binlsb - 4 * 127 - 23);
+        a.desc[(fi * 4 + 1) * kDescDim + tid] = (float)(binlsb - 127 - 23);
         a.desc[(fi * 4 + 2) * kDescDim + tid] = (float)(kchain * 1000 + npass);
         a.desc[(fi * 4 + 3) * kDescDim + tid] = ok ? 1.0f : 0.0f;
     }
@@ -1210,7 +1210,6 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
     S.aw = reinterpret_cast<AxisW*>(pbuf); pbuf += sizeof(AxisW) * SP;
     S.slot = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * 32 * kDescThreads;
-    S.ew = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * SP;
     S.ring = reinterpret_cast<float*>(pbuf);
     S.cellmin = cellmin;
     S.misc = misc;
@@ -1276,7 +1275,7 @@ size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp)
 size_t describe_stream_smem_bytes(int max_span, int n_dsp) {
     const size_t SP = (size_t)max_span, RP = (size_t)ring_pitch_for(max_span);
     return sizeof(float) * kDescDim * n_dsp + sizeof(double) * 4 * SP + sizeof(AxisW) * SP +
-           sizeof(double) * 32 * kDescThreads + sizeof(int) * SP + sizeof(float) * kSRing * RP;
+           sizeof(double) * 32 * kDescThreads + sizeof(float) * kSRing * RP;
 }
 
 int describe_stream_blocks_per_sm(size_t smem) {
