@@ -796,14 +796,6 @@ __device__ __forceinline__ void stream_misc_rearm(int* misc) {
     if (t < 16) misc[t] = (t == 1) ? -(1 << 30) : (1 << 30);
 }
 
-// a[i] for a register array indexed by a runtime value (select chain, no local memory)
-__device__ __forceinline__ int pick6(const int (&v)[6], int i) {
-    int r = v[0];
-#pragma unroll
-    for (int k = 1; k < 6; ++k) r = (i == k) ? v[k] : r;
-    return r;
-}
-
 __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const StreamSmem& S, const DevKeypoint& kp,
                                                       double f, double cosa, double sina, float* raw_out,
                                                       int ring_pitch, int* misc) {
@@ -861,13 +853,19 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         stream_misc_rearm(misc);
         return true;
     }
-    int st[6];   // first lattice index of cell c = -1..3 at st[c + 1]; st[5] = kmax + 1 (registers, read via pick6)
+    int st[6];   // first lattice index of cell c = -1..3 at st[c + 1]; st[5] = kmax + 1
     st[5] = kmax + 1;
 #pragma unroll
     for (int c = 4; c >= 0; --c) st[c] = min(misc[2 + c], st[c + 1]);
     int maxnc = 0;
 #pragma unroll
     for (int c = 0; c < 5; ++c) maxnc = max(maxnc, st[c + 1] - st[c]);
+    // run-time indexed copy in shared memory (misc[8..13] of this scale's
+    // buffer): every thread stores the same values before its own reads, so no
+    // barrier is needed; one LDS replaces a 5-deep select chain per lookup
+    int* sts = misc + 8;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) sts[c] = st[c];
     const int ub = kmin - 1;        // lattice index of ring column 0
     const int sw = kmax - kmin + 3; // ring columns in use
     const double wm1 = (double)(w - 1), hm1 = (double)(h - 1);
@@ -895,12 +893,12 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         const bool have = R <= 3;
         int Ra = 0, Rb = -1, va = 0, vb = -1, P = 1;
         if (have) {
-            const int rows = pick6(st, R + 2) - pick6(st, R + 1);
+            const int rows = sts[(R + 2)] - sts[(R + 1)];
             if (sub > 0 || rows > kSMaxPassRows) {   // a cell-row taller than a pass: equal row splits
                 const int nsplit = (rows + kSMaxPassRows - 1) / kSMaxPassRows;
                 const int chunk = (rows + nsplit - 1) / nsplit;
-                va = pick6(st, R + 1) + sub * chunk;
-                vb = min(va + chunk, pick6(st, R + 2)) - 1;
+                va = sts[(R + 1)] + sub * chunk;
+                vb = min(va + chunk, sts[(R + 2)]) - 1;
                 Ra = Rb = R;
                 if (++sub == nsplit) {
                     sub = 0;
@@ -911,14 +909,14 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 int tot = rows;
                 ++R;
                 while (R <= 3) {
-                    const int rr = pick6(st, R + 2) - pick6(st, R + 1);
+                    const int rr = sts[(R + 2)] - sts[(R + 1)];
                     if (rr > kSMaxPassRows || tot + rr > kSMaxPassRows) break;
                     tot += rr;
                     ++R;
                 }
                 Rb = R - 1;
-                va = pick6(st, Ra + 1);
-                vb = pick6(st, Rb + 2) - 1;
+                va = sts[(Ra + 1)];
+                vb = sts[(Rb + 2)] - 1;
             }
             P = kSLanes / ((Rb - Ra + 1) * 5);
             // P1: samples of rows [va-1, vb+1] not yet in the ring (describe.cpp:56-65)
@@ -1065,9 +1063,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
             int npts = 0, nc = 1, rv0 = 0, cu0 = 0;
             if (cell < ncells) {
                 const int Rl = Ra + cell / 5, Cl = cell % 5 - 1;
-                const int r0 = max(va, pick6(st, Rl + 1)), r1 = min(vb, pick6(st, Rl + 2) - 1);
-                cu0 = pick6(st, Cl + 1);
-                nc = pick6(st, Cl + 2) - cu0;
+                const int r0 = max(va, sts[(Rl + 1)]), r1 = min(vb, sts[(Rl + 2)] - 1);
+                cu0 = sts[(Cl + 1)];
+                nc = sts[(Cl + 2)] - cu0;
                 rv0 = r0;
                 if (r1 >= r0 && nc > 0) npts = (r1 - r0 + 1) * nc;
             }
@@ -1079,8 +1077,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
             // point pi = part + j*P of the cell in row-major order: (rr, cc),
             // advanced incrementally (dq rows + dr columns per step)
             const int ncs = max(nc, 1);
-            int rr = part / ncs, cc = part - rr * ncs;
-            const int dq = P / ncs, dr = P - dq * ncs;
+            const float inv_ncs = 1.0f / (float)ncs;   // exact quotients for operands < 2^10
+            int rr = (int)(((float)part + 0.5f) * inv_ncs), cc = part - rr * ncs;
+            const int dq = (int)(((float)P + 0.5f) * inv_ncs), dr = P - dq * ncs;
             for (int pi = part; pi < npts; pi += P) {
                 const int v = rv0 + rr, u = cu0 + cc;
                 cc += dr;
