@@ -918,7 +918,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 va = sts[(Ra + 1)];
                 vb = sts[(Rb + 2)] - 1;
             }
-            P = kSLanes / ((Rb - Ra + 1) * 5);
+            P = (Rb - Ra + 1) == 1 ? 25 : (Rb - Ra + 1) == 2 ? 12 : (Rb - Ra + 1) == 3 ? 8 : (Rb - Ra + 1) == 4 ? 6 : 5;   // 125 / (5 * cell rows)
             // P1: samples of rows [va-1, vb+1] not yet in the ring (describe.cpp:56-65)
             const int s0 = max(va - 1, have_hi + 1), s1 = vb + 1;
             if (s1 >= s0) {
@@ -1039,7 +1039,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                     const int l0 = cell * pP;
                     // lanes in a rotated (per-orientation) fixed order: the 8
                     // orientations of one cell hit 8 different bank pairs
-                    int qq = bori % pP;
+                    int qq = bori < pP ? bori : bori - pP;   // bori % pP (bori < 8 <= 2 * pP)
                     int q = 0;
                     for (; q + 1 < pP; q += 2) {
                         const int qa = qq, qb = (qq + 1 == pP) ? 0 : qq + 1;
@@ -1059,7 +1059,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         // P2: lane (cell, part) over its share of the cell's points
         {
             const int ncells = (Rb - Ra + 1) * 5;
-            const int cell = tid / P, part = tid - cell * P;
+            const int cell = (int)(((float)tid + 0.5f) * (1.0f / (float)P)), part = tid - cell * P;   // tid / P (exact)
             int npts = 0, nc = 1, rv0 = 0, cu0 = 0;
             if (cell < ncells) {
                 const int Rl = Ra + cell / 5, Cl = cell % 5 - 1;
@@ -1155,7 +1155,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
             }
             if (cell < ncells && lmin < (1 << 20)) atomicMin(&S.cellmin[(npass & 1) * 32 + cell], lmin);
         }
-        kchain = max(kchain, ((vb - va + 1) * maxnc + P - 1) / P);
+        kchain = max(kchain, (int)((float)((vb - va + 1) * maxnc) * (1.0f / (float)P)) + 1);   // >= ceil(./P): a bound
         ++npass;
         __syncthreads();
         pending = true;
