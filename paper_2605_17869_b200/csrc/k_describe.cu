@@ -796,25 +796,39 @@ __device__ __forceinline__ void stream_misc_rearm(int* misc) {
     if (t < 16) misc[t] = (t == 1) ? -(1 << 30) : (1 << 30);
 }
 
+// Per-(keypoint, DSP scale) scalars (describe.cpp:37-47), formed once per
+// keypoint by one thread per scale instead of redundantly by every thread.
+struct ScaleSetup {
+    double cx, cy, bw;
+    int lvl, radius, kA, kB;
+};
+__device__ __forceinline__ ScaleSetup make_scale_setup(const PyramidDesc& p, const DevKeypoint& kp, double f) {
+    ScaleSetup r;
+    const double to_input = ldexp(1.0, kp.octave) * (p.upsampled ? 0.5 : 1.0);
+    r.cx = kp.x / to_input;
+    r.cy = kp.y / to_input;
+    const double sigma_rel = kp.sigma / to_input;
+    r.lvl = nearest_level_d(p, f * sigma_rel);
+    r.bw = 3.0 * f * sigma_rel;
+    r.radius = (int)llround(r.bw * (kDescCells + 1) * 0.5 * 1.4142135623730951);
+    // table span [kA, kB] contains the in-range span and its guard entries
+    const double hb = 2.5 * r.bw;
+    r.kA = max(-r.radius - 1, (int)floor(-hb) - 3);
+    r.kB = min(r.radius + 1, (int)ceil(hb) + 3);
+    return r;
+}
+
 __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const StreamSmem& S, const DevKeypoint& kp,
-                                                      double f, double cosa, double sina, float* raw_out,
-                                                      int ring_pitch, int* misc) {
+                                                      const ScaleSetup& ss, double cosa, double sina,
+                                                      float* raw_out, int ring_pitch, int* misc) {
     const PyramidDesc& p = a.pyr;
     const OctaveDesc& od = p.oct[kp.octave];
-    const double to_input = ldexp(1.0, kp.octave) * (p.upsampled ? 0.5 : 1.0);
-    const double cx = kp.x / to_input, cy = kp.y / to_input;
-    const double sigma_rel = kp.sigma / to_input;
-    const int lvl = nearest_level_d(p, f * sigma_rel);
+    const double cx = ss.cx, cy = ss.cy, bw = ss.bw;
+    const int lvl = ss.lvl, radius = ss.radius, kA = ss.kA, kB = ss.kB;
     const float* __restrict__ img =
         od.gauss + (long long)kp.image * p.gauss_img_stride(kp.octave) + (long long)lvl * od.level_stride;
     const int w = od.w, h = od.h, pitch = od.pitch;
-    const double bw = 3.0 * f * sigma_rel;
-    const int radius = (int)llround(bw * (kDescCells + 1) * 0.5 * 1.4142135623730951);
     const int tid = threadIdx.x;
-    // table span [kA, kB] contains the in-range span and its guard entries
-    const double hb = 2.5 * bw;
-    const int kA = max(-radius - 1, (int)floor(-hb) - 3);
-    const int kB = min(radius + 1, (int)ceil(hb) + 3);
     const int span = kB - kA + 1;
     if (span > a.max_span) {   // host sized the tables from the largest sigma; never clip silently
         if (tid == 0) atomicOr(a.err, kErrDescriptorLattice);
@@ -1198,6 +1212,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     __shared__ double red[4];
     __shared__ int misc[32];
     __shared__ int cellmin[64];
+    __shared__ ScaleSetup sscale[kMaxDsp];
     const int SP = a.max_span;
     const int RP = ring_pitch_for(SP);
     StreamSmem S;
@@ -1232,9 +1247,11 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
         if (k >= n) break;
         const DevKeypoint kp = a.kps[k];
         const double2 cs = a.trig[k];
+        if (tid < a.n_dsp) sscale[tid] = make_scale_setup(a.pyr, kp, a.dsp[tid]);
+        __syncthreads();
         bool all_ok = true;
         for (int fi = 0; fi < a.n_dsp; ++fi, ++call) {
-            const bool ok = raw_descriptor_stream(a, S, kp, a.dsp[fi], cs.x, cs.y, S.raw + fi * kDescDim, RP,
+            const bool ok = raw_descriptor_stream(a, S, kp, sscale[fi], cs.x, cs.y, S.raw + fi * kDescDim, RP,
                                                   misc + 16 * (call & 1));
             const bool sok = __syncthreads_and(ok);
             if (!sok && a.force_slow == 0) {
