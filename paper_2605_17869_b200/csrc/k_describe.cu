@@ -736,7 +736,7 @@ describe_fast_kernel(const __grid_constant__ DescArgs a) {
 #define DSIFT_P1_TH 4
 #endif
 #ifndef DSIFT_P1_ILP
-#define DSIFT_P1_ILP 2
+#define DSIFT_P1_ILP 3
 #endif
 constexpr int kP1Ilp = DSIFT_P1_ILP;   // interior samples in flight per thread
 constexpr int kSRing = 32;                 // sample rows resident (power of two)
