@@ -110,11 +110,15 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
             __syncwarp();
         }
         // one window pixel q (row-major, orient.cpp:40-58): its bin and leaf value
+        // q / nx without an integer division: exact for q < 2^20 (the window
+        // is at most a few thousand pixels)
+        const float inv_nx = 1.0f / (float)max(nx, 1);
         auto pixel = [&](int q, int& bin, float& val) {
             bin = -1;
             val = 0.0f;
             if (q < npx) {
-                const int x = xa + q % nx, y = ya + q / nx;
+                const int qy = (int)(((float)q + 0.5f) * inv_nx);
+                const int x = xa + (q - qy * nx), y = ya + qy;
                 const float* r0 = img + (long long)y * od.pitch;
                 const float gx = F_SUB(__ldg(r0 + x + 1), __ldg(r0 + x - 1));
                 const float gy = F_SUB(__ldg(r0 + od.pitch + x), __ldg(r0 - od.pitch + x));
