@@ -67,3 +67,23 @@ def test_hypot_bit_exact(lc, mode, n):
     first = (C.c_double * 3)()
     bad = lc.lc_hypot_mismatch(4242 + mode, n, mode, first)
     assert bad == 0, f"{bad} mismatches, first (x, y, got) = {list(first)}"
+
+
+def test_atan2f_x_equal_one(lc):
+    # fdlibm routes x == 1 to atanf(y); the restatement takes its generic fast
+    # path there (y / 1 == y, atanf odd bit for bit) -- check against glibc
+    libm = C.CDLL("libm.so.6")
+    libm.atan2f.restype = C.c_float
+    libm.atan2f.argtypes = [C.c_float, C.c_float]
+    lc.lc_atan2f_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p]
+    import numpy as np
+    rng = np.random.default_rng(11)
+    bits = rng.integers(0, 2**32, 200_000, dtype=np.uint64).astype(np.uint32)
+    y = bits.view(np.float32)
+    y = y[np.isfinite(y)]
+    y = np.concatenate([y, rng.uniform(-4, 4, 50_000).astype(np.float32), np.float32([0.0, -0.0, 1e-30, -3e38])])
+    x = np.ones_like(y)
+    out = np.empty_like(y)
+    lc.lc_atan2f_batch(y.ctypes.data, x.ctypes.data, len(y), out.ctypes.data)
+    ref = np.array([libm.atan2f(float(v), 1.0) for v in y], np.float32)
+    assert out.view(np.uint32).tolist() == ref.view(np.uint32).tolist()
