@@ -49,7 +49,6 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
-    ap.add_argument("--desc-kernel", type=int, default=2, help="certified descriptor kernel (A/B)")
     return ap.parse_args()
 
 
@@ -261,7 +260,6 @@ def run_ours(args, rank, local_rank, world):
     stream = torch.cuda.Stream()
     ex.set_stream(stream.cuda_stream)
     ex.set_profiling(True)
-    ex.set_desc_kernel(args.desc_kernel)
     imgs = torch.empty((B, H, W), dtype=torch.float32, device="cuda")
     ex.synth_value_noise(imgs.data_ptr(), B, W, H, SEED0 + rank * B, 5, cells_for(W))
     stream.synchronize()
@@ -411,7 +409,7 @@ def run_ours(args, rank, local_rank, world):
                      "keypoints_per_s": kps_per_image * B / desc_s,
                      "lattice_points_per_s_est": kps_per_image * B * lattice_per_kp / desc_s,
                      "share_of_step": stages["describe"] / max(1e-9, sum(stages.values())),
-                     "exact_fallbacks_last_step": fallbacks, "desc_kernel": args.desc_kernel}
+                     "exact_fallbacks_last_step": fallbacks}
 
     # ---- matching: ratio_match of the first two images' descriptors,
     # device-resident (DLPack export, no host copy), CUDA events

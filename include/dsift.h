@@ -12,8 +12,10 @@
  * DSIFT_EINVAL it is the reference's std::invalid_argument text).
  *
  * Threading: one dsift_ctx per (device, host thread); all device work of a
- * context is ordered on its CUDA stream.  Results stay on the device until
- * copied or exported and are owned by the context until the next extract.
+ * context is ordered on its CUDA stream (host inputs are copied on a second
+ * stream so they overlap the previous batch).  Results stay on the device
+ * until copied or exported; a result is owned by its dsift_result (the
+ * context's own one by default) until the next extract into it.
  */
 #ifndef DSIFT_H
 #define DSIFT_H
@@ -25,7 +27,7 @@
 extern "C" {
 #endif
 
-#define DSIFT_ABI_VERSION 1
+#define DSIFT_ABI_VERSION 2
 
 enum {
     DSIFT_OK = 0,
@@ -64,6 +66,17 @@ typedef struct dsift_keypoint {
 } dsift_keypoint;
 
 typedef struct dsift_ctx dsift_ctx;
+/* A batch result (keypoints, descriptors, offsets) with its own completion
+ * event.  Every context has a built-in one; dsift_result_create adds more so
+ * several batches can be in flight on one context. */
+typedef struct dsift_result dsift_result;
+
+/* detsift::GrayImage (core.hpp:11-26) as a view: row-major float32
+ * width x height, values in [0, 1], on the host or the device (per flags). */
+typedef struct dsift_image {
+    const float* data;
+    int32_t width, height;
+} dsift_image;
 
 /* input flags */
 #define DSIFT_INPUT_HOST 0
@@ -86,8 +99,10 @@ int dsift_create(int device, const dsift_config* cfg, dsift_ctx** out);
 void dsift_destroy(dsift_ctx* ctx);
 /* Use the caller's cudaStream_t (NULL restores the context's own stream). */
 int dsift_set_stream(dsift_ctx* ctx, void* cuda_stream);
-/* Per-image capacity of the keypoint work lists (0 = automatic, from the
- * image size).  Overflow is reported as DSIFT_ECAPACITY, never truncated. */
+/* Per-image capacity of the keypoint work lists.  0 = automatic: sized from
+ * the image, grown x4 and the batch replayed inside dsift_result_sync if a
+ * list overflows (so every keypoint is still returned).  A fixed capacity
+ * reports an overflow as DSIFT_ECAPACITY, never truncated output. */
 int dsift_set_capacity(dsift_ctx* ctx, int64_t max_keypoints_per_image);
 
 /* ---- full pipeline: detsift::extract (io.cpp:111-142) --------------------- */
@@ -97,6 +112,19 @@ int dsift_set_capacity(dsift_ctx* ctx, int64_t max_keypoints_per_image);
  * per image in canonical order (core.cpp:116-170). */
 int dsift_extract_batch(dsift_ctx* ctx, const float* images, int n, int w, int h, int flags);
 int dsift_extract(dsift_ctx* ctx, const float* image, int w, int h, int flags);
+/* Ragged batch: n images of any sizes (the reference's extract takes any size
+ * per call, io.cpp:111-142).  Same-size images are processed together; the
+ * output is in batch order, image i's features bit-identical to a
+ * single-image extract of it.  Device inputs must stay valid until
+ * dsift_result_sync returns (a capacity overflow replays the batch). */
+int dsift_extract_images(dsift_ctx* ctx, const dsift_image* images, int n, int flags);
+/* Result handles.  dsift_result_select(ctx, r) routes the following extract
+ * and dsift_result_* calls of ctx to r (NULL = the context's own result), so
+ * a serving loop keeps batch k+1 running while it reads batch k out.  A
+ * result must be destroyed before its context. */
+int dsift_result_create(dsift_ctx* ctx, dsift_result** out);
+void dsift_result_destroy(dsift_result* result);
+int dsift_result_select(dsift_ctx* ctx, dsift_result* result);
 /* 8-bit ingest (replaces load_image's float conversion, io.cpp:49-81): n
  * images of w x h pixels with channels = 1 (P5 gray) or 3 (P6 RGB,
  * interleaved), host or device (flags).  The bytes are converted on the
@@ -152,7 +180,8 @@ int dsift_load_image(const char* path, int32_t* w, int32_t* h, int32_t* channels
  * count converted on the device (dev_out must be a device pointer). */
 int dsift_ingest_u8(dsift_ctx* ctx, const uint8_t* pixels, int64_t n_px, int channels, int flags,
                     float* dev_out);
-/* Waits for the last extract; *total = keypoints over all images. */
+/* dsift_result_* act on the selected result (dsift_result_select).
+ * Waits for the last extract; *total = keypoints over all images. */
 int dsift_result_sync(dsift_ctx* ctx, int64_t* total);
 /* [begin, begin+count) of `image` inside the batch result (after sync). */
 int dsift_result_range(dsift_ctx* ctx, int image, int64_t* begin, int64_t* count);
@@ -217,22 +246,19 @@ int64_t dsift_kernel_launches(dsift_ctx* ctx);
  * descriptors} of the last extract. */
 int dsift_set_profiling(dsift_ctx* ctx, int on);
 /* Options: DSIFT_OPT_FORCE_EXACT = 1 routes every descriptor through the
- * exact scan-order kernel (test hook for the certified fast path). */
+ * exact scan-order kernel (test hook for the certified fast path); 0 or 1. */
 #define DSIFT_OPT_FORCE_EXACT 1
-/* DSIFT_OPT_DESC_KERNEL selects the certified descriptor kernel: 2 (default)
- * = band-streamed cell-lane kernel, 1 = the earlier item/run kernel.  Both are
- * bit-identical to the reference; the option exists for A/B measurement. */
-#define DSIFT_OPT_DESC_KERNEL 2
+/* DSIFT_OPT_CAPACITY_SCALE: scale of the automatic work-list capacities in
+ * 1/1000 (default 1000; an overflow multiplies it by 4 and replays). */
+#define DSIFT_OPT_CAPACITY_SCALE 2
 int dsift_set_option(dsift_ctx* ctx, int key, int64_t value);
 /* Statistics of the last synced result: DSIFT_STAT_EXACT_FALLBACKS = number
  * of keypoints whose descriptor the fast path could not certify. */
 #define DSIFT_STAT_EXACT_FALLBACKS 1
+/* DSIFT_STAT_REPLAYS = times the last result was replayed after an automatic
+ * capacity overflow. */
+#define DSIFT_STAT_REPLAYS 2
 int64_t dsift_stat(dsift_ctx* ctx, int key);
-/* Test probe: evaluates the device restatements of the host libm calls on
- * the path (dsift_math.cuh) over n inputs.  mode 0: atan2f, in = n x {y, x}
- * float32 pairs, out = n float32; mode 1: exp, in/out = n float64; mode 2:
- * sin/cos, in = n float64, out = n x {sin, cos} float64. */
-int dsift_libm_probe(dsift_ctx* ctx, int mode, const void* in, int64_t n, void* out);
 int dsift_stage_times(dsift_ctx* ctx, float* ms5);
 
 #ifdef __cplusplus

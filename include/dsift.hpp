@@ -1,9 +1,14 @@
 // include/dsift.hpp — header-only C++ face of the C ABI, mirroring the
 // reference's extraction API so existing C++ callers swap one include:
 //
-//   reference:  detsift::FeatureSet detsift::extract(const GrayImage&, const SiftConfig&, int workers)
+//   reference:  detsift::FeatureSet detsift::extract(const GrayImage&, const SiftConfig&, int workers = 1)
 //               (/root/reference/proj/include/detsift/io.hpp:17-19)
-//   here:       dsift::FeatureSet  dsift::extract(const GrayImage&, const SiftConfig&, int device)
+//   here:       dsift::FeatureSet  dsift::extract(const GrayImage&, const SiftConfig&, int workers = 1)
+//
+// `workers` keeps its meaning (host threads, 0 = all; parallel.hpp:12-16) and,
+// as in the reference, never changes the output.  The device is
+// dsift::default_device() ($DSIFT_DEVICE, else 0); Extractor picks one
+// explicitly.  Each host thread reuses one cached context per config.
 //
 // The types restate detsift's (core.hpp:11-78) field for field; Keypoint is
 // layout-identical to the reference struct and to dsift_keypoint.  Errors
@@ -14,6 +19,7 @@
 #include <algorithm>
 #include <array>
 #include <cstdint>
+#include <cstdlib>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -68,6 +74,7 @@ struct SiftConfig {   // core.hpp:30-47
         return c;
     }
     void validate() const;   // SiftConfig::validate (core.cpp:17-46)
+    bool operator==(const SiftConfig&) const = default;
 };
 
 struct Keypoint {   // core.hpp:55-63
@@ -127,7 +134,7 @@ inline void SiftConfig::validate() const {
 // RAII context: one device, one stream, reusable across many images.
 class Extractor {
    public:
-    explicit Extractor(const SiftConfig& cfg = {}, int device = 0) : cfg_(cfg) {
+    explicit Extractor(const SiftConfig& cfg = {}, int device = 0) : cfg_(cfg), device_(device) {
         const dsift_config c = cfg_.to_c();
         dsift_ctx* ctx = nullptr;
         check(dsift_create(device, &c, &ctx));
@@ -137,22 +144,13 @@ class Extractor {
     FeatureSet extract(const GrayImage& img) {
         return std::move(extract_batch(&img, 1)[0]);
     }
-    // Same-size images in one batch (one pipeline pass over the batch).
+    // Any number of images of any sizes in one call (dsift_extract_images);
+    // result i is bit-identical to extract(imgs[i]).
     std::vector<FeatureSet> extract_batch(const GrayImage* imgs, int n) {
         if (n <= 0) return {};
-        const int w = imgs[0].width, h = imgs[0].height;
-        std::vector<float> packed;
-        const float* src = imgs[0].data.data();
-        if (n > 1) {
-            packed.resize(size_t(n) * w * h);
-            for (int i = 0; i < n; ++i) {
-                if (imgs[i].width != w || imgs[i].height != h)
-                    throw std::invalid_argument("extract_batch: images must share one size");
-                std::copy(imgs[i].data.begin(), imgs[i].data.end(), packed.begin() + size_t(i) * w * h);
-            }
-            src = packed.data();
-        }
-        check(dsift_extract_batch(ctx_.get(), src, n, w, h, DSIFT_INPUT_HOST));
+        std::vector<dsift_image> views(static_cast<size_t>(n));
+        for (int i = 0; i < n; ++i) views[i] = dsift_image{imgs[i].data.data(), imgs[i].width, imgs[i].height};
+        check(dsift_extract_images(ctx_.get(), views.data(), n, DSIFT_INPUT_HOST));
         int64_t total = 0;
         check(dsift_result_sync(ctx_.get(), &total));
         std::vector<Keypoint> kps(static_cast<size_t>(total));
@@ -201,21 +199,38 @@ class Extractor {
         return h;
     }
     dsift_ctx* handle() { return ctx_.get(); }
+    int device() const { return device_; }
+    const SiftConfig& config() const { return cfg_; }
 
    private:
     struct Deleter {
         void operator()(dsift_ctx* c) const { dsift_destroy(c); }
     };
     SiftConfig cfg_;
+    int device_ = 0;
     std::unique_ptr<dsift_ctx, Deleter> ctx_;
 };
 
-// Drop-in for detsift::extract; `device` replaces `workers` (output is
-// bit-identical to the reference for any device, as the reference's is for
-// any worker count).
-inline FeatureSet extract(const GrayImage& img, const SiftConfig& cfg = {}, int device = 0) {
-    Extractor ex(cfg, device);
-    return ex.extract(img);
+// The device the drop-in extract() uses: $DSIFT_DEVICE, else 0.
+inline int default_device() {
+    const char* e = std::getenv("DSIFT_DEVICE");
+    return e ? std::atoi(e) : 0;
+}
+
+// Drop-in for detsift::extract (io.hpp:17-19, io.cpp:111-142).  `workers`
+// is accepted with the reference's meaning and, like there, does not change
+// the output (io.hpp:17-18); the fan-out is the GPU's.  The context (stream,
+// buffers) is cached per host thread and reused while config and device stay
+// the same, so per-image calls pay no setup.
+inline FeatureSet extract(const GrayImage& img, const SiftConfig& cfg = {}, int workers = 1) {
+    (void)workers;
+    thread_local std::unique_ptr<Extractor> cached;
+    const int device = default_device();
+    if (!cached || cached->device() != device || !(cached->config() == cfg)) {
+        cached.reset();
+        cached = std::make_unique<Extractor>(cfg, device);
+    }
+    return cached->extract(img);
 }
 
 }  // namespace dsift

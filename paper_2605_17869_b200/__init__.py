@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import threading
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -125,8 +126,7 @@ _LIB = None
 
 
 def library_path() -> str:
-    # DSIFT_LIBRARY: an alternative in-tree build (A/B measurements)
-    return os.environ.get("DSIFT_LIBRARY") or os.path.join(HERE, "libdsift.so")
+    return os.path.join(HERE, "libdsift.so")
 
 
 def load_library():
@@ -173,7 +173,9 @@ def load_library():
         "dsift_kernel_launches": ([vp], C.c_int64),
         "dsift_set_profiling": ([vp, i32], C.c_int), "dsift_stage_times": ([vp, vp], C.c_int),
         "dsift_set_option": ([vp, i32, i64], C.c_int), "dsift_stat": ([vp, i32], C.c_int64),
-        "dsift_libm_probe": ([vp, i32, vp, i64, vp], C.c_int),
+        "dsift_extract_images": ([vp, vp, i32, i32], C.c_int),
+        "dsift_result_create": ([vp, vp], C.c_int), "dsift_result_destroy": ([vp], None),
+        "dsift_result_select": ([vp, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -215,7 +217,22 @@ class Extractor:
         _check(self.lib, self.lib.dsift_create(device, C.byref(self._ccfg), C.byref(ctx)))
         self.ctx = ctx
         self.device = device
-        self.batch = 0
+        self._batch = 0
+        self._own_batch = 0
+        self._selected = None
+        self._stream = None
+
+    @property
+    def batch(self) -> int:
+        return self._batch
+
+    @batch.setter
+    def batch(self, n: int) -> None:
+        self._batch = n
+        if getattr(self, "_selected", None) is not None:
+            self._selected.batch = n
+        else:
+            self._own_batch = n
 
     def close(self):
         if getattr(self, "ctx", None):
@@ -237,6 +254,7 @@ class Extractor:
     # ---- hot path ----------------------------------------------------------
     def set_stream(self, cuda_stream_handle: int | None) -> None:
         _check(self.lib, self.lib.dsift_set_stream(self.ctx, C.c_void_p(cuda_stream_handle or 0)))
+        self._stream = cuda_stream_handle
 
     def set_capacity(self, per_image: int) -> None:
         _check(self.lib, self.lib.dsift_set_capacity(self.ctx, per_image))
@@ -258,6 +276,39 @@ class Extractor:
         _check(self.lib, self.lib.dsift_extract_batch(self.ctx, a.ctypes.data, a.shape[0], a.shape[2],
                                                       a.shape[1], INPUT_HOST))
         self.batch = a.shape[0]
+
+    def submit_images(self, images, device: bool = False) -> None:
+        """Enqueue a ragged batch (dsift_extract_images): a list of [h, w]
+        float32 host arrays of any sizes, or (device_ptr, w, h) tuples."""
+        n = len(images)
+        arr = (_Image * max(1, n))()
+        keep = []
+        for i, im in enumerate(images):
+            if device:
+                ptr, w, h = im
+                arr[i] = _Image(C.c_void_p(ptr), w, h)
+            else:
+                a = _f32(im)
+                keep.append(a)
+                arr[i] = _Image(C.c_void_p(a.ctypes.data), a.shape[1], a.shape[0])
+        self._pin = (arr, keep)
+        _check(self.lib, self.lib.dsift_extract_images(self.ctx, arr, n, INPUT_DEVICE if device else INPUT_HOST))
+        self.batch = n
+
+    def extract_images(self, images) -> list[FeatureSet]:
+        """detsift::extract over images of any sizes in one call; results in batch order."""
+        self.submit_images(images)
+        return self.results()
+
+    def new_result(self) -> "Result":
+        """A result handle of this context (dsift_result_create)."""
+        return Result(self)
+
+    def select(self, result: "Result | None") -> None:
+        """Route the following extract / result calls to `result` (None = the context's own)."""
+        _check(self.lib, self.lib.dsift_result_select(self.ctx, result.handle if result else None))
+        self._selected = result
+        self._batch = result.batch if result else self._own_batch
 
     def sync(self) -> int:
         total = C.c_int64()
@@ -325,12 +376,22 @@ class Extractor:
     def ratio_match(self, desc_a, desc_b, ratio: float = 0.8):
         """detsift::ratio_match (match.cpp:77-119) on the device: returns
         (pairs structured [k] (a, b, distance), putative_a, putative_b).  Inputs are
-        host arrays [n, 128] float32 or torch CUDA tensors (zero copy)."""
+        host arrays [n, 128] float32 or torch CUDA tensors (zero copy: contiguous
+        float32 [n, 128] on this context's device; the call is ordered after the
+        current torch stream)."""
         flags = INPUT_HOST
+        stream = None
         if hasattr(desc_a, "data_ptr") and getattr(desc_a, "is_cuda", False):
+            import torch
+            for t in (desc_a, desc_b):
+                if not (getattr(t, "is_cuda", False) and t.dtype == torch.float32 and t.is_contiguous()
+                        and t.dim() == 2 and t.shape[1] == DESC_DIM and t.device.index == self.device):
+                    raise InvalidArgument(DSIFT_EINVAL, "ratio_match: device descriptors must be contiguous "
+                                          f"float32 [n, {DESC_DIM}] tensors on cuda:{self.device}")
             pa, na, da = desc_a.data_ptr(), desc_a.shape[0], desc_a.shape[1]
             pb, nb, db = desc_b.data_ptr(), desc_b.shape[0], desc_b.shape[1]
             flags = INPUT_DEVICE
+            stream = torch.cuda.current_stream(self.device).cuda_stream
         else:
             a = np.ascontiguousarray(desc_a, np.float32)
             b = np.ascontiguousarray(desc_b, np.float32)
@@ -340,9 +401,15 @@ class Extractor:
         cap = max(1, min(na, nb))
         out = np.zeros(cap, MATCH_DTYPE)
         n, put_a, put_b = C.c_int64(), C.c_int64(), C.c_int64()
-        _check(self.lib, self.lib.dsift_ratio_match(self.ctx, C.c_void_p(pa), na, C.c_void_p(pb), nb, da, db,
-                                                    C.c_float(ratio), flags, out.ctypes.data, cap, C.byref(n),
-                                                    C.byref(put_a), C.byref(put_b)))
+        if stream is not None:   # run on the producer's stream, then restore the context's own
+            self.set_stream(stream)
+        try:
+            _check(self.lib, self.lib.dsift_ratio_match(self.ctx, C.c_void_p(pa), na, C.c_void_p(pb), nb, da, db,
+                                                        C.c_float(ratio), flags, out.ctypes.data, cap, C.byref(n),
+                                                        C.byref(put_a), C.byref(put_b)))
+        finally:
+            if stream is not None:
+                self.set_stream(self._stream)
         return out[:n.value], put_a.value, put_b.value
 
     def magsac_lite(self, matches, iterations: int, tau: float, seed: int):
@@ -397,34 +464,17 @@ class Extractor:
         """Route every descriptor through the exact scan-order kernel (test hook)."""
         _check(self.lib, self.lib.dsift_set_option(self.ctx, 1, int(on)))
 
-    def set_desc_kernel(self, which: int) -> None:
-        """Certified descriptor kernel: 2 = band-streamed cell-lane (default), 1 = earlier run kernel."""
-        _check(self.lib, self.lib.dsift_set_option(self.ctx, 2, int(which)))
+    def set_capacity_scale(self, permille: int) -> None:
+        """Scale of the automatic work-list capacities in 1/1000 (DSIFT_OPT_CAPACITY_SCALE)."""
+        _check(self.lib, self.lib.dsift_set_option(self.ctx, 2, int(permille)))
+
+    def replays(self) -> int:
+        """Times the last result was replayed after an automatic capacity overflow."""
+        return int(self.lib.dsift_stat(self.ctx, 2))
 
     def exact_fallbacks(self) -> int:
         """Keypoints of the last result whose fast-path certificate failed."""
         return int(self.lib.dsift_stat(self.ctx, 1))
-
-    def libm_probe(self, mode: int, inputs: np.ndarray) -> np.ndarray:
-        """Device restatements of atan2f (mode 0, inputs [n, 2] float32 (y, x)),
-        exp (mode 1, float64) and sin/cos (mode 2, float64 -> [n, 2] (sin, cos))."""
-        if mode == 3:   # inputs = (seed, n): [mismatches, first failing (y << 32 | x) bits]
-            seed, n = inputs
-            a = np.array([seed], np.uint64)
-            out = np.zeros(2, np.uint64)
-            _check(self.lib, self.lib.dsift_libm_probe(self.ctx, 3, a.ctypes.data, int(n), out.ctypes.data))
-            return out
-        if mode == 0:
-            a = np.ascontiguousarray(inputs, np.float32).reshape(-1, 2)
-            out = np.empty(len(a), np.float32)
-        elif mode == 1:
-            a = np.ascontiguousarray(inputs, np.float64).ravel()
-            out = np.empty(len(a), np.float64)
-        else:
-            a = np.ascontiguousarray(inputs, np.float64).ravel()
-            out = np.empty((len(a), 2), np.float64)
-        _check(self.lib, self.lib.dsift_libm_probe(self.ctx, mode, a.ctypes.data, len(a), out.ctypes.data))
-        return out
 
     def export_torch(self, which: int = 1):
         """Zero-copy DLPack export of the last result as a torch CUDA tensor
@@ -538,6 +588,29 @@ def load_image(path: str) -> np.ndarray:
     return out
 
 
+class _Image(C.Structure):
+    _fields_ = [("data", C.c_void_p), ("width", C.c_int32), ("height", C.c_int32)]
+
+
+class Result:
+    """A dsift_result handle: one more batch in flight on the same context
+    (select it, submit, select another, submit, select back, read)."""
+
+    def __init__(self, ex: "Extractor"):
+        self.ex = ex
+        self.batch = 0
+        h = C.c_void_p()
+        _check(ex.lib, ex.lib.dsift_result_create(ex.ctx, C.byref(h)))
+        self.handle = h
+
+    def close(self) -> None:
+        if self.handle:
+            if self.ex._selected is self:
+                self.ex.select(None)
+            self.ex.lib.dsift_result_destroy(self.handle)
+            self.handle = None
+
+
 class _MagsacResult(C.Structure):
     _fields_ = [("success", C.c_int32), ("best_iteration", C.c_int32), ("score", C.c_double),
                 ("h", C.c_double * 9)]
@@ -562,10 +635,29 @@ def corner_error(h_est, h_gt, width: float, height: float) -> float:
     return out.value
 
 
-def extract(img, cfg: SiftConfig | None = None, device: int = 0) -> FeatureSet:
-    """FeatureSet detsift::extract(const GrayImage&, const SiftConfig&) on a B200."""
-    with Extractor(cfg, device) as ex:
-        return ex.extract(img)
+_TLS = threading.local()
+
+
+def default_device() -> int:
+    """The device the drop-in extract() runs on: $DSIFT_DEVICE, else 0."""
+    return int(os.environ.get("DSIFT_DEVICE", "0"))
+
+
+def extract(img, cfg: SiftConfig | None = None, workers: int = 1) -> FeatureSet:
+    """FeatureSet detsift::extract(const GrayImage&, const SiftConfig&, int workers)
+    (io.hpp:17-19) on a B200.  `workers` keeps the reference's meaning — host
+    threads, 0 = all — and, as in the reference, never changes the output; the
+    device parallelism is the GPU's.  The device is default_device().  Each
+    host thread reuses one cached context per (device, config)."""
+    cfg = cfg or SiftConfig()
+    dev = default_device()
+    key = (dev, repr(cfg))
+    cached = getattr(_TLS, "ex", None)
+    if cached is None or cached[0] != key:
+        if cached is not None:
+            cached[1].close()
+        _TLS.ex = (key, Extractor(cfg, dev))
+    return _TLS.ex[1].extract(img)
 
 
 def quantize_u8(desc: np.ndarray) -> np.ndarray:

@@ -73,4 +73,26 @@ struct ScanState {
     unsigned long long cap;       // capacity of the compacted output
 };
 
+struct Counters {          // one small device block, cleared per batch
+    unsigned long long n_det;
+    unsigned long long n_ori;
+    unsigned err;
+    unsigned det_ticket;
+    unsigned ori_ticket;
+    unsigned n_slow;      // keypoints the certified fast descriptor path handed to the exact kernel
+    unsigned ref_ticket;
+    unsigned n_fixed;     // (keypoint, scale) pairs the stream kernel recomputed exactly in place
+    unsigned long long n_kp;   // refined keypoints (compacted)
+    unsigned emit_ticket;      // orientation fan-out tiles
+    unsigned desc_ticket;      // describe: dynamic keypoint claims
+};
+
+// Per-result device totals: every size group's counters are folded in here
+// (OR of the error words, sum of the exact-fallback counts).
+struct BatchTotals {
+    unsigned err;
+    unsigned pad;
+    unsigned long long slow;
+};
+
 }  // namespace dsift

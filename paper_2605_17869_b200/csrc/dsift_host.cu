@@ -188,49 +188,62 @@ struct DevBuf {
     }
 };
 
-struct Counters {          // one small device block, cleared per batch
-    unsigned long long n_det;
-    unsigned long long n_ori;
-    unsigned err;
-    unsigned det_ticket;
-    unsigned ori_ticket;
-    unsigned n_slow;      // keypoints the certified fast descriptor path handed to the exact kernel
-    unsigned ref_ticket;
-    unsigned n_fixed;     // (keypoint, scale) pairs the stream kernel recomputed exactly in place
-    unsigned long long n_kp;   // refined keypoints (compacted)
-    unsigned emit_ticket;      // orientation fan-out tiles
-    unsigned desc_ticket;      // describe: dynamic keypoint claims
+// One size group of a (possibly ragged) batch: images of one size, packed
+// contiguously on the device.
+struct Group {
+    int w = 0, h = 0;
+    std::vector<int> idx;          // batch indices, ascending
+    const float* dev = nullptr;    // [idx.size()][h][w] device images
+    long long cap_det = 0, cap_ori = 0;
+    long long stage_base = 0;      // first staging row (ragged batches)
+    long long offs_base = 0;       // first entry in the staging offsets
 };
 
 }  // namespace dsift
 
 using namespace dsift;
 
+// A batch result: output buffers, its completion event and the replay record.
+// A context owns a default result; dsift_result_create adds more so one
+// context can keep several batches in flight (dsift_result_select).
+struct dsift_result {
+    dsift_ctx* owner = nullptr;
+    DevBuf pub_kps, desc, desc_u8, offsets, totals, input, input_u8;
+    DevBuf stage_kps, stage_desc, stage_u8, stage_offs, map;   // ragged batches only
+    cudaEvent_t done = nullptr;        // the whole batch is written
+    cudaEvent_t input_free = nullptr;  // input[] no longer read by the batch's kernels
+    bool pending = false, ready = false;
+    int batch = 0;
+    int64_t total = 0;
+    unsigned long long slow = 0;
+    std::vector<int64_t> h_offsets;
+    std::vector<Group> groups;         // replayed on a capacity overflow (automatic capacity)
+    std::vector<long long> h_map;      // ragged batches: image -> (staging offsets entry, row base)
+    bool direct = true;                // one group in batch order: outputs written in place
+    int retries = 0;
+};
+
 struct dsift_ctx {
     int device = 0;
     cudaStream_t own_stream = nullptr;
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;   // host -> device input copies (overlap the previous batch)
     Cfg cfg;
     long long cap_override = 0;
+    double cap_scale = 1.0;   // automatic capacities grow x4 after an overflow (then the batch is replayed)
     Plan plan;
-    int batch = 0;            // images in the current pyramid / result
+    int batch = 0;            // images in the current pyramid
     PyramidDesc pyr{};
-    DevBuf det_aux, input_u8, ori_aux, match_in, match_scratch, match_best, geom_in, geom_scratch, geom_out;
-    DevBuf tma_maps;
-    DevBuf pyramid, input, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps,
-        pub_kps, desc, desc_u8, offsets, sort_keys, sort_idx, sort_temp, scratch, stage_kps, stage_out, trig, slow,
-        ref_states, keep;
+    DevBuf det_aux, ori_aux, match_in, match_scratch, match_best, geom_in, geom_scratch, geom_out;
+    DevBuf pyramid, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps, sort_work, scratch,
+        stage_kps, stage_out, trig, slow, ref_states, keep, stage_in;
     long long cap_det = 0, cap_ori = 0;
     long long launches = 0;
-    bool result_pending = false, result_ready = false;
-    int64_t total = 0;
-    std::vector<int64_t> h_offsets;
     int sm_count = 148;
-    cudaEvent_t done = nullptr;
     bool profiling = false;
     int force_exact = 0;
-    int desc_kernel = 2;   // 2 = stream (cell-lane) certified kernel, 1 = previous fast kernel
-    unsigned long long last_slow = 0;
+    dsift_result def;
+    dsift_result* cur = &def;
     cudaEvent_t stage_ev[6] = {};
 };
 
@@ -349,12 +362,6 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
     }
 }
 
-static long long auto_cap(dsift_ctx* c, double factor) {
-    if (c->cap_override > 0) return c->cap_override;
-    const long long px = (long long)c->plan.in_w * c->plan.in_h;
-    return std::max<long long>(4096, (long long)(px * factor));
-}
-
 static Counters* counters(dsift_ctx* c) { return c->counters.as<Counters>(); }
 
 static unsigned detect_tiles(const PyramidDesc& d, int* base, int* per_image) {
@@ -394,24 +401,17 @@ bool tma_encode_3d_f32(CUtensorMap* map, const float* base, uint64_t d0, uint64_
 }
 
 // K2's TMA maps: per octave, the DoG stack {w, h, batch * (s+2)}, box
-// {36, 34, s+2} (detect tile + halo, all DoG levels of one image).
-static unsigned build_dog_maps(dsift_ctx* c, const PyramidDesc& d) {
-    if (std::getenv("DSIFT_NO_TMA")) return 0u;
-    std::vector<CUtensorMap> maps((size_t)std::max(1, d.n_oct));
+// {36, 34, s+2} (detect tile + halo, all DoG levels of one image).  They go
+// into the kernel's __grid_constant__ parameter block.
+static unsigned build_dog_maps(const PyramidDesc& d, CUtensorMap* maps) {
     unsigned mask = 0;
     for (int o = 0; o < d.n_oct && o < 32; ++o) {
         const OctaveDesc& od = d.oct[o];
         if (od.tiles_x == 0) continue;
-        if (tma_encode_3d_f32(&maps[(size_t)o], od.dog, (uint64_t)od.w, (uint64_t)od.h,
+        if (tma_encode_3d_f32(&maps[o], od.dog, (uint64_t)od.w, (uint64_t)od.h,
                               (uint64_t)d.batch * (uint64_t)(d.s + 2), (uint64_t)od.pitch,
                               (uint64_t)od.level_stride, 36u, 34u, (uint32_t)(d.s + 2)))
             mask |= 1u << o;
-    }
-    if (mask) {
-        c->tma_maps.ensure(sizeof(CUtensorMap) * maps.size());
-        cuda_check(cudaMemcpyAsync(c->tma_maps.as<void>(), maps.data(), sizeof(CUtensorMap) * maps.size(),
-                                   cudaMemcpyHostToDevice, c->stream),
-                   "H2D tensor maps");
     }
     return mask;
 }
@@ -422,8 +422,7 @@ static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
     a.pyr = c->pyr;
     a.n_tiles = detect_tiles(c->pyr, a.oct_tile_base, &a.tiles_per_image);
     a.pre_gate = 0.5f * cf.contrast_threshold / cf.intervals;
-    a.tma_mask = build_dog_maps(c, a.pyr);
-    a.dog_maps = c->tma_maps.as<void>();
+    a.tma_mask = build_dog_maps(a.pyr, a.dog_maps);
     a.contrast_gate = double(cf.contrast_threshold) / cf.intervals;
     a.edge_r = cf.edge_ratio;
     a.max_iters = cf.max_refine_iters;
@@ -441,17 +440,16 @@ static void run_detect(dsift_ctx* c, int raw_mode, long long cap) {
     } else {
         a.cand_out = nullptr;
     }
-    {   // count -> scan -> emit scratch: masks, counts, offsets, CUB temp
+    {   // count -> scan -> emit scratch: masks, counts, offsets, scan state
         const size_t nt = std::max(1u, a.n_tiles);
         const size_t masks = (sizeof(unsigned) * 256 * nt + 255) & ~size_t(255);
         const size_t cnts = (sizeof(unsigned) * nt + 255) & ~size_t(255);
-        a.scan_temp_bytes = detect_scan_temp_bytes(a.n_tiles);
-        c->det_aux.ensure(masks + 2 * cnts + a.scan_temp_bytes + 256);
+        c->det_aux.ensure(masks + 2 * cnts + scan_state_bytes((long long)nt) + 256);
         char* base = c->det_aux.as<char>();
         a.hit_masks = reinterpret_cast<unsigned*>(base);
         a.tile_counts = reinterpret_cast<unsigned*>(base + masks);
         a.tile_offsets = reinterpret_cast<unsigned*>(base + masks + cnts);
-        a.scan_temp = base + masks + 2 * cnts;
+        a.scan_state = base + masks + 2 * cnts;
     }
     cuda_check(launch_detect(a, c->stream), "detect");
     c->launches += 3;
@@ -590,8 +588,8 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
         ++c->launches;
         return;
     }
-    // certified fast path over every keypoint, then the exact kernel over the
-    // (rare) keypoints whose certificate failed
+    // certified stream kernel over every keypoint, then the exact kernel over
+    // the (rare) keypoints whose certificate failed
     const long long cap_n = n_host >= 0 ? n_host : c->cap_ori;
     c->slow.ensure(sizeof(int) * (size_t)std::max<long long>(1, cap_n));
     Counters* ctr = counters(c);
@@ -602,11 +600,7 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
     a.slow_cap = cap_n;
     a.force_slow = c->force_exact;
     DescArgs af = a;
-    af.chunk_rows = 6;   // kFastChunk: the fast kernel's sample ring holds chunk + 2 rows
-    {
-        const char* hp = std::getenv("DSIFT_HOT_PAIR");
-        af.hot_pair = hp ? std::atoi(hp) : 1;
-    }
+    af.chunk_rows = 6;   // the stream kernel's in-place exact recompute works in 6-row chunks
     {
         double fmax = 0.0;
         for (double f : fs) fmax = std::max(fmax, f);
@@ -614,23 +608,14 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
     }
     const size_t smem_exact = describe_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
     if (smem_exact > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
-    if (c->desc_kernel == 1) {   // previous certified kernel (kept for A/B measurements)
-        const size_t smem_fast = describe_fast_smem_bytes(a.max_axis, af.chunk_rows, a.n_dsp);
-        if (smem_fast > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
-        const int per_sm = std::max(1, describe_blocks_per_sm(smem_fast));
-        int grid = c->sm_count * per_sm;
-        if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
-        cuda_check(launch_describe_fast(af, grid, c->stream), "describe fast");
-    } else {
-        const size_t smem_s = std::max(describe_stream_smem_bytes(af.max_span, a.n_dsp),
-                                       describe_stream_exact_smem_bytes(af.max_axis, af.chunk_rows, a.n_dsp));
-        if (smem_s > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
-        const int per_sm = std::max(1, describe_stream_blocks_per_sm(smem_s));
-        int grid = c->sm_count * per_sm;
-        if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
-        cuda_check(cudaMemsetAsync(af.ticket, 0, sizeof(unsigned), c->stream), "memset ticket");
-        cuda_check(launch_describe_stream(af, grid, c->stream), "describe stream");
-    }
+    const size_t smem_s = std::max(describe_stream_smem_bytes(af.max_span, a.n_dsp),
+                                   describe_stream_exact_smem_bytes(af.max_axis, af.chunk_rows, a.n_dsp));
+    if (smem_s > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
+    const int per_sm = std::max(1, describe_stream_blocks_per_sm(smem_s));
+    int grid = c->sm_count * per_sm;
+    if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
+    cuda_check(cudaMemsetAsync(af.ticket, 0, sizeof(unsigned), c->stream), "memset ticket");
+    cuda_check(launch_describe_stream(af, grid, c->stream), "describe stream");
     DescArgs b = a;
     b.slow_list = c->slow.as<int>();
     b.n_slow = &ctr->n_slow;
@@ -648,98 +633,262 @@ static void reset_counters(dsift_ctx* c) {
     cuda_check(cudaMemsetAsync(c->counters.as<void>(), 0, sizeof(Counters), c->stream), "memset");
 }
 
+// Stage-level input (one image): host images go through the context's own
+// staging buffer.
 static const float* stage_input(dsift_ctx* c, const float* images, int n, int w, int h, int flags) {
     if (flags & DSIFT_INPUT_DEVICE) return images;
     const size_t bytes = sizeof(float) * (size_t)n * w * h;
-    c->input.ensure(bytes);
-    cuda_check(cudaMemcpyAsync(c->input.as<void>(), images, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
-    return c->input.as<float>();
+    c->stage_in.ensure(bytes);
+    cuda_check(cudaMemcpyAsync(c->stage_in.as<void>(), images, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+    return c->stage_in.as<float>();
+}
+
+static void ensure_events(dsift_result* r) {
+    if (!r->done) cuda_check(cudaEventCreateWithFlags(&r->done, cudaEventDisableTiming), "event");
+    if (!r->input_free) cuda_check(cudaEventCreateWithFlags(&r->input_free, cudaEventDisableTiming), "event");
+}
+
+// Per-group capacities (automatic: from the input size, x cap_scale after an
+// overflow; or the caller's dsift_set_capacity).
+static void group_caps(dsift_ctx* c, Group& g) {
+    const long long n = (long long)g.idx.size();
+    auto cap = [&](double factor) -> long long {
+        if (c->cap_override > 0) return c->cap_override;
+        const double px = (double)g.w * g.h * c->cap_scale;
+        return std::max<long long>((long long)(4096 * c->cap_scale), (long long)(px * factor));
+    };
+    g.cap_det = n * cap(1.0 / 12.0);   // candidates (extrema)
+    g.cap_ori = n * cap(1.0 / 16.0);   // oriented keypoints
+}
+
+// The pipeline for one size group: K1 pyramid -> K2/K3 detect + refine -> K4
+// orientation + fan-out -> K7 canonical sort -> K5/K6 descriptors, all on the
+// context stream.  Keypoints / descriptors / per-image offsets go to the given
+// output pointers.
+static void run_group(dsift_ctx* c, dsift_result* r, const Group& g, dsift_keypoint* out_kps, float* out_desc,
+                      unsigned char* out_u8, long long* out_offs) {
+    const int n = (int)g.idx.size();
+    c->plan = make_plan(c->cfg, g.w, g.h);
+    c->batch = n;
+    build_pyramid_desc(c);
+    reset_counters(c);
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[0], c->stream), "event");
+    launch_pyramid(c, g.dev);
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[1], c->stream), "event");
+    c->cap_det = g.cap_det;
+    c->cap_ori = g.cap_ori;
+    run_detect(c, 1, c->cap_det);   // K2: compacted extrema
+    run_refine(c, c->cap_det);      // K3: one thread per candidate
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[2], c->stream), "event");
+    c->ori_kps.ensure(sizeof(DevKeypoint) * (size_t)c->cap_ori);
+    run_orient(c, c->det_kps.as<DevKeypoint>(), -1, c->cap_det, c->ori_kps.as<DevKeypoint>(), c->cap_ori, nullptr,
+               orient_depth(c->cfg.c, nullptr, c->plan));
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[3], c->stream), "event");
+    // canonical order (K7, hand-written bucket sort over the actual count)
+    const long long cap = c->cap_ori;
+    SortGeom sg;
+    sg.s = c->plan.s;
+    sg.rows = c->plan.in_h;
+    sg.per_image = (unsigned)(c->plan.n_oct * c->plan.s * c->plan.in_h);
+    c->sort_work.ensure(sort_work_bytes(cap, sg, n));
+    c->sorted_kps.ensure(sizeof(DevKeypoint) * (size_t)cap);
+    Counters* ctr = counters(c);
+    cuda_check(launch_canonical_sort(c->ori_kps.as<DevKeypoint>(), &ctr->n_ori, cap, sg, c->sort_work.as<void>(),
+                                     c->sorted_kps.as<DevKeypoint>(), out_kps, n, out_offs, c->stream, &c->launches),
+               "sort");
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[4], c->stream), "event");
+    const double smax = c->cfg.c.sigma0 * std::pow(2.0, (c->cfg.c.intervals + 0.5) / c->cfg.c.intervals) * 1.001;
+    run_describe(c, c->sorted_kps.as<DevKeypoint>(), -1, out_desc, out_u8, 0, 0.0, smax, &ctr->n_ori);
+    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[5], c->stream), "event");
+    cuda_check(launch_fold_totals(ctr, r->totals.as<BatchTotals>(), c->stream), "fold");
+    ++c->launches;
+}
+
+// Runs every group of r (first run or a capacity replay) and, for a ragged
+// batch, gathers the groups' staged outputs into batch order.
+static void run_batch(dsift_ctx* c, dsift_result* r) {
+    set_device(c);
+    ensure_counters(c);
+    r->pending = r->ready = false;
+    r->total = 0;
+    long long rows = 0, offs = 0;
+    size_t pyr_max = 0;
+    for (Group& g : r->groups) {
+        group_caps(c, g);
+        g.stage_base = rows;
+        g.offs_base = offs;
+        rows += g.cap_ori;
+        offs += (long long)g.idx.size() + 1;
+        const Plan p = make_plan(c->cfg, g.w, g.h);
+        size_t bytes = 0;
+        for (int o = 0; o < p.n_oct; ++o) {
+            const size_t lv = sizeof(float) * (size_t)p.pitch[o] * p.oh[o] * g.idx.size();
+            bytes += ((lv * (p.s + 3) + 255) & ~size_t(255)) + ((lv * (p.s + 2) + 255) & ~size_t(255));
+        }
+        pyr_max = std::max(pyr_max, bytes);
+    }
+    c->pyramid.ensure(pyr_max);   // one allocation for every group of the batch
+    r->totals.ensure(sizeof(BatchTotals));
+    cuda_check(cudaMemsetAsync(r->totals.as<void>(), 0, sizeof(BatchTotals), c->stream), "memset");
+    r->offsets.ensure(sizeof(long long) * (size_t)(r->batch + 1));
+    if (r->direct) {
+        const Group& g = r->groups[0];
+        r->pub_kps.ensure(sizeof(dsift_keypoint) * (size_t)g.cap_ori);
+        r->desc.ensure(sizeof(float) * kDescDim * (size_t)g.cap_ori);
+        r->desc_u8.ensure((size_t)kDescDim * (size_t)g.cap_ori);
+        run_group(c, r, g, r->pub_kps.as<dsift_keypoint>(), r->desc.as<float>(), r->desc_u8.as<unsigned char>(),
+                  r->offsets.as<long long>());
+        cuda_check(cudaEventRecord(r->input_free, c->stream), "event");
+    } else {
+        r->stage_kps.ensure(sizeof(dsift_keypoint) * (size_t)rows);
+        r->stage_desc.ensure(sizeof(float) * kDescDim * (size_t)rows);
+        r->stage_u8.ensure((size_t)kDescDim * (size_t)rows);
+        r->stage_offs.ensure(sizeof(long long) * (size_t)offs);
+        for (const Group& g : r->groups)
+            run_group(c, r, g, r->stage_kps.as<dsift_keypoint>() + g.stage_base,
+                      r->stage_desc.as<float>() + g.stage_base * kDescDim,
+                      r->stage_u8.as<unsigned char>() + g.stage_base * kDescDim,
+                      r->stage_offs.as<long long>() + g.offs_base);
+        cuda_check(cudaEventRecord(r->input_free, c->stream), "event");
+        // batch index -> (staging offsets entry, staging row base)
+        std::vector<long long>& map = r->h_map;
+        map.assign(2 * (size_t)r->batch, 0);
+        for (const Group& g : r->groups)
+            for (size_t j = 0; j < g.idx.size(); ++j) {
+                map[2 * (size_t)g.idx[j]] = g.offs_base + (long long)j;
+                map[2 * (size_t)g.idx[j] + 1] = g.stage_base;
+            }
+        r->map.ensure(sizeof(long long) * map.size());
+        cuda_check(cudaMemcpyAsync(r->map.as<void>(), map.data(), sizeof(long long) * map.size(),
+                                   cudaMemcpyHostToDevice, c->stream), "H2D");
+        r->pub_kps.ensure(sizeof(dsift_keypoint) * (size_t)rows);
+        r->desc.ensure(sizeof(float) * kDescDim * (size_t)rows);
+        r->desc_u8.ensure((size_t)kDescDim * (size_t)rows);
+        cuda_check(launch_ragged_gather(r->map.as<long long>(), r->stage_offs.as<long long>(), r->batch,
+                                        r->stage_kps.as<dsift_keypoint>(), r->stage_desc.as<float>(),
+                                        r->stage_u8.as<unsigned char>(), r->offsets.as<long long>(),
+                                        r->pub_kps.as<dsift_keypoint>(), r->desc.as<float>(),
+                                        r->desc_u8.as<unsigned char>(), c->stream),
+                   "ragged gather");
+        c->launches += 2;
+    }
+    cuda_check(cudaEventRecord(r->done, c->stream), "event");
+    r->pending = true;
+}
+
+// Extraction entry: validates every image (reference messages, before any
+// work is enqueued), groups the batch by image size (first-occurrence
+// order), stages host / scattered inputs contiguously per group and runs it.
+static void extract_images(dsift_ctx* c, const dsift_image* imgs, int n, int flags, dsift_result* r) {
+    if (!r) r = c->cur;
+    r->pending = r->ready = false;   // a failed submit leaves no stale result behind
+    r->total = 0;
+    r->batch = 0;
+    r->groups.clear();
+    if (n <= 0) invalid("extract: batch must contain at least one image");
+    if (!imgs) invalid("extract: null image pointer");
+    set_device(c);
+    ensure_events(r);
+    std::vector<Group> groups;
+    for (int i = 0; i < n; ++i) {
+        if (!imgs[i].data) invalid("extract: null image pointer");
+        (void)make_plan(c->cfg, imgs[i].width, imgs[i].height);   // throws the reference's message
+        auto it = std::find_if(groups.begin(), groups.end(),
+                               [&](const Group& g) { return g.w == imgs[i].width && g.h == imgs[i].height; });
+        if (it == groups.end()) {
+            groups.emplace_back();
+            groups.back().w = imgs[i].width;
+            groups.back().h = imgs[i].height;
+            it = groups.end() - 1;
+        }
+        it->idx.push_back(i);
+    }
+    const bool device = (flags & DSIFT_INPUT_DEVICE) != 0;
+    bool contiguous = groups.size() == 1;
+    if (contiguous) {
+        const size_t px = (size_t)groups[0].w * groups[0].h;
+        for (int i = 1; i < n && contiguous; ++i) contiguous = imgs[i].data == imgs[0].data + (size_t)i * px;
+    }
+    r->direct = groups.size() == 1;
+    if (device && contiguous) {
+        groups[0].dev = imgs[0].data;   // zero-copy: the caller's batch (kept valid until result_sync)
+    } else {
+        size_t total_px = 0;
+        for (const Group& g : groups) total_px += (size_t)g.w * g.h * g.idx.size();
+        r->input.ensure(sizeof(float) * total_px);
+        cudaStream_t cs = device ? c->stream : c->copy_stream;
+        if (!device) cuda_check(cudaStreamWaitEvent(cs, r->input_free, 0), "wait");   // previous batch done with input[]
+        float* dst = r->input.as<float>();
+        for (Group& g : groups) {
+            g.dev = dst;
+            const size_t px = (size_t)g.w * g.h;
+            for (int i : g.idx) {
+                cuda_check(cudaMemcpyAsync(dst, imgs[i].data, sizeof(float) * px,
+                                           device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, cs),
+                           "copy input");
+                dst += px;
+            }
+        }
+        if (!device) {
+            cuda_check(cudaEventRecord(r->input_free, cs), "event");   // reused as "input staged"
+            cuda_check(cudaStreamWaitEvent(c->stream, r->input_free, 0), "wait");
+        }
+    }
+    r->batch = n;
+    r->retries = 0;
+    r->groups = std::move(groups);
+    run_batch(c, r);
 }
 
 static void extract_batch(dsift_ctx* c, const float* images, int n, int w, int h, int flags) {
     if (n <= 0) invalid("extract: batch must contain at least one image");
     if (!images) invalid("extract: null image pointer");
-    set_device(c);
-    c->plan = make_plan(c->cfg, w, h);
-    c->batch = n;
-    build_pyramid_desc(c);
-    ensure_counters(c);
-    reset_counters(c);
-    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[0], c->stream), "event");
-    const float* dev_in = stage_input(c, images, n, w, h, flags);
-    launch_pyramid(c, dev_in);
-    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[1], c->stream), "event");
-
-    c->cap_det = (long long)n * auto_cap(c, 1.0 / 12.0);   // candidates (extrema) per batch
-    c->cap_ori = (long long)n * auto_cap(c, 1.0 / 16.0);
-    run_detect(c, 1, c->cap_det);                        // K2: compacted extrema
-    run_refine(c, c->cap_det);                           // K3: one thread per candidate
-    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[2], c->stream), "event");
-    c->ori_kps.ensure(sizeof(DevKeypoint) * (size_t)c->cap_ori);
-    run_orient(c, c->det_kps.as<DevKeypoint>(), -1, c->cap_det, c->ori_kps.as<DevKeypoint>(), c->cap_ori,
-               nullptr, orient_depth(c->cfg.c, nullptr, c->plan));
-    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[3], c->stream), "event");
-
-    // canonical order
-    const long long cap = c->cap_ori;
-    c->sort_keys.ensure(sizeof(unsigned long long) * 2 * (size_t)cap);
-    c->sort_idx.ensure(sizeof(int) * 2 * (size_t)cap);
-    const size_t tb = sort_temp_bytes(cap);
-    c->sort_temp.ensure(tb);
-    SortBuffers sb;
-    sb.keys_a = c->sort_keys.as<unsigned long long>();
-    sb.keys_b = sb.keys_a + cap;
-    sb.idx_a = c->sort_idx.as<int>();
-    sb.idx_b = sb.idx_a + cap;
-    sb.temp = c->sort_temp.as<void>();
-    sb.temp_bytes = tb;
-    c->sorted_kps.ensure(sizeof(DevKeypoint) * (size_t)cap);
-    c->pub_kps.ensure(sizeof(dsift_keypoint) * (size_t)cap);
-    c->offsets.ensure(sizeof(long long) * (size_t)(n + 1));
-    Counters* ctr = counters(c);
-    cuda_check(launch_canonical_sort(c->ori_kps.as<DevKeypoint>(), &ctr->n_ori, cap, sb,
-                                     c->sorted_kps.as<DevKeypoint>(), c->pub_kps.as<dsift_keypoint>(), n,
-                                     c->offsets.as<long long>(), c->stream, &c->launches),
-               "sort");
-    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[4], c->stream), "event");
-    c->desc.ensure(sizeof(float) * kDescDim * (size_t)cap);
-    c->desc_u8.ensure((size_t)kDescDim * (size_t)cap);
-    const double smax = c->cfg.c.sigma0 * std::pow(2.0, (c->cfg.c.intervals + 0.5) / c->cfg.c.intervals) * 1.001;
-    run_describe(c, c->sorted_kps.as<DevKeypoint>(), -1, c->desc.as<float>(), c->desc_u8.as<unsigned char>(), 0,
-                 0.0, smax, &ctr->n_ori);
-    if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[5], c->stream), "event");
-    cuda_check(cudaEventRecord(c->done, c->stream), "event");
-    c->result_pending = true;
-    c->result_ready = false;
+    std::vector<dsift_image> v((size_t)n);
+    for (int i = 0; i < n; ++i) v[(size_t)i] = dsift_image{images + (size_t)i * (size_t)std::max(0, w) * std::max(0, h), w, h};
+    extract_images(c, v.data(), n, flags, nullptr);
 }
 
-static void result_sync(dsift_ctx* c) {
-    if (!c->result_pending && !c->result_ready) throw Error{DSIFT_ESTATE, "result: no extract issued"};
-    if (c->result_ready) return;
+static void result_sync(dsift_ctx* c, dsift_result* r) {
+    if (!r->pending && !r->ready) throw Error{DSIFT_ESTATE, "result: no extract issued"};
+    if (r->ready) return;
     set_device(c);
-    cuda_check(cudaEventSynchronize(c->done), "sync");
-    cuda_check(cudaGetLastError(), "async kernel error");
-    Counters h{};
-    cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(Counters), cudaMemcpyDeviceToHost), "D2H");
-    c->result_pending = false;
-    if (h.err & kErrHistogramRange)   // same text as detsum.cpp:140 (std::out_of_range)
-        throw Error{DSIFT_ERANGE, "histogram: bin index out of range"};
-    if (h.err) {
-        std::string m = "device work list overflow:";
-        if (h.err & kErrKeypointCapacity) m += " keypoints";
-        if (h.err & kErrOrientedCapacity) m += " oriented keypoints";
-        if (h.err & kErrCandidateCapacity) m += " candidates";
-        if (h.err & kErrDescriptorLattice) m += " descriptor lattice";
-        m += " (raise dsift_set_capacity)";
-        throw Error{DSIFT_ECAPACITY, m};
+    for (;;) {
+        cuda_check(cudaEventSynchronize(r->done), "sync");
+        cuda_check(cudaGetLastError(), "async kernel error");
+        BatchTotals t{};
+        cuda_check(cudaMemcpy(&t, r->totals.as<void>(), sizeof(t), cudaMemcpyDeviceToHost), "D2H");
+        r->pending = false;
+        if (t.err & kErrHistogramRange)   // same text as detsum.cpp:140 (std::out_of_range)
+            throw Error{DSIFT_ERANGE, "histogram: bin index out of range"};
+        const unsigned list_err = kErrKeypointCapacity | kErrOrientedCapacity | kErrCandidateCapacity;
+        if ((t.err & list_err) && c->cap_override == 0 && r->retries < 4) {
+            // automatic capacity overflowed: grow it and replay the batch (the
+            // inputs are still on the device), so the caller still gets every keypoint
+            c->cap_scale *= 4.0;
+            ++r->retries;
+            run_batch(c, r);
+            continue;
+        }
+        if (t.err) {
+            std::string m = "device work list overflow:";
+            if (t.err & kErrKeypointCapacity) m += " keypoints";
+            if (t.err & kErrOrientedCapacity) m += " oriented keypoints";
+            if (t.err & kErrCandidateCapacity) m += " candidates";
+            if (t.err & kErrDescriptorLattice) m += " descriptor lattice";
+            m += " (raise dsift_set_capacity)";
+            throw Error{DSIFT_ECAPACITY, m};
+        }
+        r->slow = t.slow;
+        break;
     }
-    c->total = (int64_t)h.n_ori;
-    c->last_slow = (unsigned long long)h.n_slow + h.n_fixed;
-    c->h_offsets.assign(c->batch + 1, 0);
-    cuda_check(cudaMemcpy(c->h_offsets.data(), c->offsets.as<void>(), sizeof(long long) * (c->batch + 1),
+    r->h_offsets.assign((size_t)r->batch + 1, 0);
+    cuda_check(cudaMemcpy(r->h_offsets.data(), r->offsets.as<void>(), sizeof(long long) * (r->batch + 1),
                           cudaMemcpyDeviceToHost), "D2H");
-    c->result_ready = true;
+    r->total = r->h_offsets[(size_t)r->batch];
+    r->ready = true;
 }
+
+static void result_sync(dsift_ctx* c) { result_sync(c, c->cur); }
 
 // ---- SHA-256 / DSF1 (sha256.cpp, core.cpp:153-196), host side -------------------------
 static void sha256(const uint8_t* data, size_t n, char* hex) {
@@ -847,8 +996,10 @@ int dsift_create(int device, const dsift_config* cfg, dsift_ctx** out) {
         if (device < 0 || device >= ndev) throw Error{DSIFT_ECUDA, "create: no such CUDA device"};
         set_device(ctx.get());
         cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+        cuda_check(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking), "stream");
         ctx->stream = ctx->own_stream;
-        cuda_check(cudaEventCreateWithFlags(&ctx->done, cudaEventDisableTiming), "event");
+        ctx->def.owner = ctx.get();
+        ensure_events(&ctx->def);
         cuda_check(cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device), "attr");
         ensure_counters(ctx.get());
         *out = ctx.release();
@@ -859,9 +1010,12 @@ void dsift_destroy(dsift_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
-    if (c->done) cudaEventDestroy(c->done);
+    cudaStreamSynchronize(c->copy_stream);
+    if (c->def.done) cudaEventDestroy(c->def.done);
+    if (c->def.input_free) cudaEventDestroy(c->def.input_free);
     for (auto& e : c->stage_ev)
         if (e) cudaEventDestroy(e);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
 }
@@ -890,6 +1044,52 @@ int dsift_extract_batch(dsift_ctx* c, const float* images, int n, int w, int h, 
 
 int dsift_extract(dsift_ctx* c, const float* image, int w, int h, int flags) {
     return dsift_extract_batch(c, image, 1, w, h, flags);
+}
+
+int dsift_extract_images(dsift_ctx* c, const dsift_image* images, int n, int flags) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (n > 65535) invalid("extract: at most 65535 images per call");
+        extract_images(c, images, n, flags, nullptr);
+    });
+}
+
+int dsift_result_create(dsift_ctx* c, dsift_result** out) {
+    return guard([&] {
+        if (!c || !out) invalid("null argument");
+        set_device(c);
+        auto r = std::make_unique<dsift_result>();
+        r->owner = c;
+        ensure_events(r.get());
+        *out = r.release();
+    });
+}
+
+void dsift_result_destroy(dsift_result* r) {
+    if (!r) return;
+    dsift_ctx* c = r->owner;
+    if (c && r == &c->def) return;   // the context's own result lives with the context
+    if (c) {
+        cudaSetDevice(c->device);
+        if (c->cur == r) c->cur = &c->def;
+    }
+    if (r->done) {
+        cudaEventSynchronize(r->done);
+        cudaEventDestroy(r->done);
+    }
+    if (r->input_free) {
+        cudaEventSynchronize(r->input_free);
+        cudaEventDestroy(r->input_free);
+    }
+    delete r;
+}
+
+int dsift_result_select(dsift_ctx* c, dsift_result* r) {
+    return guard([&] {
+        if (!c) invalid("null context");
+        if (r && r->owner != c) invalid("result: belongs to another context");
+        c->cur = r ? r : &c->def;
+    });
 }
 
 // ---- matching (match.cpp:77-119) --------------------------------------------
@@ -1105,20 +1305,19 @@ int dsift_corner_error(const double* h_est, const double* h_gt, double width, do
 }
 
 // ---- image ingest (io.cpp:49-81) ---------------------------------------------
-static const float* ingest_to_input(dsift_ctx* c, const uint8_t* pixels, long long n_px, int channels, int flags) {
+static void ingest(dsift_ctx* c, const uint8_t* pixels, long long n_px, int channels, int flags, DevBuf& bytes_buf,
+                   float* dev_out) {
     if (channels != 1 && channels != 3) invalid("ingest: channels must be 1 (P5) or 3 (P6)");
     if (!pixels) invalid("extract: null image pointer");
     const size_t bytes = (size_t)n_px * channels;
     const unsigned char* dev_bytes = reinterpret_cast<const unsigned char*>(pixels);
     if (!(flags & DSIFT_INPUT_DEVICE)) {
-        c->input_u8.ensure(bytes);
-        cuda_check(cudaMemcpyAsync(c->input_u8.as<void>(), pixels, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
-        dev_bytes = c->input_u8.as<unsigned char>();
+        bytes_buf.ensure(bytes);
+        cuda_check(cudaMemcpyAsync(bytes_buf.as<void>(), pixels, bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+        dev_bytes = bytes_buf.as<unsigned char>();
     }
-    c->input.ensure(sizeof(float) * (size_t)n_px);
-    cuda_check(launch_ingest_u8(dev_bytes, n_px, channels, c->input.as<float>(), c->stream), "ingest");
+    cuda_check(launch_ingest_u8(dev_bytes, n_px, channels, dev_out, c->stream), "ingest");
     ++c->launches;
-    return c->input.as<float>();
 }
 
 int dsift_extract_batch_u8(dsift_ctx* c, const uint8_t* pixels, int n, int w, int h, int channels, int flags) {
@@ -1127,8 +1326,14 @@ int dsift_extract_batch_u8(dsift_ctx* c, const uint8_t* pixels, int n, int w, in
         if (n <= 0) invalid("extract: batch must contain at least one image");
         if (w <= 0 || h <= 0) invalid("build_scale_space: empty image");
         set_device(c);
-        const float* dev = ingest_to_input(c, pixels, (long long)n * w * h, channels, flags);
-        extract_batch(c, dev, n, w, h, DSIFT_INPUT_DEVICE);
+        dsift_result* r = c->cur;
+        r->pending = r->ready = false;
+        const long long n_px = (long long)n * w * h;
+        ensure_events(r);
+        cuda_check(cudaStreamWaitEvent(c->stream, r->input_free, 0), "wait");
+        r->input.ensure(sizeof(float) * (size_t)n_px);
+        ingest(c, pixels, n_px, channels, flags, r->input_u8, r->input.as<float>());
+        extract_batch(c, r->input.as<float>(), n, w, h, DSIFT_INPUT_DEVICE);
     });
 }
 
@@ -1137,9 +1342,7 @@ int dsift_ingest_u8(dsift_ctx* c, const uint8_t* pixels, int64_t n_px, int chann
         if (!c) invalid("null context");
         if (!dev_out) invalid("ingest: null output");
         set_device(c);
-        const float* dev = ingest_to_input(c, pixels, n_px, channels, flags);
-        cuda_check(cudaMemcpyAsync(dev_out, dev, sizeof(float) * (size_t)n_px, cudaMemcpyDeviceToDevice, c->stream),
-                   "D2D");
+        ingest(c, pixels, n_px, channels, flags, c->scratch, dev_out);
         cuda_check(cudaStreamSynchronize(c->stream), "sync");
     });
 }
@@ -1216,7 +1419,7 @@ int dsift_result_sync(dsift_ctx* c, int64_t* total) {
     return guard([&] {
         if (!c) invalid("null context");
         result_sync(c);
-        if (total) *total = c->total;
+        if (total) *total = c->cur->total;
     });
 }
 
@@ -1224,9 +1427,10 @@ int dsift_result_range(dsift_ctx* c, int image, int64_t* begin, int64_t* count) 
     return guard([&] {
         if (!c) invalid("null context");
         result_sync(c);
-        if (image < 0 || image >= c->batch) invalid("result: image index out of range");
-        if (begin) *begin = c->h_offsets[image];
-        if (count) *count = c->h_offsets[image + 1] - c->h_offsets[image];
+        const dsift_result* r = c->cur;
+        if (image < 0 || image >= r->batch) invalid("result: image index out of range");
+        if (begin) *begin = r->h_offsets[image];
+        if (count) *count = r->h_offsets[image + 1] - r->h_offsets[image];
     });
 }
 
@@ -1234,14 +1438,15 @@ int dsift_result_copy(dsift_ctx* c, dsift_keypoint* kps, float* desc, uint8_t* d
     return guard([&] {
         if (!c) invalid("null context");
         result_sync(c);
-        const size_t n = (size_t)c->total;
+        const dsift_result* r = c->cur;
+        const size_t n = (size_t)r->total;
         if (kps && n)
-            cuda_check(cudaMemcpy(kps, c->pub_kps.as<void>(), n * sizeof(dsift_keypoint), cudaMemcpyDeviceToHost), "D2H");
+            cuda_check(cudaMemcpy(kps, r->pub_kps.as<void>(), n * sizeof(dsift_keypoint), cudaMemcpyDeviceToHost), "D2H");
         if (desc && n)
-            cuda_check(cudaMemcpy(desc, c->desc.as<void>(), n * kDescDim * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
+            cuda_check(cudaMemcpy(desc, r->desc.as<void>(), n * kDescDim * sizeof(float), cudaMemcpyDeviceToHost), "D2H");
         if (desc_u8 && n)
-            cuda_check(cudaMemcpy(desc_u8, c->desc_u8.as<void>(), n * kDescDim, cudaMemcpyDeviceToHost), "D2H");
-        if (offsets) std::memcpy(offsets, c->h_offsets.data(), sizeof(int64_t) * (c->batch + 1));
+            cuda_check(cudaMemcpy(desc_u8, r->desc_u8.as<void>(), n * kDescDim, cudaMemcpyDeviceToHost), "D2H");
+        if (offsets) std::memcpy(offsets, r->h_offsets.data(), sizeof(int64_t) * (r->batch + 1));
     });
 }
 
@@ -1249,11 +1454,12 @@ int dsift_result_device(dsift_ctx* c, const dsift_keypoint** kps, const float** 
                         const int64_t** offsets) {
     return guard([&] {
         if (!c) invalid("null context");
-        if (!c->result_pending && !c->result_ready) throw Error{DSIFT_ESTATE, "result: no extract issued"};
-        if (kps) *kps = c->pub_kps.as<dsift_keypoint>();
-        if (desc) *desc = c->desc.as<float>();
-        if (desc_u8) *desc_u8 = c->desc_u8.as<uint8_t>();
-        if (offsets) *offsets = reinterpret_cast<const int64_t*>(c->offsets.as<long long>());
+        const dsift_result* r = c->cur;
+        if (!r->pending && !r->ready) throw Error{DSIFT_ESTATE, "result: no extract issued"};
+        if (kps) *kps = r->pub_kps.as<dsift_keypoint>();
+        if (desc) *desc = r->desc.as<float>();
+        if (desc_u8) *desc_u8 = r->desc_u8.as<uint8_t>();
+        if (offsets) *offsets = reinterpret_cast<const int64_t*>(r->offsets.as<long long>());
     });
 }
 
@@ -1267,23 +1473,24 @@ int dsift_export_dlpack(dsift_ctx* c, int which, void** out) {
     return guard([&] {
         if (!c || !out) invalid("null argument");
         result_sync(c);
+        dsift_result* r = c->cur;
         auto* h = new DlHolder();
         DLTensor& t = h->t.dl_tensor;
         t.device = {kDLCUDA, c->device};
         t.ndim = 2;
         t.strides = nullptr;
         t.byte_offset = 0;
-        h->shape[0] = c->total;
+        h->shape[0] = r->total;
         if (which == DSIFT_EXPORT_KEYPOINTS) {
-            h->keep = c->pub_kps.ptr;
+            h->keep = r->pub_kps.ptr;
             h->shape[1] = 7;
             t.dtype = {kDLFloat, 32, 1};
         } else if (which == DSIFT_EXPORT_DESC_F32) {
-            h->keep = c->desc.ptr;
+            h->keep = r->desc.ptr;
             h->shape[1] = kDescDim;
             t.dtype = {kDLFloat, 32, 1};
         } else if (which == DSIFT_EXPORT_DESC_U8) {
-            h->keep = c->desc_u8.ptr;
+            h->keep = r->desc_u8.ptr;
             h->shape[1] = kDescDim;
             t.dtype = {kDLUInt, 8, 1};
         } else {
@@ -1302,16 +1509,17 @@ int dsift_result_sha256(dsift_ctx* c, int image, char hex65[65]) {
     return guard([&] {
         if (!c) invalid("null context");
         result_sync(c);
-        if (image < 0 || image >= c->batch) invalid("result: image index out of range");
-        const int64_t b = c->h_offsets[image], n = c->h_offsets[image + 1] - b;
+        const dsift_result* r = c->cur;
+        if (image < 0 || image >= r->batch) invalid("result: image index out of range");
+        const int64_t b = r->h_offsets[image], n = r->h_offsets[image + 1] - b;
         std::vector<uint8_t> buf(16 + (size_t)n * (28 + kDescDim * 4));
         const uint32_t hdr[3] = {1u, (uint32_t)n, (uint32_t)kDescDim};
         std::memcpy(buf.data(), "DSF1", 4);
         std::memcpy(buf.data() + 4, hdr, 12);
         if (n) {
-            cuda_check(cudaMemcpy(buf.data() + 16, c->pub_kps.as<dsift_keypoint>() + b, (size_t)n * 28,
+            cuda_check(cudaMemcpy(buf.data() + 16, r->pub_kps.as<dsift_keypoint>() + b, (size_t)n * 28,
                                   cudaMemcpyDeviceToHost), "D2H");
-            cuda_check(cudaMemcpy(buf.data() + 16 + (size_t)n * 28, c->desc.as<float>() + b * kDescDim,
+            cuda_check(cudaMemcpy(buf.data() + 16 + (size_t)n * 28, r->desc.as<float>() + b * kDescDim,
                                   (size_t)n * kDescDim * 4, cudaMemcpyDeviceToHost), "D2H");
         }
         sha256(buf.data(), buf.size(), hex65);
@@ -1331,7 +1539,6 @@ int dsift_build_scale_space(dsift_ctx* c, const float* image, int w, int h, int 
         const float* dev_in = stage_input(c, image, 1, w, h, flags);
         launch_pyramid(c, dev_in);
         cuda_check(cudaStreamSynchronize(c->stream), "sync");
-        c->result_pending = c->result_ready = false;
     });
 }
 
@@ -1368,7 +1575,6 @@ int dsift_load_scale_space(dsift_ctx* c, int n_oct, int upsampled, const int32_t
                 cuda_check(cudaMemcpy2D(od.dog + i * od.level_stride, sizeof(float) * od.pitch, dog[o * (s + 2) + i],
                                         sizeof(float) * od.w, sizeof(float) * od.w, od.h, cudaMemcpyHostToDevice), "H2D");
         }
-        c->result_pending = c->result_ready = false;
     });
 }
 
@@ -1483,6 +1689,17 @@ int dsift_detect(dsift_ctx* c, dsift_keypoint* out, int64_t cap, int64_t* n) {
     });
 }
 
+// Stage-level calls: the device error word as the reference's exceptions
+// (NaN pixel -> std::out_of_range, detsum.cpp:138-141) or a loud overflow.
+static Counters check_stage_errors(dsift_ctx* c) {
+    Counters h{};
+    cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+    if (h.err & kErrHistogramRange) throw Error{DSIFT_ERANGE, "histogram: bin index out of range"};
+    if (h.err & kErrOrientedCapacity) throw Error{DSIFT_ECAPACITY, "device work list overflow: oriented keypoints"};
+    if (h.err & kErrDescriptorLattice) throw Error{DSIFT_ECAPACITY, "descriptor lattice exceeds table capacity"};
+    return h;
+}
+
 static DevKeypoint* upload_kps(dsift_ctx* c, const dsift_keypoint* kps, int64_t n) {
     std::vector<DevKeypoint> v((size_t)n);
     for (int64_t i = 0; i < n; ++i) {
@@ -1520,6 +1737,7 @@ int dsift_orientation_histograms(dsift_ctx* c, const dsift_keypoint* kps, int64_
         reset_counters(c);
         run_orient(c, dk, n, n, tmp, n * bins, hist, orient_depth(c->cfg.c, &hk, c->plan));
         cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        check_stage_errors(c);
         cuda_check(cudaMemcpy(out, hist, sizeof(float) * (size_t)n * bins, cudaMemcpyDeviceToHost), "D2H");
     });
 }
@@ -1540,8 +1758,7 @@ int dsift_assign_orientations(dsift_ctx* c, const dsift_keypoint* kps, int64_t n
         reset_counters(c);
         run_orient(c, dk, n, n, tmp, n * bins, nullptr, orient_depth(c->cfg.c, &hk, c->plan));
         cuda_check(cudaStreamSynchronize(c->stream), "sync");
-        Counters h{};
-        cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
+        const Counters h = check_stage_errors(c);
         std::vector<DevKeypoint> v((size_t)h.n_ori);
         if (!v.empty())
             cuda_check(cudaMemcpy(v.data(), tmp, v.size() * sizeof(DevKeypoint), cudaMemcpyDeviceToHost), "D2H");
@@ -1565,10 +1782,7 @@ static void stage_describe(dsift_ctx* c, const dsift_keypoint* kps, int64_t n, f
     reset_counters(c);
     run_describe(c, dk, n, d, raw_mode ? nullptr : d8, raw_mode, f, stage_smax(c, kps, n), nullptr);
     cuda_check(cudaStreamSynchronize(c->stream), "sync");
-    Counters h{};
-    cuda_check(cudaMemcpy(&h, c->counters.as<void>(), sizeof(h), cudaMemcpyDeviceToHost), "D2H");
-    if (h.err & kErrHistogramRange) throw Error{DSIFT_ERANGE, "histogram: bin index out of range"};
-    if (h.err & kErrDescriptorLattice) throw Error{DSIFT_ECAPACITY, "descriptor lattice exceeds table capacity"};
+    check_stage_errors(c);
     cuda_check(cudaMemcpy(out, d, sizeof(float) * kDescDim * (size_t)n, cudaMemcpyDeviceToHost), "D2H");
     if (out_u8 && !raw_mode)
         cuda_check(cudaMemcpy(out_u8, d8, (size_t)kDescDim * n, cudaMemcpyDeviceToHost), "D2H");
@@ -1598,52 +1812,25 @@ int dsift_synth_value_noise(dsift_ctx* c, float* dev_out, int n, int w, int h, u
 
 int64_t dsift_kernel_launches(dsift_ctx* c) { return c ? c->launches : 0; }
 
-int dsift_libm_probe(dsift_ctx* c, int mode, const void* in, int64_t n, void* out) {
-    return guard([&] {
-        if (!c || !in || !out) invalid("null argument");
-        if (mode < 0 || mode > 3) invalid("libm_probe: mode must be 0 (atan2f), 1 (exp), 2 (sincos) or 3 (division)");
-        set_device(c);
-        if (mode == 3) {   // in = uint64 seed, n = operand pairs, out = uint64[2] (mismatches, first)
-            void *din = nullptr, *dout = nullptr;
-            cuda_check(cudaMalloc(&din, 8), "cudaMalloc");
-            cuda_check(cudaMalloc(&dout, 16), "cudaMalloc");
-            cuda_check(cudaMemcpy(din, in, 8, cudaMemcpyHostToDevice), "H2D");
-            cuda_check(cudaMemset(dout, 0, 16), "memset");
-            cuda_check(launch_libm_probe(mode, din, n, dout, c->stream), "probe");
-            cuda_check(cudaStreamSynchronize(c->stream), "sync");
-            cuda_check(cudaMemcpy(out, dout, 16, cudaMemcpyDeviceToHost), "D2H");
-            cudaFree(din);
-            cudaFree(dout);
-            return;
-        }
-        const size_t isz = mode == 0 ? 8 : 8, osz = mode == 0 ? 4 : (mode == 1 ? 8 : 16);
-        void *din = nullptr, *dout = nullptr;
-        cuda_check(cudaMalloc(&din, isz * (size_t)std::max<int64_t>(n, 1)), "cudaMalloc");
-        cuda_check(cudaMalloc(&dout, osz * (size_t)std::max<int64_t>(n, 1)), "cudaMalloc");
-        cuda_check(cudaMemcpy(din, in, isz * (size_t)n, cudaMemcpyHostToDevice), "H2D");
-        cuda_check(launch_libm_probe(mode, din, n, dout, c->stream), "probe");
-        cuda_check(cudaStreamSynchronize(c->stream), "sync");
-        cuda_check(cudaMemcpy(out, dout, osz * (size_t)n, cudaMemcpyDeviceToHost), "D2H");
-        cudaFree(din);
-        cudaFree(dout);
-    });
-}
-
 int dsift_set_option(dsift_ctx* c, int key, int64_t value) {
     return guard([&] {
         if (!c) invalid("null context");
-        if (key == DSIFT_OPT_FORCE_EXACT) c->force_exact = value > 0 ? 1 : (int)value;   // < 0: diagnostics (-1 trust fast sums, -2 dump)
-        else if (key == DSIFT_OPT_DESC_KERNEL) {
-            if (value != 1 && value != 2) invalid("set_option: descriptor kernel must be 1 or 2");
-            c->desc_kernel = (int)value;
+        if (key == DSIFT_OPT_FORCE_EXACT) {
+            if (value != 0 && value != 1) invalid("set_option: FORCE_EXACT must be 0 or 1");
+            c->force_exact = (int)value;
+        } else if (key == DSIFT_OPT_CAPACITY_SCALE) {
+            if (value <= 0) invalid("set_option: CAPACITY_SCALE must be > 0 (1/1000 units)");
+            c->cap_scale = (double)value / 1000.0;
+        } else {
+            invalid("set_option: unknown key");
         }
-        else invalid("set_option: unknown key");
     });
 }
 
 int64_t dsift_stat(dsift_ctx* c, int key) {
     if (!c) return -1;
-    if (key == DSIFT_STAT_EXACT_FALLBACKS) return (int64_t)c->last_slow;
+    if (key == DSIFT_STAT_EXACT_FALLBACKS) return (int64_t)c->cur->slow;
+    if (key == DSIFT_STAT_REPLAYS) return (int64_t)c->cur->retries;
     return -1;
 }
 

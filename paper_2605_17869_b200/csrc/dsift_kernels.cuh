@@ -1,6 +1,7 @@
 // dsift_kernels.cuh — launch-argument structs and launcher entry points of
 // the device stages (one definition shared by k_*.cu and dsift_host.cu).
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include "dsift_common.cuh"
@@ -43,14 +44,14 @@ struct DetectArgs {
     unsigned* hit_masks;         // [n_tiles][256] per-thread (level, row) hit bits (s <= 8)
     unsigned* tile_counts;       // [n_tiles]
     unsigned* tile_offsets;      // [n_tiles] exclusive scan of tile_counts
-    void* scan_temp;
-    size_t scan_temp_bytes;
-    // TMA: per-octave 3-D maps of the DoG stack {w, h, batch * (s+2)} (device
-    // memory, CUtensorMap each); octave o is staged by TMA iff bit o is set
-    const void* dog_maps;
+    void* scan_state;            // launch_scan_u32 scratch
+    // TMA: per-octave 3-D maps of the DoG stack {w, h, batch * (s+2)}, passed
+    // by value in the __grid_constant__ parameter block (no global-memory
+    // descriptor, so no tensormap proxy fence is needed); octave o is staged
+    // by TMA iff bit o is set
     unsigned tma_mask;
+    CUtensorMap dog_maps[kMaxOctaves];
 };
-size_t detect_scan_temp_bytes(unsigned n_tiles);
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st);
 cudaError_t launch_refine(const DetectArgs& a, const DevCandidate* cand, const unsigned long long* n_cand,
                           long long cap, int* keep, cudaStream_t st);
@@ -96,8 +97,7 @@ struct DescArgs {
     unsigned* fix_count;   // stream kernel: (keypoint, scale) pairs recomputed exactly in place
     unsigned* ticket;      // stream kernel: next keypoint to claim (zeroed before the launch)
     long long slow_cap;
-    int force_slow;        // test hook: fail every certificate
-    int hot_pair;          // fast path: cache the (o0, o0+1) accumulators in registers
+    int force_slow;        // test hook (DSIFT_OPT_FORCE_EXACT): fail every certificate
     int max_span;          // stream kernel: table/ring width bound (in-range span + guards)
     float* desc;
     unsigned char* desc_u8;
@@ -106,29 +106,39 @@ struct DescArgs {
 cudaError_t launch_describe(const DescArgs& a, int grid, cudaStream_t st);
 size_t describe_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
 
-struct SortBuffers {
-    unsigned long long *keys_a, *keys_b;
-    int *idx_a, *idx_b;
-    void* temp;
-    size_t temp_bytes;
+// K7 bucket geometry: bucket = image * per_image + (octave * s + interval - 1) * rows + floor(y)
+struct SortGeom {
+    int s;              // intervals per octave
+    int rows;           // input image height (keypoint y is in input coordinates)
+    unsigned per_image; // n_oct * s * rows
 };
-size_t sort_temp_bytes(long long cap);
+size_t sort_work_bytes(long long cap, const SortGeom& g, int batch);
 cudaError_t launch_canonical_sort(const DevKeypoint* in, const unsigned long long* n_dev, long long cap,
-                                  const SortBuffers& sb, DevKeypoint* out, dsift_keypoint* out_pub,
+                                  const SortGeom& g, void* work, DevKeypoint* out, dsift_keypoint* out_pub,
                                   int batch, long long* offsets, cudaStream_t st, long long* launches);
+// device-wide exclusive scan of n uint32 (single pass, decoupled look-back);
+// state = scan_state_bytes(n) of scratch; *total_out (optional) = the sum
+size_t scan_state_bytes(long long n);
+cudaError_t launch_scan_u32(const unsigned* in, unsigned* out, long long n, void* state, unsigned* total_out,
+                            cudaStream_t st);
 cudaError_t launch_value_noise(float* out, int n, int w, int h, unsigned long long seed0, int octaves,
                                int cells, double* scratch, int nparts, cudaStream_t st);
 
-int describe_blocks_per_sm(size_t smem);
-cudaError_t launch_libm_probe(int mode, const void* in, long long n, void* out, cudaStream_t st);
-size_t describe_fast_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
-cudaError_t launch_describe_fast(const DescArgs& a, int grid, cudaStream_t st);
 size_t describe_stream_smem_bytes(int max_span, int n_dsp);
 size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
 int describe_stream_blocks_per_sm(size_t smem);
 cudaError_t launch_describe_stream(const DescArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev, long long n_host, double2* trig,
                         long long cap, cudaStream_t st);
+
+// k_batch.cu: result bookkeeping.  Folds a group's counters into the
+// result's totals; gathers a ragged batch's per-group staged outputs into
+// batch order (map = per image: staging-offsets entry, staging row base).
+cudaError_t launch_fold_totals(const Counters* ctr, BatchTotals* tot, cudaStream_t st);
+cudaError_t launch_ragged_gather(const long long* map, const long long* stage_offs, int n,
+                                 const dsift_keypoint* skp, const float* sdesc, const unsigned char* su8,
+                                 long long* offsets, dsift_keypoint* kp, float* desc, unsigned char* u8,
+                                 cudaStream_t st);
 
 size_t match_scratch_bytes(long long na, long long nb);
 // k_geom.cu: m = n x 4 doubles (x1, y1, x2, y2)

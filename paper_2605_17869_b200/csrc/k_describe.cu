@@ -33,8 +33,6 @@ namespace dsift {
 constexpr int kDescThreads = 128;
 constexpr int kTreeDepth = 13;   // per-bin leaves < 8192 (checked on the host)
 constexpr int kRing = 32;
-constexpr int kFastChunk = 6;                 // lattice rows per fast-path chunk
-constexpr int kSampRing = kFastChunk + 2;     // sample rows kept (chunk + guard rows)        // per-bin leaf ring (flushed every 16 candidate points)
 constexpr float kUndef = -1.0f;  // describe.cpp:188
 
 struct DescSmem {
@@ -391,326 +389,18 @@ describe_exact_kernel(const __grid_constant__ DescArgs a) {
 }
 
 // ------------------------------------------------------------------------------
-// Fast path: order-free FP64 accumulation + per-bin rounding certificate.
+// Certified order-free accumulation.
 //
 // Every histogram bin of describe.cpp:126 is the reference's pairwise tree
 // over float leaves (detsum.cpp:19-31).  For nonnegative leaves that tree is
 // within D*u*S of the exact sum S (D = depth <= 13, u = 2^-53), and any FP64
-// summation whose terms nest at most K deep is within K*u*S of S.  The fast
-// path sums each bin's leaves in a balanced, point-parallel order; if the
+// summation whose terms nest at most K deep is within K*u*S of S.  The stream
+// kernel below sums each bin's leaves in a point-parallel order; if the
 // interval [S(1-e), S(1+e)] with e = (K+D+slack)*u rounds to a single float,
 // that float IS the reference's bit pattern (rounding is monotone).  Bins that
-// fail the test (probability ~1e-7 each) send their keypoint to the exact
-// kernel above, so the output is bit-identical either way.
+// fail the test are recomputed with the exact kernel above, so the output is
+// bit-identical either way.
 // ------------------------------------------------------------------------------
-struct FastSmem {
-    double* q2;     // (k/bw)^2
-    double* ax;     // cx + cos*k
-    double* cy_su;  // cy + sin*k
-    double* sv;     // sin*k
-    double* cv;     // cos*k
-    float* frac;
-    int* c0;
-    float* samp;    // ring of kSampRing sample rows x A
-    float2* pvf;    // [chunk][A] (value, fo)
-    float* wct;     // [4][A] column weight of histogram column c at lattice u
-    unsigned char* po0;
-    double* acc;    // [8][128] item-private partial sums
-    short* lsb;     // [8][128] item-private min exponent of any leaf's lowest bit
-    float* raw;     // [n_dsp][128]
-    int* misc;      // band / column-range scratch
-};
-
-// exponent of the least significant mantissa bit of a nonzero float
-__device__ __forceinline__ int float_lsb_exp(float x) {
-    const int e = (int)((__float_as_uint(x) >> 23) & 0xffu);
-    return e == 0 ? -149 : e - 150;
-}
-
-__device__ __forceinline__ bool raw_descriptor_fast(const DescArgs& a, const FastSmem& S, const DevKeypoint& kp,
-                                                    double f, double cosa, double sina, float* raw_out) {
-    const PyramidDesc& p = a.pyr;
-    const OctaveDesc& od = p.oct[kp.octave];
-    const double to_input = ldexp(1.0, kp.octave) * (p.upsampled ? 0.5 : 1.0);
-    const double cx = kp.x / to_input, cy = kp.y / to_input;
-    const double sigma_rel = kp.sigma / to_input;
-    const int lvl = nearest_level_d(p, f * sigma_rel);
-    const float* __restrict__ img =
-        od.gauss + (long long)kp.image * p.gauss_img_stride(kp.octave) + (long long)lvl * od.level_stride;
-    const int w = od.w, h = od.h, pitch = od.pitch;
-    const double bw = 3.0 * f * sigma_rel;
-    const int radius = (int)llround(bw * (kDescCells + 1) * 0.5 * 1.4142135623730951);
-    const int tid = threadIdx.x;
-    if (2 * radius + 3 > a.max_axis) {
-        if (tid == 0) atomicOr(a.err, kErrDescriptorLattice);
-        raw_out[tid] = 0.0f;
-        __syncthreads();
-        return true;
-    }
-    const int kbase = -radius - 1;
-    const int naxis = 2 * radius + 3;
-    // misc[0..1] = in-range span [kmin, kmax]; misc[2+2c], misc[3+2c] = span of
-    // the points feeding histogram column c (bin floor in {c-1, c});
-    // misc[10+2(R+1)], misc[11+2(R+1)] = rows of band R (bin floor == R)
-    if (tid < 20) S.misc[tid] = (tid & 1) ? -(1 << 30) : (1 << 30);
-    __syncthreads();
-    for (int i = tid; i < naxis; i += kDescThreads) {   // describe.cpp:48-52, 72-73, 89-99
-        const int k = kbase + i;
-        const double q = D_DIV((double)k, bw);
-        const double bn = D_ADD(q, (double)(kDescCells / 2 - 0.5));
-        const int c = (int)floor(bn);
-        S.q2[i] = D_MUL(q, q);
-        S.c0[i] = c;
-        S.frac[i] = (float)D_SUB(bn, (double)c);
-        S.ax[i] = D_ADD(cx, D_MUL(cosa, (double)k));
-        S.cy_su[i] = D_ADD(cy, D_MUL(sina, (double)k));
-        S.sv[i] = D_MUL(sina, (double)k);
-        S.cv[i] = D_MUL(cosa, (double)k);
-        const float fr = (float)D_SUB(bn, (double)c);
-#pragma unroll
-        for (int cc = 0; cc < kDescCells; ++cc) S.wct[cc * a.max_axis + i] = (cc - c) ? fr : F_SUB(1.0f, fr);
-        if (i >= 1 && i < naxis - 1 && bn > -1.0 && bn < (double)kDescCells) {
-            atomicMin(&S.misc[0], k);
-            atomicMax(&S.misc[1], k);
-            if (c >= 0) { atomicMin(&S.misc[2 + 2 * c], k); atomicMax(&S.misc[3 + 2 * c], k); }
-            if (c + 1 < kDescCells) { atomicMin(&S.misc[4 + 2 * c], k); atomicMax(&S.misc[5 + 2 * c], k); }
-            atomicMin(&S.misc[12 + 2 * c], k);
-            atomicMax(&S.misc[13 + 2 * c], k);
-        }
-    }
-    __syncthreads();
-    const int kmin = S.misc[0], kmax = S.misc[1];
-    const int width = kmax - kmin + 1;
-    const int swidth = width + 2;
-    const int A = a.max_axis;
-    const int brow = tid >> 5, bcol = (tid >> 3) & 3, bori = tid & 7;
-    double binacc = 0.0;
-    int binlsb = 1 << 20;   // min lowest-bit exponent over this bin's nonzero leaves
-    int kterms = 0;         // max sequential terms in any partial sum this thread formed
-    int sampled_to = kmin - 2;   // last lattice row whose samples sit in the ring
-#define SROW(v) (S.samp + ((unsigned)((v) - kmin + 1) & (kSampRing - 1)) * swidth)
-
-    // bands: rows whose vbin floor is R (R = -1..3) feed histogram rows R and R+1
-    for (int R = -1; R < kDescCells; ++R) {
-        const int vb0 = S.misc[12 + 2 * R], vb1 = S.misc[13 + 2 * R];
-        if (vb1 < vb0) continue;
-        const int tr_first = R < 0 ? 0 : R;
-        const int ntr = (R < 0 || R + 1 >= kDescCells) ? 1 : 2;
-        const int npairs = ntr * kDescCells;
-        const int lg = (npairs == 8) ? 4 : 5;       // slices per (row, col) pair = 2^lg
-        const int nsl = 1 << lg;
-        const int pair = tid >> lg, slice = tid & (nsl - 1);
-        const int tr = tr_first + (pair >> 2), tc = pair & 3;
-        const int uc0 = S.misc[2 + 2 * tc], uc1 = S.misc[3 + 2 * tc];
-        const int ucount = uc1 - uc0 + 1;
-        const float inv_uc = 1.0f / (float)ucount;
-        const float* wcol = S.wct + tc * A + (uc0 - kbase);
-        const bool upper = (tr != R);               // ri = 1 -> wr = fr
-#pragma unroll
-        for (int o = 0; o < kDescOrients; ++o) {
-            S.acc[o * kDescThreads + tid] = 0.0;
-            S.lsb[o * kDescThreads + tid] = (short)32767;
-        }
-        int myterms = 0;
-        for (int v0 = vb0; v0 <= vb1; v0 += a.chunk_rows) {
-            const int v1 = min(v0 + a.chunk_rows - 1, vb1);
-            const int nrows = v1 - v0 + 1;
-            // samples for rows [v0-1, v1+1]; rows already in the ring are kept
-            const int s0 = max(v0 - 1, sampled_to + 1), s1 = v1 + 1;
-            __syncthreads();
-            const float inv_sw = 1.0f / (float)swidth;   // exact row split for idx < 2^16
-            const double wm1 = (double)(w - 1), hm1 = (double)(h - 1);
-            for (int idx = tid; idx < (s1 - s0 + 1) * swidth; idx += kDescThreads) {
-                const int rr = (int)(((float)idx + 0.5f) * inv_sw), cc = idx - rr * swidth;
-                const int vv = s0 + rr, u = kmin - 1 + cc;
-                const double px = D_SUB(S.ax[u - kbase], S.sv[vv - kbase]);
-                const double py = D_ADD(S.cy_su[u - kbase], S.cv[vv - kbase]);
-                float sv = kUndef;
-                if (!(px < 0.0 || px > wm1 || py < 0.0 || py > hm1))
-                    sv = sample_bilinear(img, w, h, pitch, px, py);
-                SROW(vv)[cc] = sv;
-            }
-            sampled_to = s1;
-            __syncthreads();
-            const float inv_w = 1.0f / (float)width;
-            for (int idx = tid; idx < nrows * width; idx += kDescThreads) {
-                const int rr = (int)(((float)idx + 0.5f) * inv_w), cc = idx - rr * width;
-                const int vv = v0 + rr, u = kmin + cc;
-                const float* mid = SROW(vv) + cc + 1;
-                const float left = mid[-1], right = mid[1], up = SROW(vv - 1)[cc + 1], down = SROW(vv + 1)[cc + 1];
-                unsigned char o0 = 0xff;
-                float value = 0.0f, fo = 0.0f;
-                if (!(left == kUndef || right == kUndef || up == kUndef || down == kUndef)) {
-                    const float du = F_MUL(0.5f, F_SUB(right, left));
-                    const float dv = F_MUL(0.5f, F_SUB(down, up));
-                    const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
-                    float theta = dsift_atan2f(dv, du);
-                    if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
-                    if (isnan(theta)) {   // reference: negative bin -> std::out_of_range
-                        atomicOr(a.err, kErrHistogramRange);
-                        theta = 0.0f;
-                    }
-                    double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
-                    if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
-                    const double arg = D_MUL(-D_ADD(S.q2[u - kbase], S.q2[vv - kbase]), 0.125);
-                    const float wgt = (float)dsift_exp(arg);
-                    value = F_MUL(mag, wgt);
-                    const int o = (int)floor(obin);
-                    fo = (float)D_SUB(obin, (double)o);
-                    o0 = (unsigned char)o;
-                }
-                S.pvf[rr * A + cc] = make_float2(value, fo);
-                S.po0[rr * A + cc] = o0;
-            }
-            __syncthreads();
-            // balanced accumulation: item (pair, slice) takes a contiguous run of
-            // the pair's rows x [uc0, uc1] block (row-major); two leaves per
-            // point.  The (o0, o0+1) accumulator pair lives in registers while
-            // the run's orientation stays put (gradient orientation is spatially
-            // coherent); it is spilled to the item's shared slots on a change.
-            const int tot = nrows * ucount;
-            const int runlen = (tot + nsl - 1) >> lg;
-            const int i0 = slice * runlen, i1 = min(tot, i0 + runlen);
-            if (i0 < i1) {
-                int rr = (int)(((float)i0 + 0.5f) * inv_uc), cu = i0 - rr * ucount;
-                int hot = -1;
-                double ha = 0.0, hb = 0.0;
-                int ea = 0x7fff, eb = 0x7fff;   // min exponent field of nonzero leaves
-                const int cbase = uc0 - kmin;
-                for (int i = i0; i < i1; ++i) {
-                    const int pidx = rr * A + cbase + cu;
-                    const int o0 = S.po0[pidx];
-                    if (o0 != 0xff) {
-                        const float fr = S.frac[v0 + rr - kbase];
-                        const float wr = upper ? fr : F_SUB(1.0f, fr);
-                        const float2 pv = S.pvf[pidx];
-                        const float t = F_MUL(F_MUL(pv.x, wr), wcol[cu]);
-                        const float l0 = F_MUL(t, F_SUB(1.0f, pv.y));   // orientation o0
-                        const float l1 = F_MUL(t, pv.y);                // orientation o0 + 1
-                        if (o0 != hot) {
-                            if (hot >= 0) {
-                                const int ia = hot * kDescThreads + tid;
-                                const int ib = ((hot + 1) & (kDescOrients - 1)) * kDescThreads + tid;
-                                S.acc[ia] = S.acc[ia] + ha;
-                                S.acc[ib] = S.acc[ib] + hb;
-                                S.lsb[ia] = (short)min((int)S.lsb[ia], ea);
-                                S.lsb[ib] = (short)min((int)S.lsb[ib], eb);
-                            }
-                            hot = o0;
-                            ha = hb = 0.0;
-                            ea = eb = 0x7fff;
-                        }
-                        ha = ha + (double)l0;
-                        hb = hb + (double)l1;
-                        const unsigned b0 = __float_as_uint(l0), b1 = __float_as_uint(l1);
-                        ea = min(ea, b0 ? max((int)(b0 >> 23), 1) : 0x7fff);
-                        eb = min(eb, b1 ? max((int)(b1 >> 23), 1) : 0x7fff);
-                        ++myterms;
-                    }
-                    if (++cu == ucount) {
-                        cu = 0;
-                        ++rr;
-                    }
-                }
-                if (hot >= 0) {
-                    const int ia = hot * kDescThreads + tid;
-                    const int ib = ((hot + 1) & (kDescOrients - 1)) * kDescThreads + tid;
-                    S.acc[ia] = S.acc[ia] + ha;
-                    S.acc[ib] = S.acc[ib] + hb;
-                    S.lsb[ia] = (short)min((int)S.lsb[ia], ea);
-                    S.lsb[ib] = (short)min((int)S.lsb[ib], eb);
-                }
-            }
-        }
-        // a leaf's path: <= myterms adds in its register run + <= myterms spills
-        kterms = max(kterms, 2 * myterms + 2);
-        __syncthreads();
-        // fold this band's slices into the bins of rows R, R+1 (fixed order)
-        if (brow >= tr_first && brow < tr_first + ntr) {
-            const int bp = ((brow - tr_first) << 2) + bcol;
-            double sacc = 0.0;
-            for (int sl = 0; sl < nsl; ++sl) {
-                sacc = sacc + S.acc[bori * kDescThreads + bp * nsl + sl];
-                binlsb = min(binlsb, (int)S.lsb[bori * kDescThreads + bp * nsl + sl] - 150);
-            }
-            binacc = binacc + sacc;
-        }
-        __syncthreads();   // the next band re-zeroes S.acc
-    }
-#undef SROW
-    // certificate: |tree - S| <= 13u S,  |binacc - S| <= (K + 32 + 2) u S
-    const int kmaxterms = __reduce_max_sync(0xffffffffu, kterms);
-    if ((tid & 31) == 0) S.misc[20 + (tid >> 5)] = kmaxterms;
-    __syncthreads();
-    const int K = max(max(S.misc[20], S.misc[21]), max(S.misc[22], S.misc[23]));
-    // (a) exact case: if every leaf's lowest bit and the sum's top bit span at
-    //     most 53 bits, every partial sum in ANY order is exact, so the tree
-    //     and this sum are both the exact S;
-    // (b) otherwise the rounding-interval test.
-    bool ok;
-    float res;
-    const int top = (int)((__double_as_longlong(binacc) >> 52) & 0x7ff) - 1023;
-    if (binacc == 0.0 || top - binlsb <= 52) {
-        ok = true;
-        res = __double2float_rn(binacc);
-    } else {
-        const double e = (double)(K + 64 + 16) * 0x1p-53;
-        const double lo = binacc * (1.0 - e), hi = binacc * (1.0 + e);
-        const float flo = __double2float_rn(lo), fhi = __double2float_rn(hi);
-        ok = (flo == fhi);
-        res = flo;
-    }
-    ok = ok && !a.force_slow;
-    raw_out[tid] = res;
-    __syncthreads();
-    return ok;
-}
-
-__global__ void __launch_bounds__(kDescThreads, 6)
-describe_fast_kernel(const __grid_constant__ DescArgs a) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    __shared__ double red[4];
-    __shared__ int misc[24];
-    const int A = a.max_axis;
-    FastSmem S;
-    unsigned char* pbuf = sm;
-    S.q2 = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
-    S.ax = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
-    S.cy_su = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
-    S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
-    S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * A;
-    S.acc = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * kDescOrients * kDescThreads;
-    S.frac = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * A;
-    S.c0 = reinterpret_cast<int*>(pbuf); pbuf += sizeof(int) * A;
-    S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * a.n_dsp;
-    S.samp = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kSampRing * A;
-    S.pvf = reinterpret_cast<float2*>(pbuf); pbuf += sizeof(float2) * a.chunk_rows * A;
-    S.wct = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescCells * A;
-    S.lsb = reinterpret_cast<short*>(pbuf); pbuf += sizeof(short) * kDescOrients * kDescThreads;
-    S.po0 = pbuf;
-    S.misc = misc;
-
-    const long long n = a.n_host >= 0 ? a.n_host : (long long)*a.n_dev;
-    const int tid = threadIdx.x;
-    for (long long k = blockIdx.x; k < n; k += gridDim.x) {
-        const DevKeypoint kp = a.kps[k];
-        const double2 cs = a.trig[k];
-        bool ok = true;
-        for (int fi = 0; fi < a.n_dsp; ++fi)
-            ok &= raw_descriptor_fast(a, S, kp, a.dsp[fi], cs.x, cs.y, S.raw + fi * kDescDim);
-        const bool all_ok = __syncthreads_and(ok);
-        if (!all_ok) {
-            if (tid == 0) {
-                const unsigned slot = atomicAdd(a.slow_count, 1u);
-                if ((long long)slot < a.slow_cap) a.slow_out[slot] = (int)k;
-                else atomicOr(a.err, kErrDescriptorLattice);
-            }
-            continue;   // the exact kernel writes this keypoint's descriptor
-        }
-        dsp_epilogue(a, S.raw, k, red);
-        __syncthreads();
-    }
-}
 
 // ------------------------------------------------------------------------------
 // Stream path (the production certified kernel): band-streamed, cell-lane.
@@ -728,7 +418,7 @@ describe_fast_kernel(const __grid_constant__ DescArgs a) {
 //       private slot [ri][ci][o] in shared memory (no divergence, no atomics);
 //   P3  bin-owner threads fold the lane slots of the pass into their FP64 bin
 //       sum (fixed lane order), overlapped with the next pass's P1.
-// Each bin is then certified exactly like the fast path above (exact-span or
+// Each bin is then certified as described above (exact-span or
 // rounding-interval test against the reference's pairwise tree); keypoints
 // with an uncertified bin go to the exact kernel.
 // ------------------------------------------------------------------------------
@@ -1179,7 +869,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
     }
     stream_misc_rearm(misc);   // every thread read misc before the pass barriers
     if (tid < 32) S.cellmin[((npass - 1) & 1) * 32 + tid] = 1 << 20;   // folded before the last barrier
-    // certificate (see the fast path): chain <= kchain in a lane slot, <= 51 in
+    // certificate (see above): chain <= kchain in a lane slot, <= 51 in
     // the fold, <= npass across passes; the reference tree is <= 13 deep
     bool ok;
     float res;
@@ -1195,14 +885,6 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         res = flo;
     }
     raw_out[tid] = res;
-    if (a.force_slow == -2) {   // diagnostic dump (block 0, keypoint 0): rows fi*4 + field
-        const int fi = (int)(raw_out - S.raw) / kDescDim;
-        a.desc[(fi * 4 + 0) * kDescDim + tid] = (float)binacc;
-        a.desc[(fi * 4 + 1) * kDescDim + tid] = (float)(binlsb - 127 - 23);
-        a.desc[(fi * 4 + 2) * kDescDim + tid] = (float)(kchain * 1000 + npass);
-        a.desc[(fi * 4 + 3) * kDescDim + tid] = ok ? 1.0f : 0.0f;
-    }
-    if (a.force_slow < 0) return true;   // diagnostic: trust the fast sums unconditionally
     return ok && !a.force_slow;
 }
 
@@ -1238,10 +920,9 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     // costs up to ~16x another (its DSP lattices scale with sigma^2), so a
     // static stride would leave the slowest CTA ~10% behind the mean
     __shared__ unsigned s_k;
-    const bool diag = a.force_slow == -2;   // diagnostic dump: block 0, keypoint 0 only
-    for (int it = 0;; ++it) {
+    for (;;) {
         __syncthreads();                   // everyone is done with the previous s_k
-        if (tid == 0) s_k = diag ? (blockIdx.x == 0 && it == 0 ? 0u : 0xffffffffu) : atomicAdd(a.ticket, 1u);
+        if (tid == 0) s_k = atomicAdd(a.ticket, 1u);
         __syncthreads();
         const long long k = (long long)s_k;
         if (k >= n) break;
@@ -1254,7 +935,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
             const bool ok = raw_descriptor_stream(a, S, kp, sscale[fi], cs.x, cs.y, S.raw + fi * kDescDim, RP,
                                                   misc + 16 * (call & 1));
             const bool sok = __syncthreads_and(ok);
-            if (!sok && a.force_slow == 0) {
+            if (!sok && !a.force_slow) {
                 // a bin the certificate could not prove: recompute this scale with
                 // the exact scan-order trees, in place (the stream working set is
                 // dead; the exact working set aliases it, raw[] is kept)
@@ -1273,7 +954,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
             }
             continue;   // the exact kernel writes this keypoint's descriptor
         }
-        if (a.force_slow != -2) dsp_epilogue(a, S.raw, k, red);
+        dsp_epilogue(a, S.raw, k, red);
         __syncthreads();
     }
 }
@@ -1338,34 +1019,11 @@ cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev,
     return cudaGetLastError();
 }
 
-size_t describe_fast_smem_bytes(int max_axis, int chunk_rows, int n_dsp) {
-    const size_t A = (size_t)max_axis;
-    return sizeof(double) * 5 * A + sizeof(double) * kDescOrients * kDescThreads +
-           sizeof(short) * kDescOrients * kDescThreads + sizeof(float) * A + sizeof(int) * A +
-           sizeof(float) * kDescDim * n_dsp + sizeof(float) * kSampRing * A + sizeof(float) * 2 * chunk_rows * A +
-           sizeof(float) * kDescCells * A + chunk_rows * A + 16;
-}
-
-int describe_blocks_per_sm(size_t smem) {
-    cudaFuncSetAttribute(describe_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, describe_fast_kernel, kDescThreads, smem) != cudaSuccess) n = 1;
-    return n;
-}
-
 cudaError_t launch_describe(const DescArgs& a, int grid, cudaStream_t st) {
     const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, a.raw_mode ? 1 : a.n_dsp);
     cudaError_t e = cudaFuncSetAttribute(describe_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     describe_exact_kernel<<<grid, kDescThreads, smem, st>>>(a);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_describe_fast(const DescArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = describe_fast_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
-    cudaError_t e = cudaFuncSetAttribute(describe_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    describe_fast_kernel<<<grid, kDescThreads, smem, st>>>(a);
     return cudaGetLastError();
 }
 

@@ -10,7 +10,6 @@
 // scan plus a decoupled look-back over ticket-ordered tiles.  Output order is
 // (image, octave, tile, thread, level, row) — fixed by construction, no
 // atomics on order; canonical order is restored later by the sort (K7).
-#include <cub/device/device_scan.cuh>
 #include <cuda_runtime.h>
 
 #include "dsift_common.cuh"
@@ -123,7 +122,7 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
         if (threadIdx.x == 0) {
             mbar_init(&bar, 1);
             mbar_arrive_expect_tx(&bar, (unsigned)(sizeof(float) * kDetPitch * kDetHalo * nlev));
-            tma_load_3d(lv_s, static_cast<const CUtensorMap*>(a.dog_maps) + o, xs - 1, ys - 1, b * nlev, &bar);
+            tma_load_3d(lv_s, &a.dog_maps[o], xs - 1, ys - 1, b * nlev, &bar);
         }
         __syncthreads();
         mbar_wait(&bar, 0);
@@ -226,7 +225,8 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
     }
 }
 
-// K2b: candidates of tile t go to [tile_offsets[t], +count) in (thread, level,
+// K2b (after the device-wide scan of the tile counts, k_sort.cu): candidates
+// of tile t go to [tile_offsets[t], +count) in (thread, level,
 // row) order -- the same deterministic order as a single-pass look-back.  One
 // warp per tile (8 tiles per CTA): lane j replays count-kernel threads 8j..8j+7.
 __global__ void __launch_bounds__(256)
@@ -334,12 +334,6 @@ cudaError_t launch_refine(const DetectArgs& a, const DevCandidate* cand, const u
     return cudaGetLastError();
 }
 
-size_t detect_scan_temp_bytes(unsigned n_tiles) {
-    size_t bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const unsigned*)nullptr, (unsigned*)nullptr, (int)n_tiles);
-    return bytes;
-}
-
 cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st) {
     if (a.n_tiles == 0) return cudaSuccess;
     const size_t smem = sizeof(float) * (size_t)(a.pyr.s + 2) * kDetHalo * kDetPitch + 128;
@@ -347,8 +341,7 @@ cudaError_t launch_detect(const DetectArgs& a, cudaStream_t st) {
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fn<<<a.n_tiles, kDetThreads, smem, st>>>(a);
-    size_t tb = a.scan_temp_bytes;
-    e = cub::DeviceScan::ExclusiveSum(a.scan_temp, tb, a.tile_counts, a.tile_offsets, (int)a.n_tiles, st);
+    e = launch_scan_u32(a.tile_counts, a.tile_offsets, (long long)a.n_tiles, a.scan_state, nullptr, st);
     if (e != cudaSuccess) return e;
     detect_emit_kernel<<<(a.n_tiles + 7) / 8, 256, 0, st>>>(a);
     return cudaGetLastError();

@@ -34,15 +34,6 @@
 
 namespace dsift {
 
-// A/B switch for measurements: DSIFT_BLUR_V1=1 keeps the v1 LEVEL kernel.
-static bool blur_v1_forced() {
-    static const int v = [] {
-        const char* e = std::getenv("DSIFT_BLUR_V1");
-        return e ? std::atoi(e) : 0;
-    }();
-    return v != 0;
-}
-
 constexpr int kTileW = 64;
 constexpr int kTileH = 64;
 constexpr int kBlurThreads = 256;
@@ -76,94 +67,8 @@ __device__ __forceinline__ float fetch_input(const BlurArgs& a, const float* __r
     }
 }
 
-template <int R, int MODE>
-__global__ void __launch_bounds__(kBlurThreads)
-blur_level_kernel(const __grid_constant__ BlurArgs a) {
-    constexpr int kLen = 2 * R + 1;
-    constexpr int kInH = kTileH + 2 * R;
-    constexpr int kInW = kTileW + 2 * R;
-    constexpr int kInPitch = (kInW + 3) & ~3;      // float4-aligned rows
-    constexpr int kChunks = (2 * R + 4 + 3) / 4;   // float4 chunks per H window
-    extern __shared__ __align__(16) float smem[];
-    float* in_s = smem;                            // [kInH][kInPitch]
-    float* tmp_s = smem + kInH * kInPitch;         // [kInH][kTileW]
-
-    const int b = blockIdx.z;
-    const int x0 = blockIdx.x * kTileW, y0 = blockIdx.y * kTileH;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const float* __restrict__ src = a.src + b * a.src_img_stride;
-
-    // ---- stage the input tile (reflect-101 at the borders) -------------------
-    for (int r = warp; r < kInH; r += kBlurThreads / 32) {
-        const int gy = reflect101(y0 - R + r, a.h);
-        for (int c = lane; c < kInW; c += 32) {
-            const int gx = reflect101(x0 - R + c, a.w);
-            in_s[r * kInPitch + c] = fetch_input<MODE>(a, src, gx, gy);
-        }
-    }
-    __syncthreads();
-
-    // ---- horizontal pass: rows [0, kInH), 4 columns per thread ---------------
-    for (int item = tid; item < kInH * (kTileW / 4); item += kBlurThreads) {
-        const int r = item / (kTileW / 4), g = item % (kTileW / 4);
-        const float4* row = reinterpret_cast<const float4*>(in_s + r * kInPitch + 4 * g);
-        double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
-#pragma unroll
-        for (int q = 0; q < kChunks; ++q) {
-            const float4 v4 = row[q];
-            const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
-#pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int e = 4 * q + m;
-                if (e >= 2 * R + 4) break;
-                const double x = (double)vv[m];
-                if (e - 0 >= 0 && e - 0 < kLen) acc0 = __fma_rn(a.taps[e - 0], x, acc0);
-                if (e - 1 >= 0 && e - 1 < kLen) acc1 = __fma_rn(a.taps[e - 1], x, acc1);
-                if (e - 2 >= 0 && e - 2 < kLen) acc2 = __fma_rn(a.taps[e - 2], x, acc2);
-                if (e - 3 >= 0 && e - 3 < kLen) acc3 = __fma_rn(a.taps[e - 3], x, acc3);
-            }
-        }
-        *reinterpret_cast<float4*>(tmp_s + r * kTileW + 4 * g) =
-            make_float4((float)acc0, (float)acc1, (float)acc2, (float)acc3);
-    }
-    __syncthreads();
-
-    // ---- vertical pass: 4 rows per thread, lanes along x ---------------------
-    float* __restrict__ dst = a.dst + b * a.dst_img_stride;
-    float* __restrict__ dog = a.dog ? a.dog + b * a.dog_img_stride : nullptr;
-    float* __restrict__ seed = (MODE == kModeDecimate) ? a.seed + b * a.seed_img_stride : nullptr;
-    for (int item = tid; item < kTileW * (kTileH / 4); item += kBlurThreads) {
-        const int c = item % kTileW, rg = item / kTileW;
-        const int x = x0 + c;
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-        for (int e = 0; e < 2 * R + 4; ++e) {
-            const double v = (double)tmp_s[(4 * rg + e) * kTileW + c];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int t = e - j;
-                if (t >= 0 && t < kLen) acc[j] = __fma_rn(a.taps[t], v, acc[j]);
-            }
-        }
-        if (x < a.w) {
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const int y = y0 + 4 * rg + j;
-                if (y >= a.h) break;
-                const float g = (float)acc[j];
-                const long long o = (long long)y * a.pitch + x;
-                dst[o] = g;
-                if (MODE == kModeLevel || MODE == kModeDecimate) {
-                    const float prev = in_s[(4 * rg + j + R) * kInPitch + c + R];
-                    if (MODE == kModeDecimate) seed[o] = prev;
-                    if (dog) dog[o] = g - prev;
-                }
-            }
-        }
-    }
-}
-
-// Generic-radius fallback (R up to kMaxRadius); same arithmetic, runtime taps.
+// Generic-radius path (16 < R <= kMaxRadius, configs with a large sigma0);
+// same arithmetic as the tiled kernel below, runtime taps.
 template <int MODE>
 __global__ void __launch_bounds__(kBlurThreads)
 blur_level_kernel_any(const __grid_constant__ BlurArgs a, int R) {
@@ -217,31 +122,15 @@ static size_t blur_smem_bytes(int R) {
 }
 
 template <int MODE>
-static cudaError_t launch_mode(const BlurArgs& a, int R, int batch, cudaStream_t st) {
+static cudaError_t launch_any(const BlurArgs& a, int R, int batch, cudaStream_t st) {
     const dim3 grid((a.w + kTileW - 1) / kTileW, (a.h + kTileH - 1) / kTileH, batch);
     const size_t smem = blur_smem_bytes(R);
-    void (*fn)(BlurArgs) = nullptr;
-    switch (R) {
-#define DSIFT_R(r) case r: fn = blur_level_kernel<r, MODE>; break;
-        DSIFT_R(1) DSIFT_R(2) DSIFT_R(3) DSIFT_R(4) DSIFT_R(5) DSIFT_R(6) DSIFT_R(7) DSIFT_R(8)
-        DSIFT_R(9) DSIFT_R(10) DSIFT_R(11) DSIFT_R(12) DSIFT_R(13) DSIFT_R(14) DSIFT_R(15)
-        DSIFT_R(16)
-#undef DSIFT_R
-        default: break;
-    }
-    if (fn) {
-        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        fn<<<grid, kBlurThreads, smem, st>>>(a);
-        return cudaGetLastError();
-    }
     cudaError_t e = cudaFuncSetAttribute(blur_level_kernel_any<MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     blur_level_kernel_any<MODE><<<grid, kBlurThreads, smem, st>>>(a, R);
     return cudaGetLastError();
 }
-
 
 // ---------------------------------------------------------------------------
 // LEVEL-mode blur, v2 (the 5 incremental levels of every octave).
@@ -528,20 +417,13 @@ static cudaError_t launch_v2(const BlurArgs& a, int R, int batch, cudaStream_t s
 }
 
 cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStream_t st) {
-    const bool v2 = R >= 1 && R <= 16 && !blur_v1_forced();
+    const bool tiled = R >= 1 && R <= 16;
     switch (mode) {
-        case kModeLevel:
-            if (v2 && a.src_pitch == a.pitch) return launch_v2<kModeLevel>(a, R, batch, st);
-            return launch_mode<kModeLevel>(a, R, batch, st);
-        case kModeRaw:
-            if (v2) return launch_v2<kModeRaw>(a, R, batch, st);
-            return launch_mode<kModeRaw>(a, R, batch, st);
+        case kModeLevel: return tiled ? launch_v2<kModeLevel>(a, R, batch, st) : launch_any<kModeLevel>(a, R, batch, st);
+        case kModeRaw: return tiled ? launch_v2<kModeRaw>(a, R, batch, st) : launch_any<kModeRaw>(a, R, batch, st);
         case kModeUpsample:
-            if (v2) return launch_v2<kModeUpsample>(a, R, batch, st);
-            return launch_mode<kModeUpsample>(a, R, batch, st);
-        default:
-            if (v2) return launch_v2<kModeDecimate>(a, R, batch, st);
-            return launch_mode<kModeDecimate>(a, R, batch, st);
+            return tiled ? launch_v2<kModeUpsample>(a, R, batch, st) : launch_any<kModeUpsample>(a, R, batch, st);
+        default: return tiled ? launch_v2<kModeDecimate>(a, R, batch, st) : launch_any<kModeDecimate>(a, R, batch, st);
     }
 }
 

@@ -1,55 +1,180 @@
 // k_sort.cu — K7: canonical order (reference: core.cpp:116-170
-// keypoint_less / canonical_sort) and per-image segmentation.
+// keypoint_less / canonical_sort) and per-image segmentation, plus the
+// device-wide exclusive scan the detector's compaction uses.
 //
 // The reference's total order is (octave, interval, y, x, angle, sigma,
-// response, descriptor bytes).  All keypoint floats are >= +0 (angle -0 is
-// canonicalised, orient.cpp:99-100), so their IEEE bit patterns order like
-// the values and the order is an LSD radix sort on three 64-bit keys:
-//   k1 = sigma:response,  k2 = x:angle,  k3 = image:octave:interval:y.
-// Descriptors are a pure function of the keypoint fields, so full-key ties
-// are byte-identical rows and the descriptor tie-break never changes bytes;
-// the CTA sort therefore runs BEFORE descriptors, which are then written
-// directly in canonical order (no 512-byte row permutation).
-#include <cub/device/device_radix_sort.cuh>
+// response, descriptor bytes).  Descriptors are a pure function of the
+// keypoint fields, so full-key ties are byte-identical rows: the sort runs
+// BEFORE the descriptor stage, which then writes rows directly in canonical
+// order (no 512-byte row permutation).
+//
+// Bucket sort over the actual count n (device-resident, never the capacity):
+//   bucket(kp) = image * NBI + (octave * s + interval - 1) * H + floor(y)
+// (H = input height; y is in input coordinates, y in [0, H)), which is
+// monotone in the key's leading fields (image, octave, interval, y).  A
+// C3 image has ~15k keypoints over 8*3*1200 = 28.8k buckets, so a bucket
+// holds ~0.5 keypoints on average (orientation fan-out copies share one).
+//   K7a count:   bucket id per keypoint + integer-atomic bucket counts;
+//   K7b scan:    exclusive scan of the counts (decoupled look-back);
+//   K7c scatter: slot = bucket start + atomic cursor (arbitrary order inside
+//                a bucket ...);
+//   K7d rank:    ... made canonical: each keypoint's final slot is its bucket
+//                start + the number of bucket members with a smaller
+//                (y, x, angle, sigma, response, original index) — a pure
+//                function of the data, whatever order K7c produced;
+//   K7e gather:  sorted DevKeypoint list, the public 28-byte keypoints and the
+//                per-image offsets (= the start of each image's first bucket).
+// All keypoint floats are >= +0 here (x, y > 0 by construction, sigma > 0,
+// response = |D|, angle canonicalised to +0, orient.cpp:99-100), so their
+// IEEE bit patterns order like the values.
 #include <cuda_runtime.h>
+
+#include <algorithm>
 
 #include "dsift_common.cuh"
 #include "dsift_kernels.cuh"
+#include "dsift_scan.cuh"
 
 namespace dsift {
 
-__global__ void sort_keys_kernel(const DevKeypoint* __restrict__ kp, const unsigned long long* n_dev,
-                                 long long cap, int which, const int* __restrict__ perm,
-                                 unsigned long long* __restrict__ keys, int* __restrict__ idx) {
+// ---- device-wide exclusive scan of uint32 (single pass, decoupled look-back) ----
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 8;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_u32_kernel(const unsigned* __restrict__ in, unsigned* __restrict__ out, long long n, ScanState st,
+                unsigned n_tiles, unsigned* total_out) {
+    __shared__ unsigned ticket_s;
+    __shared__ unsigned long long off_s;
+    __shared__ unsigned warp_sum[kScanThreads / 32];
+    const unsigned t = scan_ticket(st, &ticket_s);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const long long base = (long long)t * kScanTile + (long long)threadIdx.x * kScanItems;
+    unsigned v[kScanItems];
+    unsigned sum = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        v[k] = base + k < n ? __ldg(in + base + k) : 0u;
+        sum += v[k];
+    }
+    unsigned incl = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const unsigned nb = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += nb;
+    }
+    if (lane == 31) warp_sum[warp] = incl;
+    __syncthreads();
+    unsigned warp_off = 0, tile_total = 0;
+#pragma unroll
+    for (int q = 0; q < kScanThreads / 32; ++q) {
+        warp_off += q < warp ? warp_sum[q] : 0u;
+        tile_total += warp_sum[q];
+    }
+    const unsigned long long off = scan_exclusive(st, t, tile_total, n_tiles, &off_s);
+    unsigned run = (unsigned)off + warp_off + incl - sum;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+        if (base + k < n) out[base + k] = run;
+        run += v[k];
+    }
+    if (total_out && t == n_tiles - 1 && threadIdx.x == kScanThreads - 1) *total_out = run;
+}
+
+size_t scan_state_bytes(long long n) {
+    const long long tiles = std::max<long long>(1, (n + kScanTile - 1) / kScanTile);
+    return sizeof(unsigned long long) * (size_t)tiles + 256;
+}
+
+cudaError_t launch_scan_u32(const unsigned* in, unsigned* out, long long n, void* state, unsigned* total_out,
+                            cudaStream_t st) {
+    if (n <= 0) {
+        if (total_out) return cudaMemsetAsync(total_out, 0, sizeof(unsigned), st);
+        return cudaSuccess;
+    }
+    const unsigned tiles = (unsigned)((n + kScanTile - 1) / kScanTile);
+    cudaError_t e = cudaMemsetAsync(state, 0, scan_state_bytes(n), st);
+    if (e != cudaSuccess) return e;
+    ScanState s;
+    s.states = static_cast<unsigned long long*>(state);
+    s.ticket = reinterpret_cast<unsigned*>(static_cast<char*>(state) + sizeof(unsigned long long) * tiles);
+    s.total = reinterpret_cast<unsigned long long*>(static_cast<char*>(state) + sizeof(unsigned long long) * tiles + 64);
+    s.cap = ~0ull;
+    scan_u32_kernel<<<tiles, kScanThreads, 0, st>>>(in, out, n, s, tiles, total_out);
+    return cudaGetLastError();
+}
+
+// ---- K7 ----------------------------------------------------------------------
+__device__ __forceinline__ unsigned sort_bucket(const DevKeypoint& k, const SortGeom& g) {
+    const int row = min(max((int)k.y, 0), g.rows - 1);   // (int) of y >= 0 = floor
+    const int lvl = k.octave * g.s + (k.interval - 1);
+    return (unsigned)k.image * g.per_image + (unsigned)(lvl * g.rows + row);
+}
+
+// strict "a before b" over the fields that can differ inside one bucket
+__device__ __forceinline__ bool sort_less(const DevKeypoint& a, int ia, const DevKeypoint& b, int ib) {
+    const unsigned a0 = __float_as_uint(a.y), b0 = __float_as_uint(b.y);
+    if (a0 != b0) return a0 < b0;
+    const unsigned a1 = __float_as_uint(a.x), b1 = __float_as_uint(b.x);
+    if (a1 != b1) return a1 < b1;
+    const unsigned a2 = __float_as_uint(a.angle), b2 = __float_as_uint(b.angle);
+    if (a2 != b2) return a2 < b2;
+    const unsigned a3 = __float_as_uint(a.sigma), b3 = __float_as_uint(b.sigma);
+    if (a3 != b3) return a3 < b3;
+    const unsigned a4 = __float_as_uint(a.response), b4 = __float_as_uint(b.response);
+    if (a4 != b4) return a4 < b4;
+    return ia < ib;   // full ties: identical bytes either way (descriptors are field-determined)
+}
+
+__global__ void sort_count_kernel(const DevKeypoint* __restrict__ kp, const unsigned long long* n_dev, SortGeom g,
+                                  unsigned* __restrict__ bkt, unsigned* __restrict__ cnt) {
     const long long n = (long long)*n_dev;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < cap;
-         i += (long long)gridDim.x * blockDim.x) {
-        const long long src = perm ? perm[i] : i;
-        unsigned long long key;
-        if (src >= n) {
-            key = ~0ull;
-        } else {
-            const DevKeypoint k = kp[src];
-            if (which == 0)
-                key = ((unsigned long long)__float_as_uint(k.sigma) << 32) | __float_as_uint(k.response);
-            else if (which == 1)
-                key = ((unsigned long long)__float_as_uint(k.x) << 32) | __float_as_uint(k.angle);
-            else
-                key = ((unsigned long long)(unsigned)k.image << 42) |
-                      ((unsigned long long)(unsigned)(k.octave & 31) << 37) |
-                      ((unsigned long long)(unsigned)(k.interval & 31) << 32) | __float_as_uint(k.y);
-        }
-        keys[i] = key;
-        if (!perm) idx[i] = (int)i;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned b = sort_bucket(kp[i], g);
+        bkt[i] = b;
+        atomicAdd(cnt + b, 1u);   // integer counts: order-free
     }
 }
 
-__global__ void gather_kernel(const DevKeypoint* __restrict__ in, const int* __restrict__ perm,
-                              const unsigned long long* n_dev, DevKeypoint* __restrict__ out,
-                              dsift_keypoint* __restrict__ out_pub) {
+__global__ void sort_scatter_kernel(const unsigned long long* n_dev, const unsigned* __restrict__ bkt,
+                                    const unsigned* __restrict__ start, unsigned* __restrict__ cnt,
+                                    int* __restrict__ tmp) {
     const long long n = (long long)*n_dev;
-    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-         i += (long long)gridDim.x * blockDim.x) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned b = bkt[i];
+        const unsigned pos = atomicSub(cnt + b, 1u) - 1u;   // any order; K7d fixes it
+        tmp[start[b] + pos] = (int)i;
+    }
+}
+
+__global__ void sort_rank_kernel(const DevKeypoint* __restrict__ kp, const unsigned long long* n_dev,
+                                 const unsigned* __restrict__ bkt, const unsigned* __restrict__ start,
+                                 const int* __restrict__ tmp, int* __restrict__ perm) {
+    const long long n = (long long)*n_dev;
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < n; j += (long long)gridDim.x * blockDim.x) {
+        const int i = tmp[j];
+        const unsigned b = bkt[i];
+        const unsigned lo = start[b], hi = start[b + 1];
+        unsigned rank = 0;
+        if (hi - lo > 1) {
+            const DevKeypoint me = kp[i];
+            for (unsigned q = lo; q < hi; ++q) {
+                const int m = tmp[q];
+                if (m != i && sort_less(kp[m], m, me, i)) ++rank;
+            }
+        }
+        perm[lo + rank] = i;
+    }
+}
+
+__global__ void sort_gather_kernel(const DevKeypoint* __restrict__ in, const int* __restrict__ perm,
+                                   const unsigned long long* n_dev, DevKeypoint* __restrict__ out,
+                                   dsift_keypoint* __restrict__ out_pub, const unsigned* __restrict__ start,
+                                   SortGeom g, int batch, long long* __restrict__ offsets) {
+    const long long n = (long long)*n_dev;
+    const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    for (long long i = tid; i < n; i += (long long)gridDim.x * blockDim.x) {
         const DevKeypoint k = in[perm[i]];
         out[i] = k;
         dsift_keypoint p;
@@ -62,59 +187,45 @@ __global__ void gather_kernel(const DevKeypoint* __restrict__ in, const int* __r
         p.interval = k.interval;
         out_pub[i] = p;
     }
+    // offsets[b] = first slot of image b = start of its first bucket (b = batch: n)
+    for (long long b = tid; b <= batch; b += (long long)gridDim.x * blockDim.x)
+        offsets[b] = (long long)start[(size_t)b * g.per_image];
 }
 
-// offsets[b] = first index of image b in the sorted list (b in [0, batch]).
-__global__ void image_offsets_kernel(const DevKeypoint* __restrict__ sorted, const unsigned long long* n_dev,
-                                     int batch, long long* offsets) {
-    const long long n = (long long)*n_dev;
-    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= batch; b += gridDim.x * blockDim.x) {
-        long long lo = 0, hi = n;
-        while (lo < hi) {
-            const long long mid = (lo + hi) >> 1;
-            if (sorted[mid].image < b) lo = mid + 1; else hi = mid;
-        }
-        offsets[b] = lo;
-    }
+size_t sort_work_bytes(long long cap, const SortGeom& g, int batch) {
+    const size_t nb = (size_t)batch * g.per_image + 1;
+    const size_t a = (sizeof(unsigned) * (size_t)cap + 255) & ~size_t(255);          // bkt
+    const size_t b = (sizeof(int) * 2 * (size_t)cap + 255) & ~size_t(255);           // tmp, perm
+    const size_t c = (sizeof(unsigned) * 2 * nb + 255) & ~size_t(255);               // cnt, start
+    return a + b + c + scan_state_bytes((long long)nb);
 }
 
-size_t sort_temp_bytes(long long cap) {
-    size_t bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, bytes, (unsigned long long*)nullptr,
-                                    (unsigned long long*)nullptr, (int*)nullptr, (int*)nullptr,
-                                    (int)cap, 0, 64);
-    return bytes;
-}
-
-// Sorts in[0..n) (n on device, capacity cap) into out / out_pub; returns the
-// number of kernel launches issued through *launches.
 cudaError_t launch_canonical_sort(const DevKeypoint* in, const unsigned long long* n_dev, long long cap,
-                                  const SortBuffers& sb, DevKeypoint* out, dsift_keypoint* out_pub,
+                                  const SortGeom& g, void* work, DevKeypoint* out, dsift_keypoint* out_pub,
                                   int batch, long long* offsets, cudaStream_t st, long long* launches) {
-    if (cap <= 0) return cudaSuccess;
+    const size_t nb = (size_t)batch * g.per_image;   // buckets; start[] has nb + 1 entries
+    char* p = static_cast<char*>(work);
+    unsigned* bkt = reinterpret_cast<unsigned*>(p);
+    p += (sizeof(unsigned) * (size_t)cap + 255) & ~size_t(255);
+    int* tmp = reinterpret_cast<int*>(p);
+    int* perm = tmp + cap;
+    p += (sizeof(int) * 2 * (size_t)cap + 255) & ~size_t(255);
+    unsigned* cnt = reinterpret_cast<unsigned*>(p);
+    unsigned* start = cnt + (nb + 1);
+    p += (sizeof(unsigned) * 2 * (nb + 1) + 255) & ~size_t(255);
+    void* scan_state = p;
+
     const int threads = 256;
-    const int grid = (int)std::min<long long>((cap + threads - 1) / threads, 148 * 16);
-    const int* perm = nullptr;
-    int* cur_idx = sb.idx_a;
-    for (int which = 0; which < 3; ++which) {
-        sort_keys_kernel<<<grid, threads, 0, st>>>(in, n_dev, cap, which, perm, sb.keys_a,
-                                                   which == 0 ? sb.idx_a : nullptr);
-        ++*launches;
-        size_t tb = sb.temp_bytes;
-        const int* vin = (which == 0) ? sb.idx_a : perm;
-        // keys_a/vin -> keys_b/idx_b ; then idx_b becomes the permutation
-        int* vout = (vin == sb.idx_b) ? sb.idx_a : sb.idx_b;
-        cudaError_t e = cub::DeviceRadixSort::SortPairs(sb.temp, tb, sb.keys_a, sb.keys_b, vin, vout,
-                                                        (int)cap, 0, 64, st);
-        if (e != cudaSuccess) return e;
-        *launches += 10;  // onesweep on 64-bit keys: histogram + exclusive sum + 8 digit passes
-        perm = vout;
-        cur_idx = vout;
-    }
-    (void)cur_idx;
-    gather_kernel<<<grid, threads, 0, st>>>(in, perm, n_dev, out, out_pub);
-    image_offsets_kernel<<<1, 256, 0, st>>>(out, n_dev, batch, offsets);
-    *launches += 2;
+    const int grid = (int)std::max<long long>(1, std::min<long long>((cap + threads - 1) / threads, 148 * 8));
+    cudaError_t e = cudaMemsetAsync(cnt, 0, sizeof(unsigned) * (nb + 1), st);
+    if (e != cudaSuccess) return e;
+    sort_count_kernel<<<grid, threads, 0, st>>>(in, n_dev, g, bkt, cnt);
+    e = launch_scan_u32(cnt, start, (long long)nb, scan_state, start + nb, st);
+    if (e != cudaSuccess) return e;
+    sort_scatter_kernel<<<grid, threads, 0, st>>>(n_dev, bkt, start, cnt, tmp);
+    sort_rank_kernel<<<grid, threads, 0, st>>>(in, n_dev, bkt, start, tmp, perm);
+    sort_gather_kernel<<<grid, threads, 0, st>>>(in, perm, n_dev, out, out_pub, start, g, batch, offsets);
+    *launches += 5;
     return cudaGetLastError();
 }
 

@@ -22,6 +22,26 @@ int main(int argc, char** argv) {
         dsift::Extractor ex(cfg, 0);
         const dsift::FeatureSet fs = ex.extract(img);
         std::cout << fs.size() << " " << ex.sha256(0) << "\n";
+        // the drop-in call with the reference's signature (workers = 8, twice:
+        // the second call reuses the thread's cached context) gives the same bytes
+        for (int rep = 0; rep < 2; ++rep) {
+            const dsift::FeatureSet d = dsift::extract(img, cfg, 8);
+            if (d.keypoints.size() != fs.keypoints.size() || d.descriptors != fs.descriptors) {
+                std::cout << "drop-in mismatch\n";
+                return 1;
+            }
+        }
+        // a mixed-size batch in one call: every image equals its single extract
+        dsift::GrayImage small(97, 53);
+        for (size_t i = 0; i < small.data.size(); ++i) small.data[i] = float((i * 2654435761u) % 1000) / 1000.0f;
+        const dsift::GrayImage batch[3] = {img, small, img};
+        const std::vector<dsift::FeatureSet> out = ex.extract_batch(batch, 3);
+        const dsift::FeatureSet fs_small = ex.extract(small);
+        if (out[0].descriptors != fs.descriptors || out[2].descriptors != fs.descriptors ||
+            out[1].descriptors != fs_small.descriptors || out[1].keypoints.size() != fs_small.keypoints.size()) {
+            std::cout << "ragged mismatch\n";
+            return 1;
+        }
         // error path mirrors the reference: too small -> std::invalid_argument
         dsift::SiftConfig no_up;
         no_up.upsample_pixel_limit = 0;

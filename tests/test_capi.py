@@ -35,7 +35,7 @@ def test_no_fallback_symbols_or_cpu_paths():
 
 def test_abi_version_and_strerror():
     lib = ds.load_library()
-    assert lib.dsift_abi_version() == 1
+    assert lib.dsift_abi_version() == 2
     assert lib.dsift_strerror(2) == b"device capacity exceeded"
 
 

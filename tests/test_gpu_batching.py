@@ -1,0 +1,123 @@
+"""GPU: the drop-in boundary beyond one same-size batch — ragged batches
+(dsift_extract_images, the reference's any-size extract, io.cpp:111-142),
+result handles (two batches in flight on one context), the automatic
+capacity replay, and the drop-in extract(img, cfg, workers) with a cached
+per-thread context (io.hpp:17-19; workers never changes the output,
+parallel.hpp:12-16)."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2605_17869_b200 as ds
+
+pytestmark = pytest.mark.gpu
+
+C5_SIZES = [(640, 480), (800, 600), (1000, 750), (1024, 768), (1280, 720), (1600, 1200), (1920, 1080),
+            (2048, 1536), (2560, 1440), (3840, 2160)]
+
+
+def splitmix64(seed):
+    s = [seed & 0xFFFFFFFFFFFFFFFF]
+
+    def nxt():
+        M = 0xFFFFFFFFFFFFFFFF
+        s[0] = (s[0] + 0x9E3779B97F4A7C15) & M
+        z = s[0]
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+    return nxt
+
+
+def c5_sizes(n):
+    """C5 resolutions drawn by SplitMix64(0xC5); every size present."""
+    rng = splitmix64(0xC5)
+    sizes = [C5_SIZES[rng() % len(C5_SIZES)] for _ in range(n - len(C5_SIZES))]
+    return sizes + C5_SIZES   # guarantee all ten
+
+
+def test_c5_ragged_batch_matches_single_images_and_reference(port, ref):
+    sizes = c5_sizes(64)
+    imgs = [port.value_noise(w, h, 0x5EED0000 + i, 5, max(8, w // 20)) for i, (w, h) in enumerate(sizes)]
+    with ds.Extractor() as ex:
+        res = ex.extract_images(imgs)
+        shas = [ex.sha256(i) for i in range(len(imgs))]
+        assert len(res) == len(imgs)
+        ex.extract_images(imgs)   # run to run
+        assert [ex.sha256(i) for i in range(len(imgs))] == shas
+        singles = []
+        for im in imgs:
+            ex.extract(im)
+            singles.append(ex.sha256(0))
+    assert shas == singles
+    # the reference on a sample (small, mid, 4K)
+    for i in (0, 5, len(imgs) - 1):
+        k, d = ref.extract(imgs[i], None, os.cpu_count() or 1)
+        assert shas[i] == ref.hash_features(k, d), sizes[i]
+        assert res[i].keypoints.tobytes() == np.ascontiguousarray(k).tobytes()
+
+
+def test_result_handles_two_batches_in_flight(port):
+    a = np.stack([port.value_noise(320, 240, 0x5EED0100 + i, 5, 16) for i in range(3)])
+    b = [port.value_noise(200, 150, 0x5EED0200, 5, 10), port.value_noise(321, 199, 0x5EED0201, 5, 16)]
+    with ds.Extractor() as ex:
+        want_a = [f.descriptors.tobytes() for f in ex.extract_batch(a)]
+        want_b = [f.descriptors.tobytes() for f in ex.extract_images(b)]
+        r1, r2 = ex.new_result(), ex.new_result()
+        ex.select(r1)
+        ex.submit(a)
+        ex.select(r2)
+        ex.submit_images(b)        # batch 2 enqueued while batch 1 is unread
+        ex.select(r1)
+        got_a = [f.descriptors.tobytes() for f in ex.results()]
+        ex.select(r2)
+        got_b = [f.descriptors.tobytes() for f in ex.results()]
+        ex.select(None)
+        r1.close()
+        r2.close()
+    assert got_a == want_a and got_b == want_b
+
+
+def test_automatic_capacity_replays_instead_of_failing(port):
+    # automatic capacities started at 1% of their size: the first pass
+    # overflows, the batch is replayed with x4 lists until it fits, and the
+    # caller still receives every keypoint (the reference has no such limit)
+    img = port.value_noise(320, 240, 0x5EED0009, 5, 16)
+    k, d = port.extract(img)
+    with ds.Extractor() as ex:
+        ex.set_capacity_scale(10)
+        fs = ex.extract(img)
+        assert ex.replays() >= 1
+        assert fs.keypoints.tobytes() == k.tobytes()
+        assert ex.sha256(0) == port.hash_features(k, d)
+        ex.set_capacity(8)   # a fixed capacity still fails loudly
+        with pytest.raises(ds.DsiftError) as e:
+            ex.extract(img)
+        assert e.value.code == ds.DSIFT_ECAPACITY
+
+
+def test_drop_in_extract_workers_and_cached_context(port):
+    img = port.value_noise(160, 120, 0x5EED0007, 5, 8)
+    k, d = port.extract(img)
+    want = port.hash_features(k, d)
+    f1 = ds.extract(img, ds.SiftConfig(), 8)
+    ctx1 = ds._TLS.ex[1].ctx.value
+    f2 = ds.extract(img, ds.SiftConfig(), 0)
+    assert ds._TLS.ex[1].ctx.value == ctx1   # reused, not re-created
+    assert f1.keypoints.tobytes() == f2.keypoints.tobytes() == k.tobytes()
+    assert f1.descriptors.tobytes() == d.tobytes()
+    with ds.Extractor() as ex:
+        ex.extract(img)
+        assert ex.sha256(0) == want
+
+
+def test_failed_submit_leaves_no_stale_result(port):
+    img = port.value_noise(160, 120, 0x5EED0008, 5, 8)
+    with ds.Extractor() as ex:
+        ex.extract(img)
+        with pytest.raises(ds.InvalidArgument):
+            ex.submit(np.zeros((3, 3), np.float32))
+        with pytest.raises(ds.DsiftError) as e:
+            ex.sync()
+        assert e.value.code == ds.DSIFT_ESTATE

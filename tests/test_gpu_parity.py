@@ -120,44 +120,81 @@ def test_handcrafted_scale_space(port):
             assert ex.detect().tobytes() == port.detect(sp).tobytes()
 
 
+def libm_probe(mode, inputs):
+    """The product's device libm restatements (dsift_math.cuh) through the
+    test-only probe library tests/native/libdsift_probe.so."""
+    probe = C.CDLL(os.path.join(ROOT, "tests", "native", "libdsift_probe.so"))
+    probe.dsift_test_libm_probe.argtypes = [C.c_int, C.c_void_p, C.c_longlong, C.c_void_p]
+    if mode == 3:   # inputs = (seed, n): [mismatches, first failing (y << 32 | x) bits]
+        seed, n = inputs
+        a = np.array([seed], np.uint64)
+        out = np.zeros(2, np.uint64)
+        assert probe.dsift_test_libm_probe(3, a.ctypes.data, int(n), out.ctypes.data) == 0
+        return out
+    if mode == 0:
+        a = np.ascontiguousarray(inputs, np.float32).reshape(-1, 2)
+        out = np.empty(len(a), np.float32)
+    elif mode == 1:
+        a = np.ascontiguousarray(inputs, np.float64).ravel()
+        out = np.empty(len(a), np.float64)
+    else:
+        a = np.ascontiguousarray(inputs, np.float64).ravel()
+        out = np.empty((len(a), 2), np.float64)
+    assert probe.dsift_test_libm_probe(mode, a.ctypes.data, len(a), out.ctypes.data) == 0
+    return out
+
+
 def test_device_libm_matches_host():
+    # the device restatements against the host twins (2M inputs each) AND
+    # against the live glibc of this box (libm.so.6 through ctypes, a sample):
+    # atan2f, exp (the descriptor / orientation weights) and sin / cos (the
+    # keypoint's rotation, describe.cpp:51-52; glibc's sin/cos are correctly
+    # rounded on these arguments, which the live comparison pins)
     lib = C.CDLL(os.path.join(ROOT, "tests", "native", "liblibmcheck.so"))
     libm = C.CDLL("libm.so.6")
     libm.atan2f.restype = C.c_float
     libm.atan2f.argtypes = [C.c_float, C.c_float]
+    for fn in ("exp", "sin", "cos"):
+        getattr(libm, fn).restype = C.c_double
+        getattr(libm, fn).argtypes = [C.c_double]
     rng = np.random.default_rng(5)
     n = 2_000_000
     a = rng.random((n, 4), dtype=np.float32)
     scale = np.ldexp(np.float32(1), -rng.integers(0, 20, n)).astype(np.float32)
     yx = np.stack([(a[:, 0] - a[:, 1]) * scale, (a[:, 2] - a[:, 3]) * scale], 1).astype(np.float32)
-    with ds.Extractor() as ex:
-        dev = ex.libm_probe(0, yx)
-        twin = np.empty(n, np.float32)
-        ys, xs_ = np.ascontiguousarray(yx[:, 0]), np.ascontiguousarray(yx[:, 1])
-        lib.lc_atan2f_batch(ys.ctypes.data, xs_.ctypes.data, C.c_int64(n), twin.ctypes.data)
-        assert bits(dev).tobytes() == bits(twin).tobytes()
-        glibc = np.array([libm.atan2f(float(y), float(x)) for y, x in yx[:20000]], np.float32)
-        assert bits(dev[:20000]).tobytes() == bits(glibc).tobytes()
-        xs = -rng.random(n) * 12.0
-        dexp = ex.libm_probe(1, xs)
-        twin_e = np.empty(n, np.float64)
-        lib.lc_exp_batch(xs.ctypes.data, C.c_int64(n), twin_e.ctypes.data)
-        assert dexp.tobytes() == twin_e.tobytes()
-        ang = (rng.random(200000) * 6.283185307179586).astype(np.float32).astype(np.float64)
-        sc = ex.libm_probe(2, ang)
-        ts, tc = np.empty_like(ang), np.empty_like(ang)
-        lib.lc_sincos_batch(ang.ctypes.data, C.c_int64(len(ang)), ts.ctypes.data, tc.ctypes.data)
-        assert sc[:, 0].tobytes() == ts.tobytes() and sc[:, 1].tobytes() == tc.tobytes()
+    dev = libm_probe(0, yx)
+    twin = np.empty(n, np.float32)
+    ys, xs_ = np.ascontiguousarray(yx[:, 0]), np.ascontiguousarray(yx[:, 1])
+    lib.lc_atan2f_batch(ys.ctypes.data, xs_.ctypes.data, C.c_int64(n), twin.ctypes.data)
+    assert bits(dev).tobytes() == bits(twin).tobytes()
+    glibc = np.array([libm.atan2f(float(y), float(x)) for y, x in yx[:50000]], np.float32)
+    assert bits(dev[:50000]).tobytes() == bits(glibc).tobytes()
+    # exp over the argument range the path uses (weights: -(d^2)/(2 s^2) <= 0)
+    xs = -rng.random(n) * 12.0
+    dexp = libm_probe(1, xs)
+    twin_e = np.empty(n, np.float64)
+    lib.lc_exp_batch(xs.ctypes.data, C.c_int64(n), twin_e.ctypes.data)
+    assert dexp.tobytes() == twin_e.tobytes()
+    live_e = np.array([libm.exp(float(x)) for x in xs[:100000]], np.float64)
+    assert dexp[:100000].tobytes() == live_e.tobytes()
+    # sin / cos of float angles in [0, 2pi) (orientation peaks are floats)
+    ang = (rng.random(200000) * 6.283185307179586).astype(np.float32).astype(np.float64)
+    sc = libm_probe(2, ang)
+    ts, tc = np.empty_like(ang), np.empty_like(ang)
+    lib.lc_sincos_batch(ang.ctypes.data, C.c_int64(len(ang)), ts.ctypes.data, tc.ctypes.data)
+    assert sc[:, 0].tobytes() == ts.tobytes() and sc[:, 1].tobytes() == tc.tobytes()
+    live_s = np.array([libm.sin(float(x)) for x in ang], np.float64)
+    live_c = np.array([libm.cos(float(x)) for x in ang], np.float64)
+    assert sc[:, 0].tobytes() == live_s.tobytes() and sc[:, 1].tobytes() == live_c.tobytes()
 
 
 def test_fast_division_exhaustive():
     # ds_fdiv_inrange (the atan2f fast path's division, no FCHK) equals the IEEE
     # __fdiv_rn on ~4e9 operand pairs of its domain (random exponents in
     # [-100, 62] at most 60 apart, every 4th quotient near a multiple of 0.5)
-    with ds.Extractor() as ex:
-        for seed in (1, 2):
-            bad, first = ex.libm_probe(3, (seed, 2_000_000_000))
-            assert bad == 0, (int(bad), hex(int(first)))
+    for seed in (1, 2):
+        bad, first = libm_probe(3, (seed, 2_000_000_000))
+        assert bad == 0, (int(bad), hex(int(first)))
 
 
 # ---- determinism, batching, export ----------------------------------------------------
@@ -172,15 +209,11 @@ def test_determinism_batch_single_and_exact_path(port):
         for i in range(4):
             ex.extract(imgs[i])
             singles.append(ex.sha256(0))
-        ex.set_desc_kernel(1)
-        ex.extract_batch(imgs)
-        h4 = [ex.sha256(i) for i in range(4)]
-        ex.set_desc_kernel(2)
         ex.set_force_exact(True)
         ex.extract_batch(imgs)
         h3 = [ex.sha256(i) for i in range(4)]
         assert ex.exact_fallbacks() > 0
-    assert h1 == h2 == singles == h3 == h4
+    assert h1 == h2 == singles == h3
     for i in range(4):
         k, d = port.extract(imgs[i])
         assert port.hash_features(k, d) == h1[i]
