@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstdint>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include "../../paper_2605_17869_b200/csrc/dsift_math.cuh"
 
@@ -123,13 +125,14 @@ int64_t lc_exp_mismatch(uint64_t seed, int64_t n, double lo, double hi, int mode
 // counts angles whose (float)(cx + cos*u) style sample coordinate would move
 // (here: results that differ after rounding to float).
 int64_t lc_sincos_mismatch(uint64_t seed, int64_t n, int64_t* float_bad) {
+    // half float angles in [0, 2pi), half arbitrary doubles in [-8, 8)
     Rng r{seed};
     int64_t bad = 0, fb = 0;
     for (int64_t i = 0; i < n; ++i) {
-        const float a = float(r.uni() * 6.283185307179586);
+        const double a = (i & 1) ? double(float(r.uni() * 6.283185307179586)) : r.uni() * 16.0 - 8.0;
         double s, c;
-        dsift_sincos(double(a), &s, &c);
-        const double rs = std::sin(double(a)), rc = std::cos(double(a));
+        dsift_sincos(a, &s, &c);
+        const double rs = std::sin(a), rc = std::cos(a);
         if (dbits(rs) != dbits(s) || dbits(rc) != dbits(c)) {
             ++bad;
             if (float(rs) != float(s) || float(rc) != float(c)) ++fb;
@@ -137,6 +140,27 @@ int64_t lc_sincos_mismatch(uint64_t seed, int64_t n, int64_t* float_bad) {
     }
     if (float_bad) *float_bad = fb;
     return bad;
+}
+
+// Exhaustive: every float angle in [0, 2pi] (the domain describe.cpp:51-52
+// feeds), split over `threads` host threads.
+int64_t lc_sincos_exhaustive(int threads) {
+    const uint32_t hi = fbits(6.2831855f);
+    std::vector<int64_t> bad(threads, 0);
+    std::vector<std::thread> pool;
+    for (int t = 0; t < threads; ++t)
+        pool.emplace_back([&, t] {
+            for (uint64_t u = t; u <= hi; u += threads) {
+                const double a = bitsf(uint32_t(u));
+                double s, c;
+                dsift_sincos(a, &s, &c);
+                if (dbits(std::sin(a)) != dbits(s) || dbits(std::cos(a)) != dbits(c)) ++bad[t];
+            }
+        });
+    for (auto& th : pool) th.join();
+    int64_t b = 0;
+    for (int64_t x : bad) b += x;
+    return b;
 }
 
 void lc_atan2f_batch(const float* y, const float* x, int64_t n, float* out) {

@@ -41,14 +41,18 @@ def test_exp_bit_exact(lc, lo, hi, mode):
     assert bad == 0, f"{bad} mismatches, first (x, got) = {list(first)}"
 
 
-def test_sincos_float_level(lc):
-    # cos/sin feed double sample coordinates (describe.cpp:51-52); the
-    # double-double evaluation can differ from glibc's (<0.52 ulp, not always
-    # correctly rounded) in the last double bit, never after rounding to float.
+def test_sincos_bit_exact(lc):
+    # cos/sin feed the double sample coordinates (describe.cpp:51-52): the
+    # restatement of glibc's __sin_fma/__cos_fma must equal the live libm
     fb = C.c_int64()
-    bad = lc.lc_sincos_mismatch(99, 1_000_000, C.byref(fb))
-    assert fb.value == 0
-    assert bad < 10_000   # ~0.3% differ in the last double bit
+    bad = lc.lc_sincos_mismatch(99, 4_000_000, C.byref(fb))
+    assert bad == 0 and fb.value == 0
+
+
+def test_sincos_exhaustive_float_angles(lc):
+    lc.lc_sincos_exhaustive.restype = C.c_int64
+    lc.lc_sincos_exhaustive.argtypes = [C.c_int]
+    assert lc.lc_sincos_exhaustive(os.cpu_count() or 4) == 0
 
 
 def test_div_2pi_exhaustive(lc):
