@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra-configs", action="store_true", help="skip the C4 and C1-latency legs")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     return ap.parse_args()
 
@@ -91,6 +92,29 @@ def octave_plan(w, h, limit=4_000_000, sigma0=1.6, blur=0.5, s=3):
         ww //= 2
         hh //= 2
     return px
+
+
+def dfma_per_image(w, h, limit=4_000_000, sigma0=1.6, blur=0.5, s=3):
+    """Algorithmic DFMA of K1 per image: every output of both passes of every
+    blur is a (2R+1)-tap FP64 sum (scalespace.cpp:63-109): bridge on the base,
+    then s+2 incremental blurs per octave (no halo or tile overhead)."""
+    import math
+    px = octave_plan(w, h, limit, sigma0, blur, s)
+    up = w * h <= limit
+    assumed = 2 * blur if up else blur
+    bridge = 2 * math.ceil(4 * math.sqrt(sigma0 * sigma0 - assumed * assumed)) + 1
+    inc = [2 * math.ceil(4 * sigma0 * 2 ** ((i - 1) / s) * math.sqrt(2 ** (2 / s) - 1)) + 1 for i in range(1, s + 3)]
+    return 2 * (bridge * px[0] + sum(inc) * sum(px))
+
+
+def fp64_peak():
+    """Measured DFMA/s of this GPU (tools/fp64_peak, built by __graft_entry__.build())."""
+    exe = os.path.join(ROOT, "tools", "fp64_peak")
+    try:
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=60).stdout.strip().splitlines()
+        return json.loads(out[-1])
+    except Exception as e:   # reported as unmeasured, never guessed
+        return {"error": str(e)[:200]}
 
 
 def stage_bytes(w, h):
@@ -159,6 +183,42 @@ def cpu_reference_time(img, workers):
     return time.perf_counter() - t0, kind, workers, len(kps)
 
 
+def cpu_info():
+    """CPU model, host threads and glibc of this box (the baseline's context)."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    try:
+        libc = os.confstr("CS_GNU_LIBC_VERSION")
+    except (ValueError, OSError):
+        libc = "unknown"
+    return {"cpu_model": model, "host_threads": os.cpu_count(), "libc": libc}
+
+
+def cpu_throughput(w, h, n):
+    """Throughput mode of SURVEY 8(d)(ii): n concurrent detsift::extract(img, cfg,
+    workers=1) calls on n different images (ctypes drops the GIL), images/s."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle.oracle import Oracle, available
+    kind = "reference" if available("reference") else "port"
+    o = Oracle(kind)
+    imgs = [host_image(w, h, SEED0 + i) for i in range(n)]
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=n) as pool:
+        nk = sum(len(k) for k, _ in pool.map(lambda im: o.extract(im, None, 1) if kind == "reference"
+                                              else o.extract(im), imgs))
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "images/s", "cores": n, "kind": kind,
+            "sample": f"{n} images {w}x{h} (seeds {SEED0:#x}+i), {n} concurrent extract(workers=1) calls, "
+                      f"{nk} keypoints, {dt:.1f} s wall"}
+
+
 def magsac_cases():
     """Correspondences for the f4 measurement: the reference's acceptance
     configuration (acceptance.cpp:255-281: 60 inliers + 40 outliers, 1500
@@ -220,10 +280,71 @@ def run_reference(args, rank, world):
         "mpx_per_s": value * args.width * args.height / 1e6,
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": used, "kind": kind,
                          "sample": f"1 image {args.width}x{args.height} per step, detsift::extract "
-                                   f"workers={used}, {nk} keypoints"},
+                                   f"workers={used}, {nk} keypoints (latency mode: the reference's fastest "
+                                   "single-call configuration; same_config is false because a CPU step is one "
+                                   "image where the GPU step is a batch)", **cpu_info()},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- extra configs
+def c4_leg(ds, torch, steps=3, warmup=2, B=16):
+    """C4 (BASELINE configs[3]): 3840x2160, not upsampled (9 octaves), the
+    descriptor-bound config; B images per step, device-resident input, CUDA events."""
+    W4, H4 = 3840, 2160
+    with ds.Extractor(device=torch.cuda.current_device()) as ex:
+        stream = torch.cuda.Stream()
+        ex.set_stream(stream.cuda_stream)
+        ex.set_profiling(True)
+        imgs = torch.empty((B, H4, W4), dtype=torch.float32, device="cuda")
+        ex.synth_value_noise(imgs.data_ptr(), B, W4, H4, SEED0, 5, cells_for(W4))
+        stream.synchronize()
+        for _ in range(warmup):
+            ex.submit(None, n=B, w=W4, h=H4, device_ptr=imgs.data_ptr())
+            ex.sync()
+        acc = {}
+        nk = 0
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            ex.submit(None, n=B, w=W4, h=H4, device_ptr=imgs.data_ptr())
+            nk += ex.sync()
+            for k, v in ex.stage_times().items():
+                acc[k] = acc.get(k, 0.0) + v / steps
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        lat_all, lat_in = ex.lattice_points()
+    return {"workload": f"C4 {W4}x{H4} value-noise cells={cells_for(W4)}, not upsampled "
+                        f"({len(octave_plan(W4, H4))} octaves), {B} images/step, device-resident",
+            "value": B / (ms / 1e3), "unit": "images/s", "mpx_per_s": B * W4 * H4 / (ms / 1e3) / 1e6,
+            "ms_per_step": ms, "steps": steps, "keypoints_per_image": nk / (B * steps),
+            "stages_ms_per_step": acc,
+            "describe_share": acc.get("describe", 0.0) / max(1e-9, sum(acc.values())),
+            "lattice_points_per_s": lat_all / (acc["describe"] / 1e3) if acc.get("describe") else None}
+
+
+def c1_latency_leg(ds, reps=20):
+    """C1 (BASELINE configs[0]): one 640x480 image through the drop-in
+    extract(img, cfg, workers) with host buffers (cached context), wall clock per
+    call, median of `reps`; beside it the reference's extract(workers=nproc)."""
+    img = host_image(640, 480, SEED0)
+    ds.extract(img)   # creates the per-thread context
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fs = ds.extract(img)
+        ts.append(time.perf_counter() - t0)
+    out = {"workload": "C1 640x480 value-noise seed 0x5eed0000, default SiftConfig, one image per call, "
+                       "host float input and FeatureSet output (detsift::extract drop-in)",
+           "latency_ms_median": statistics.median(ts) * 1e3, "latency_ms_min": min(ts) * 1e3,
+           "calls": reps, "keypoints": len(fs)}
+    workers = os.cpu_count() or 1
+    dt, kind, used, nk = cpu_reference_time(img, workers)
+    out["reference_cpu"] = {"latency_ms": dt * 1e3, "kind": kind, "workers": used, "keypoints": nk}
+    return out
 
 
 # --------------------------------------------------------------------------- our arm
@@ -287,6 +408,7 @@ def run_ours(args, rank, local_rank, world):
         torch.cuda.synchronize()
     launches = ex.kernel_launches() - launches0
     fallbacks = ex.exact_fallbacks()
+    lat_all, lat_in = ex.lattice_points()   # last step, counted on the device
     ms = t_start.elapsed_time(t_end)
     barrier()
     ms_max = max_over_ranks(ms)
@@ -402,12 +524,22 @@ def run_ours(args, rank, local_rank, world):
                 "algorithmic_bytes_per_image": k1 + k2,
                 "per_stage_gbs": {"pyramid_dog": k1 * B / (stages["pyramid"] / 1e3) / 1e9,
                                   "extrema": k2 * B / (stages["detect"] / 1e3) / 1e9}}
-    lattice_per_kp = 24600.0
+    fp64 = fp64_peak()
+    dfma = dfma_per_image(W, H)
+    if "dfma_per_s" in fp64:
+        roofline["fp64"] = {"kernel": "K1 blur (FP64 tap sums, co-bound)", "dfma_per_image": dfma,
+                            "achieved_dfma_per_s": dfma * B / (stages["pyramid"] / 1e3),
+                            "peak_dfma_per_s": fp64["dfma_per_s"], "peak_source": "measured (tools/fp64_peak)",
+                            "frac": dfma * B / (stages["pyramid"] / 1e3) / fp64["dfma_per_s"]}
+    else:
+        roofline["fp64"] = {"dfma_per_image": dfma, "peak": None, "error": fp64.get("error")}
     desc_s = stages["describe"] / 1e3
     roofline_desc = {"bound": "issue (FP32/FP64 pipes; no dense contraction)",
                      "kernel": "K5/K6 descriptor (dominant)",
                      "keypoints_per_s": kps_per_image * B / desc_s,
-                     "lattice_points_per_s_est": kps_per_image * B * lattice_per_kp / desc_s,
+                     "lattice_points_per_s": lat_all / desc_s,
+                     "lattice_points_in_range_per_s": lat_in / desc_s,
+                     "lattice_points_per_keypoint": lat_all / max(1.0, kps_per_image * B),
                      "share_of_step": stages["describe"] / max(1e-9, sum(stages.values())),
                      "exact_fallbacks_last_step": fallbacks}
 
@@ -453,7 +585,9 @@ def run_ours(args, rank, local_rank, world):
         workers = os.cpu_count() or 1
         dt, kind, used, nk = cpu_reference_time(img, workers)
         cpu = {"value": 1.0 / dt, "unit": "images/s", "cores": used, "kind": kind,
-               "sample": f"1 image {W}x{H} (seed {SEED0:#x}), detsift::extract workers={used}, {nk} keypoints"}
+               "sample": f"1 image {W}x{H} (seed {SEED0:#x}), detsift::extract workers={used}, {nk} keypoints "
+                         "(latency mode, SURVEY 8d(i))", **cpu_info()}
+        cpu["throughput_mode"] = cpu_throughput(W, H, workers)
         if magsac is not None:   # the reference's own magsac_lite on the same correspondences
             from oracle.oracle import Oracle, available
             if available("reference"):
@@ -463,6 +597,11 @@ def run_ours(args, rank, local_rank, world):
                     ref.magsac_lite(m, iters, tau, seed, workers=workers)
                     case["reference_cpu_ms"] = (time.perf_counter() - t1) * 1e3
                     case["reference_cpu_workers"] = workers
+
+    c4 = c1 = None
+    if rank == 0 and world == 1 and not args.no_extra_configs:
+        c4 = c4_leg(ds, torch)
+        c1 = c1_latency_leg(ds)
 
     clocks = clk.summary()
     if rank == 0:
@@ -484,6 +623,8 @@ def run_ours(args, rank, local_rank, world):
             "match": match,
             "magsac": magsac,
             "cpu_baseline": cpu,
+            "c4": c4,
+            "c1_latency": c1,
             "clocks": clocks,
             "gpu_launches": launches,
         }

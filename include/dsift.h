@@ -258,6 +258,12 @@ int dsift_set_option(dsift_ctx* ctx, int key, int64_t value);
 /* DSIFT_STAT_REPLAYS = times the last result was replayed after an automatic
  * capacity overflow. */
 #define DSIFT_STAT_REPLAYS 2
+/* DSIFT_STAT_LATTICE_POINTS = descriptor lattice points of the last result,
+ * sum over keypoints and DSP scales of (2r+1)^2 (the trip count of
+ * describe.cpp:76-77), counted on the device; DSIFT_STAT_LATTICE_IN_RANGE =
+ * those inside the (-1, 4)-bin square, the points that contribute. */
+#define DSIFT_STAT_LATTICE_POINTS 3
+#define DSIFT_STAT_LATTICE_IN_RANGE 4
 int64_t dsift_stat(dsift_ctx* ctx, int key);
 int dsift_stage_times(dsift_ctx* ctx, float* ms5);
 

@@ -115,6 +115,10 @@ class Oracle:
             [C.c_int, C.POINTER(C.c_void_p)] if self.kind == "reference"
             else [C.POINTER(C.c_void_p), C.POINTER(C.c_void_p), C.POINTER(C.c_int64)])
         f("tree_sum").restype = C.c_float
+        if self.kind != "reference":
+            self.lib.dor_free.argtypes = [C.c_void_p]
+            self.lib.dor_build_scale_space.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(Config),
+                                                       C.POINTER(C.c_void_p)]
         f("tree_sum_f64").restype = C.c_double
         f("hash_features").argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_char_p]
         f("serialize").restype = C.c_int64
@@ -130,6 +134,11 @@ class Oracle:
                                         C.c_void_p, C.c_void_p]
         if self.kind == "reference":
             self.lib.oref_fs_size.restype = C.c_int64
+            self.lib.oref_fs_size.argtypes = [C.c_void_p]
+            self.lib.oref_fs_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+            self.lib.oref_fs_free.argtypes = [C.c_void_p]
+            self.lib.oref_ss_build.argtypes = [C.c_void_p, C.c_int, C.c_int, C.POINTER(Config), C.c_int,
+                                               C.POINTER(C.c_void_p)]
             self.lib.oref_splitmix_next.restype = C.c_uint64
             self.lib.oref_blob_field.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_void_p]
             self.lib.oref_add_blob.argtypes = [C.c_void_p, C.c_int, C.c_int] + [C.c_double] * 4

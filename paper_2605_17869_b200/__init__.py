@@ -129,12 +129,16 @@ def library_path() -> str:
     return os.path.join(HERE, "libdsift.so")
 
 
-def load_library():
-    """Loads the in-tree libdsift.so (fails loudly; no fallback)."""
+def load_library(path: str | None = None):
+    """Loads the in-tree libdsift.so (fails loudly; no fallback).  `path` names
+    another build of the same ABI explicitly (the test-only negative-control
+    library); it must be given before the first load."""
     global _LIB
     if _LIB is not None:
+        if path is not None and getattr(_LIB, "_path", None) != os.path.abspath(path):
+            raise DsiftError(DSIFT_ESTATE, "load_library: a different library is already loaded")
         return _LIB
-    path = library_path()
+    path = os.path.abspath(path) if path is not None else library_path()
     if not os.path.exists(path):
         raise DsiftError(DSIFT_ECUDA, f"CUDA extension missing: {path} (run __graft_entry__.build())")
     lib = C.CDLL(path)
@@ -181,6 +185,7 @@ def load_library():
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
+    lib._path = path
     _LIB = lib
     return lib
 
@@ -471,6 +476,11 @@ class Extractor:
     def replays(self) -> int:
         """Times the last result was replayed after an automatic capacity overflow."""
         return int(self.lib.dsift_stat(self.ctx, 2))
+
+    def lattice_points(self) -> tuple[int, int]:
+        """(all, in-range) descriptor lattice points of the last result, counted
+        on the device (DSIFT_STAT_LATTICE_POINTS / _IN_RANGE)."""
+        return int(self.lib.dsift_stat(self.ctx, 3)), int(self.lib.dsift_stat(self.ctx, 4))
 
     def exact_fallbacks(self) -> int:
         """Keypoints of the last result whose fast-path certificate failed."""

@@ -85,6 +85,8 @@ struct Counters {          // one small device block, cleared per batch
     unsigned long long n_kp;   // refined keypoints (compacted)
     unsigned emit_ticket;      // orientation fan-out tiles
     unsigned desc_ticket;      // describe: dynamic keypoint claims
+    unsigned long long lattice;     // describe: lattice points sum (2r+1)^2 (work unit)
+    unsigned long long lattice_in;  // describe: of those, inside the (-1, 4)-bin square (visited)
 };
 
 // Per-result device totals: every size group's counters are folded in here
@@ -93,6 +95,8 @@ struct BatchTotals {
     unsigned err;
     unsigned pad;
     unsigned long long slow;
+    unsigned long long lattice;
+    unsigned long long lattice_in;
 };
 
 }  // namespace dsift

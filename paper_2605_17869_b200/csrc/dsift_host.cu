@@ -216,6 +216,7 @@ struct dsift_result {
     int batch = 0;
     int64_t total = 0;
     unsigned long long slow = 0;
+    unsigned long long lattice = 0, lattice_in = 0;   // descriptor lattice points (DSIFT_STAT_LATTICE_*)
     std::vector<int64_t> h_offsets;
     std::vector<Group> groups;         // replayed on a capacity overflow (automatic capacity)
     std::vector<long long> h_map;      // ragged batches: image -> (staging offsets entry, row base)
@@ -597,8 +598,18 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
     a.slow_count = &ctr->n_slow;
     a.fix_count = &ctr->n_fixed;
     a.ticket = &ctr->desc_ticket;
+    a.lattice = &ctr->lattice;
+    a.lattice_in = &ctr->lattice_in;
     a.slow_cap = cap_n;
     a.force_slow = c->force_exact;
+#ifdef DSIFT_NONDET_TEST_HOOK
+    // the reference's negative control (detsum.cpp:73-109): a test-only build
+    // whose histogram sums depend on scheduling when DSIFT_NONDET=1
+    {
+        const char* v = std::getenv("DSIFT_NONDET");
+        a.nondet = v != nullptr && v[0] == '1';
+    }
+#endif
     DescArgs af = a;
     af.chunk_rows = 6;   // the stream kernel's in-place exact recompute works in 6-row chunks
     {
@@ -879,6 +890,8 @@ static void result_sync(dsift_ctx* c, dsift_result* r) {
             throw Error{DSIFT_ECAPACITY, m};
         }
         r->slow = t.slow;
+        r->lattice = t.lattice;
+        r->lattice_in = t.lattice_in;
         break;
     }
     r->h_offsets.assign((size_t)r->batch + 1, 0);
@@ -1831,6 +1844,8 @@ int64_t dsift_stat(dsift_ctx* c, int key) {
     if (!c) return -1;
     if (key == DSIFT_STAT_EXACT_FALLBACKS) return (int64_t)c->cur->slow;
     if (key == DSIFT_STAT_REPLAYS) return (int64_t)c->cur->retries;
+    if (key == DSIFT_STAT_LATTICE_POINTS) return (int64_t)c->cur->lattice;
+    if (key == DSIFT_STAT_LATTICE_IN_RANGE) return (int64_t)c->cur->lattice_in;
     return -1;
 }
 

@@ -96,9 +96,13 @@ struct DescArgs {
     unsigned* slow_count;
     unsigned* fix_count;   // stream kernel: (keypoint, scale) pairs recomputed exactly in place
     unsigned* ticket;      // stream kernel: next keypoint to claim (zeroed before the launch)
+    unsigned long long* lattice;   // stream kernel: += (2r+1)^2 lattice points per (keypoint, scale)
+    unsigned long long* lattice_in;   // stream kernel: += of those in the (-1, 4)-bin square
     long long slow_cap;
     int force_slow;        // test hook (DSIFT_OPT_FORCE_EXACT): fail every certificate
     int max_span;          // stream kernel: table/ring width bound (in-range span + guards)
+    int nondet;            // negative-control build only (DSIFT_NONDET_TEST_HOOK + env DSIFT_NONDET=1):
+                           // order-fragile float atomics instead of the fixed trees
     float* desc;
     unsigned char* desc_u8;
     unsigned* err;

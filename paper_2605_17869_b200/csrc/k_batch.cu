@@ -18,6 +18,8 @@ namespace dsift {
 __global__ void fold_totals_kernel(const Counters* __restrict__ ctr, BatchTotals* __restrict__ tot) {
     tot->err |= ctr->err;
     tot->slow += (unsigned long long)ctr->n_slow + ctr->n_fixed;
+    tot->lattice += ctr->lattice;
+    tot->lattice_in += ctr->lattice_in;
 }
 
 cudaError_t launch_fold_totals(const Counters* ctr, BatchTotals* tot, cudaStream_t st) {

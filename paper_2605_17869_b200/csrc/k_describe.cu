@@ -549,14 +549,19 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
             atomicMin(&misc[2 + (c + 1)], k);
         }
     }
+#ifdef DSIFT_NONDET_TEST_HOOK
+    if (a.nondet) raw_out[tid] = 0.0f;
+#endif
     __syncthreads();
     const int kmin = misc[0], kmax = misc[1];
+    if (tid == 0 && a.lattice) atomicAdd(a.lattice, (unsigned long long)(2 * radius + 1) * (2 * radius + 1));
     if (kmin > kmax) {   // no in-range lattice point: an all-zero histogram
         raw_out[tid] = 0.0f;
         __syncthreads();
         stream_misc_rearm(misc);
         return true;
     }
+    if (tid == 0 && a.lattice_in) atomicAdd(a.lattice_in, (unsigned long long)(kmax - kmin + 1) * (kmax - kmin + 1));
     int st[6];   // first lattice index of cell c = -1..3 at st[c + 1]; st[5] = kmax + 1
     st[5] = kmax + 1;
 #pragma unroll
@@ -565,11 +570,11 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
 #pragma unroll
     for (int c = 0; c < 5; ++c) maxnc = max(maxnc, st[c + 1] - st[c]);
     // run-time indexed copy in shared memory (misc[8..13] of this scale's
-    // buffer): every thread stores the same values before its own reads, so no
-    // barrier is needed; one LDS replaces a 5-deep select chain per lookup
+    // buffer): one LDS replaces a 5-deep select chain per lookup
     int* sts = misc + 8;
-#pragma unroll
-    for (int c = 0; c < 6; ++c) sts[c] = st[c];
+    if (tid < 6) sts[tid] = st[0] * (tid == 0) + st[1] * (tid == 1) + st[2] * (tid == 2) + st[3] * (tid == 3) +
+                            st[4] * (tid == 4) + st[5] * (tid == 5);
+    __syncthreads();
     const int ub = kmin - 1;        // lattice index of ring column 0
     const int sw = kmax - kmin + 3; // ring columns in use
     const double wm1 = (double)(w - 1), hm1 = (double)(h - 1);
@@ -858,6 +863,16 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 }
             }
             if (cell < ncells && lmin < (1 << 20)) atomicMin(&S.cellmin[(npass & 1) * 32 + cell], lmin);
+#ifdef DSIFT_NONDET_TEST_HOOK
+            if (a.nondet && cell < ncells) {   // order-fragile: float atomics in scheduling order
+                const int Rl = Ra + cell / 5, Cl = cell % 5 - 1;
+                for (int e = 0; e < 32; ++e) {
+                    const int row = Rl + (e >> 4), col = Cl + ((e >> 3) & 1);
+                    if (row >= 0 && row < kDescCells && col >= 0 && col < kDescCells && my[e * 16] != 0.0)
+                        atomicAdd(&raw_out[(row * kDescCells + col) * kDescOrients + (e & 7)], (float)my[e * 16]);
+                }
+            }
+#endif
         }
         kchain = max(kchain, (int)((float)((vb - va + 1) * maxnc) * (1.0f / (float)P)) + 1);   // >= ceil(./P): a bound
         ++npass;
@@ -884,6 +899,12 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         ok = (flo == fhi);
         res = flo;
     }
+#ifdef DSIFT_NONDET_TEST_HOOK
+    if (a.nondet) {
+        __syncthreads();
+        return true;   // raw_out holds the atomically accumulated histogram
+    }
+#endif
     raw_out[tid] = res;
     return ok && !a.force_slow;
 }

@@ -56,7 +56,11 @@ def main(argv=None) -> int:
     ap.add_argument("--runs", type=int, default=10)
     ap.add_argument("--batches", default="1,2,4,8")
     ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--library", help="another build of libdsift (the test-only negative control)")
     args = ap.parse_args(argv)
+    if args.library:
+        from . import load_library
+        load_library(args.library)
     if args.synthetic:
         w, h = (int(v) for v in args.synthetic.lower().split("x"))
         import torch
