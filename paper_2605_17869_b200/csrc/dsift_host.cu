@@ -236,7 +236,7 @@ struct dsift_ctx {
     int batch = 0;            // images in the current pyramid
     PyramidDesc pyr{};
     DevBuf det_aux, ori_aux, match_in, match_scratch, match_best, geom_in, geom_scratch, geom_out;
-    DevBuf pyramid, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps, sort_work, scratch,
+    DevBuf pyramid, blur_flags, counters, det_states, ori_states, det_kps, det_cand, ori_kps, sorted_kps, sort_work, scratch,
         stage_kps, stage_out, trig, slow, ref_states, keep, stage_in;
     long long cap_det = 0, cap_ori = 0;
     long long launches = 0;
@@ -291,6 +291,23 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
     const Plan& p = c->plan;
     const PyramidDesc& d = c->pyr;
     const int s = p.s;
+    // per-level "every value a positive normal >= 2^-100" flags (0 = yes), set by
+    // the producing kernel and read by the consumer (ALU widening); only levels
+    // whose producer checks (radius <= 16) are handed on
+    c->blur_flags.ensure(sizeof(int) * (size_t)p.n_oct * (s + 3));
+    int* flags = c->blur_flags.as<int>();
+    cuda_check(cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)p.n_oct * (s + 3), c->stream), "memset flags");
+    std::vector<char> checked((size_t)p.n_oct * (s + 3), 0);
+    auto flag_of = [&](int o, int i) { return flags + o * (s + 3) + i; };
+    // the strip kernel's source map: 3-D {w, h, batch}, box {kInW, 32, 1} (stride es)
+    auto set_map = [&](BlurArgs& a, int R, uint32_t es) {
+        const int bw = blur_strip_box_w(R);
+        a.use_tma = bw > 0 && tma_encode_3d_f32(&a.src_map, a.src, (uint64_t)a.src_w, (uint64_t)a.src_h,
+                                                  (uint64_t)c->batch, (uint64_t)a.src_pitch,
+                                                  (uint64_t)a.src_img_stride, (uint32_t)bw * es, 32u * es, 1u, es)
+                        ? 1 : 0;
+        if (!a.use_tma) fprintf(stderr, "DBG strip map failed R=%d w=%d h=%d pitch=%d bw=%d\n", R, a.src_w, a.src_h, a.src_pitch, bw);
+    };
     for (int o = 0; o < p.n_oct; ++o) {
         const OctaveDesc& od = d.oct[o];
         const long long gstride = d.gauss_img_stride(o), dstride = d.dog_img_stride(o);
@@ -311,8 +328,13 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
             a.h = od.h;
             a.pitch = od.pitch;
             fill_taps(a, p.bridge);
-            cuda_check(launch_blur(a, p.up ? kModeUpsample : kModeRaw, (int)p.bridge.size() / 2, c->batch,
-                                   c->stream), "bridge blur");
+            const int R = (int)p.bridge.size() / 2;
+            if (R <= 16) {
+                a.dst_flag = flag_of(0, 0);
+                checked[0] = 1;
+            }
+            if (!p.up) set_map(a, R, 1);
+            cuda_check(launch_blur(a, p.up ? kModeUpsample : kModeRaw, R, c->batch, c->stream), "bridge blur");
             ++c->launches;
             first_level = 1;
         } else {
@@ -333,8 +355,14 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
             a.h = od.h;
             a.pitch = od.pitch;
             fill_taps(a, p.inc[0]);
-            cuda_check(launch_blur(a, kModeDecimate, (int)p.inc[0].size() / 2, c->batch, c->stream),
-                       "decimate blur");
+            const int R = (int)p.inc[0].size() / 2;
+            if (checked[(o - 1) * (s + 3) + s]) a.src_flag = flag_of(o - 1, s);
+            if (R <= 16) {
+                a.dst_flag = flag_of(o, 1);
+                checked[o * (s + 3) + 1] = 1;
+            }
+            // (the decimated source is gathered: a stride-2 TMA box is not used)
+            cuda_check(launch_blur(a, kModeDecimate, R, c->batch, c->stream), "decimate blur");
             ++c->launches;
             first_level = 2;
         }
@@ -353,12 +381,15 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
             a.h = od.h;
             a.pitch = od.pitch;
             fill_taps(a, p.inc[i - 1]);
-            cuda_check(launch_blur(a, kModeLevel, (int)p.inc[i - 1].size() / 2, c->batch, c->stream),
-                       "level blur");
+            const int R = (int)p.inc[i - 1].size() / 2;
+            if (checked[o * (s + 3) + i - 1]) a.src_flag = flag_of(o, i - 1);
+            if (R <= 16) {
+                a.dst_flag = flag_of(o, i);
+                checked[o * (s + 3) + i] = 1;
+            }
+            set_map(a, R, 1);
+            cuda_check(launch_blur(a, kModeLevel, R, c->batch, c->stream), "level blur");
             ++c->launches;
-        }
-        if (o == 0) {
-            // octave 0 has no DoG[0] from the bridge pass: it came with level 1 above.
         }
     }
 }
@@ -377,7 +408,7 @@ static unsigned detect_tiles(const PyramidDesc& d, int* base, int* per_image) {
 }
 
 bool tma_encode_3d_f32(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                       uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2) {
+                       uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t es01) {
     using Fn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                             const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -395,7 +426,7 @@ bool tma_encode_3d_f32(CUtensorMap* map, const float* base, uint64_t d0, uint64_
     const cuuint64_t dims[3] = {d0, d1, d2};
     const cuuint64_t strides[2] = {s1 * sizeof(float), s2 * sizeof(float)};
     const cuuint32_t box[3] = {b0, b1, b2};
-    const cuuint32_t es[3] = {1, 1, 1};
+    const cuuint32_t es[3] = {es01, es01, 1};
     return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;

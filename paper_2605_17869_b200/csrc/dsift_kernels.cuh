@@ -22,7 +22,15 @@ struct BlurArgs {
     long long seed_img_stride;
     int w, h, pitch;
     double taps[2 * kMaxRadius + 1];
+    // strip kernel: TMA map of the source level (3-D {w, h, batch}, box {kInW, 32, 1};
+    // DECIMATE: element stride 2 over the previous octave's level), valid iff use_tma
+    CUtensorMap src_map;
+    int use_tma;
+    const int* src_flag;   // nonzero: a source value is not a positive normal >= 2^-100 (null: unknown)
+    int* dst_flag;         // producer: set nonzero when an output is not one
 };
+// TMA box width (floats) of the strip kernel's source map for radius R (host side)
+int blur_strip_box_w(int R);
 cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStream_t st);
 
 struct DetectArgs {

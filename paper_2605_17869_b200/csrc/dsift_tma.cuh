@@ -45,8 +45,10 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 
 // Host: encode a 3-D float32 tiled map (dims / strides in elements; the
-// innermost stride is 1).  Returns false if the driver rejects the layout.
+// innermost stride is 1); es01 = traversal stride of the two inner dimensions
+// (the box then lands as b0/es01 x b1/es01).  Returns false if the driver
+// rejects the layout.
 bool tma_encode_3d_f32(CUtensorMap* map, const float* base, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1,
-                       uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2);
+                       uint64_t s2, uint32_t b0, uint32_t b1, uint32_t b2, uint32_t es01 = 1);
 
 }  // namespace dsift

@@ -31,6 +31,7 @@
 
 #include "dsift_common.cuh"
 #include "dsift_kernels.cuh"
+#include "dsift_tma.cuh"
 
 namespace dsift {
 
@@ -228,7 +229,8 @@ __device__ __forceinline__ void b2_hpass(const BlurArgs& a, float* sm) {
 // V pass: item = (column c, 8-row group), lanes along x; writes G and, for
 // LEVEL / DECIMATE, DoG (and the DECIMATE seed = this octave's G[0]).
 template <int R, int MODE, bool kAlu>
-__device__ __forceinline__ void b2_vpass(const BlurArgs& a, const float* sm, int b, int x0, int y0) {
+__device__ __forceinline__ bool b2_vpass(const BlurArgs& a, const float* sm, int b, int x0, int y0) {
+    bool ok = true;   // every output a positive normal >= 2^-100 (the consumer's ALU widen)
     using G = B2Geom<R>;
     const int w = a.w, h = a.h, pitch = a.pitch;
     const float* __restrict__ src = a.src + b * a.src_img_stride;
@@ -262,6 +264,7 @@ __device__ __forceinline__ void b2_vpass(const BlurArgs& a, const float* sm, int
                 const int y = yb + j;
                 if (y < h) {
                     const float g = (float)acc[j];
+                    ok &= (unsigned)(__float_as_uint(g) - 0x0d800000u) < (0x7f800000u - 0x0d800000u);
                     const long long off = ob + j * pitch;
                     dp[j * pitch] = g;
                     // DoG[i-1] = G[i] - G[i-1] (scalespace.cpp:209); G[i-1] was just read (L2)
@@ -277,6 +280,7 @@ __device__ __forceinline__ void b2_vpass(const BlurArgs& a, const float* sm, int
             }
         }
     }
+    return ok;
 }
 
 template <int R, int MODE>
@@ -387,13 +391,346 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
             alu_ok &= (__float_as_int(v) >= 0x0d800000) & (__float_as_int(v) < 0x7f800000);
         }
     }
+    bool out_ok;
     if (__syncthreads_and(alu_ok)) {
         b2_hpass<R, true>(a, sm2);
-        b2_vpass<R, MODE, true>(a, sm2, b, x0, y0);
+        out_ok = b2_vpass<R, MODE, true>(a, sm2, b, x0, y0);
     } else {
         b2_hpass<R, false>(a, sm2);
-        b2_vpass<R, MODE, false>(a, sm2, b, x0, y0);
+        out_ok = b2_vpass<R, MODE, false>(a, sm2, b, x0, y0);
     }
+    if (!__syncthreads_and(out_ok) && a.dst_flag && threadIdx.x == 0) atomicOr(a.dst_flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// Strip kernel (LEVEL, RAW and DECIMATE modes).
+//
+// A CTA owns a 32-column strip of one image over a segment of rows and slides
+// down it 32 rows per step, so every horizontal-pass row is computed once per
+// segment (64x64 tiles recompute 2R halo rows per tile: +15% DFMA):
+//   1. the step's 32 new input rows (32 + 2R columns) arrive by TMA in a
+//      double-buffered float stage, issued one step ahead (decimation is a
+//      TMA element stride of 2); border strips and border rows are gathered
+//      with reflect-101 instead (scalespace.cpp:41-48);
+//   2. H pass: thread (row, 8-column segment) forms 8 outputs, each the
+//      left-to-right FP64 tap sum rounded to float (scalespace.cpp:63-86),
+//      stored as FP64 in a ring of >= 32 + 2R rows;
+//   3. V pass: thread (column pair, 4-row group) forms 8 outputs from the
+//      ring (scalespace.cpp:88-109) and writes G, DoG and the DECIMATE seed
+//      with 8-byte stores.
+// Inputs are widened to FP64 on the integer pipe when the producer of the
+// level flagged every value a positive normal >= 2^-100 (then every tmp
+// value is one too); otherwise by the conversion unit.
+// ---------------------------------------------------------------------------
+constexpr int kSW = 32, kSR = 32, kS3Threads = 128;
+
+template <int R>
+struct S3 {
+    static constexpr int kLen = 2 * R + 1;
+    static constexpr int kWinN = 8 + 2 * R;                       // inputs of 8 outputs
+    static constexpr int kM = (4 - (R & 3)) & 3;                  // x0 - R - kM = 0 (mod 4)
+    static constexpr int kInW0 = ((kSW + 2 * R + kM + 3) / 4) * 4;
+    // staged columns (TMA box width): an odd number of 16-byte chunks per row,
+    // so the 8 rows of a quarter-warp's LDS.128 fall in 8 different bank groups
+    static constexpr int kInW = ((kInW0 / 4) & 1) ? kInW0 : kInW0 + 4;
+    static constexpr int kNV = (kM + kWinN + 3) / 4;              // float4 reads per H window
+    static constexpr int kRS = (kSR + 2 * R + 3) / 4 * 4;         // ring rows (a multiple of 4)
+    static constexpr int kTP = kSW + 2;                           // ring pitch (doubles), = 2 (mod 16)
+    static constexpr size_t kStageBytes = sizeof(float) * (size_t)kSR * kInW;   // one TMA box
+    static constexpr size_t kSmem = 2 * kStageBytes + sizeof(double) * (size_t)kRS * kTP + 128;
+};
+
+__device__ __forceinline__ int reflect_fast(int p, int n) {
+    return ((unsigned)p < (unsigned)n) ? p : reflect101(p, n);
+}
+
+// a positive normal float >= 2^-100, finite
+__device__ __forceinline__ bool alu_widenable(float v) {
+    return (unsigned)(__float_as_uint(v) - 0x0d800000u) < (0x7f800000u - 0x0d800000u);
+}
+
+template <bool kAlu>
+__device__ __forceinline__ double s3_widen(float x) {
+    if (kAlu) return widen_pos_normal(x);
+    return (double)x;
+}
+
+// Gather virtual rows [t0, t0 + n) of the level's input (columns [xs, xs + kInW))
+// with reflect-101 into a float stage.
+template <int R, int MODE>
+__device__ __forceinline__ void s3_gather(const BlurArgs& a, const float* __restrict__ src, float* stg, int t0, int n,
+                                          int xs) {
+    using G = S3<R>;
+    for (int q = threadIdx.x; q < n * G::kInW; q += kS3Threads) {
+        const int r = q / G::kInW, c = q - r * G::kInW;
+        const int y = reflect_fast(t0 + r, a.h), x = reflect_fast(xs + c, a.w);
+        stg[q] = (MODE == kModeDecimate) ? __ldg(src + (long long)(2 * y) * a.src_pitch + 2 * x)
+                                         : __ldg(src + (long long)y * a.src_pitch + x);
+    }
+}
+
+// H pass over n staged rows; their ring slot is (k0 + row) mod RS.
+template <int R, bool kAlu>
+__device__ __forceinline__ void s3_hpass(const BlurArgs& a, const float* stg, double* ring, int n, int k0) {
+    using G = S3<R>;
+    const int seg = threadIdx.x >> 5, r = threadIdx.x & 31;   // a warp = 32 rows of one segment
+    if (r >= n) return;
+    const float4* wp = reinterpret_cast<const float4*>(stg + r * G::kInW + 8 * seg);
+    float win[4 * G::kNV];
+#pragma unroll
+    for (int q = 0; q < G::kNV; ++q) {
+        const float4 t = wp[q];
+        win[4 * q] = t.x;
+        win[4 * q + 1] = t.y;
+        win[4 * q + 2] = t.z;
+        win[4 * q + 3] = t.w;
+    }
+    double acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+#pragma unroll
+    for (int e = 0; e < G::kWinN; ++e) {
+        const double x = s3_widen<kAlu>(win[G::kM + e]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int t = e - j;
+            if (t >= 0 && t < G::kLen) acc[j] = __fma_rn(a.taps[t], x, acc[j]);
+        }
+    }
+    int k = k0 + r;
+    if (k >= G::kRS) k -= G::kRS;
+    double2* o0 = reinterpret_cast<double2*>(ring + k * G::kTP + 8 * seg);
+#pragma unroll
+    for (int j = 0; j < 8; j += 2)   // the float tmp of scalespace.cpp:86, kept as FP64
+        o0[j / 2] = make_double2(s3_widen<kAlu>((float)acc[j]), s3_widen<kAlu>((float)acc[j + 1]));
+}
+
+template <int R, int MODE, bool kAlu>
+__device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, float* stage0, double* ring,
+                                                uint64_t* bar) {
+    using G = S3<R>;
+    const int b = blockIdx.z;
+    const int x0 = blockIdx.x * kSW;
+    const int y_begin = blockIdx.y * seg_h;
+    const int w = a.w, h = a.h, pitch = a.pitch, sp = a.src_pitch;
+    const int y_end = min(h, y_begin + seg_h);
+    const float* __restrict__ src = a.src + b * a.src_img_stride;
+    const int xs = x0 - R - G::kM;
+    const bool strip_in = a.use_tma && xs >= 0 && xs + G::kInW <= w;
+    constexpr int kStageF = (int)(G::kStageBytes / sizeof(float));
+    // rows [t0, t0 + n) come by TMA iff they are inside the image (no reflection)
+    auto issue = [&](int t0, int n, int buf) -> bool {
+        float* st = stage0 + buf * kStageF;
+        if (strip_in && t0 >= 0 && t0 + n <= h) {
+            if (threadIdx.x == 0) {
+                mbar_arrive_expect_tx(&bar[buf], (unsigned)G::kStageBytes);
+                const int ds = (MODE == kModeDecimate) ? 2 : 1;
+                tma_load_3d(st, &a.src_map, ds * xs, ds * t0, b, &bar[buf]);
+            }
+            return true;
+        }
+        s3_gather<R, MODE>(a, src, st, t0, n, xs);
+        return false;
+    };
+    float* __restrict__ dst = a.dst + b * a.dst_img_stride;
+    float* __restrict__ dog = a.dog ? a.dog + b * a.dog_img_stride : nullptr;
+    float* __restrict__ seed = (MODE == kModeDecimate) ? a.seed + b * a.seed_img_stride : nullptr;
+    // V-pass thread: column pair cp (x = x0 + 2cp, +1), 4-row group g
+    const int cp = threadIdx.x & 15, g = threadIdx.x >> 4;
+    const int xv = x0 + 2 * cp;
+    bool out_ok = true;   // every output a positive normal >= 2^-100 (the consumer's ALU widen)
+
+    // prologue: virtual rows [y_begin - R, y_begin + R) through stage 1
+    unsigned ph0 = 0u, ph1 = 0u;
+    bool tma0, tma1;
+    tma1 = issue(y_begin - R, 2 * R, 1);
+    tma0 = issue(y_begin + R, min(kSR, y_end - y_begin), 0);   // step 0's rows
+    __syncthreads();
+    if (tma1) {
+        mbar_wait(&bar[1], ph1);
+        ph1 ^= 1u;
+    }
+    s3_hpass<R, kAlu>(a, stage0 + kStageF, ring, 2 * R, 0);
+    int kn = 2 * R;   // ring slot of the next new row
+    int kv = 4 * g;   // ring slot of this thread's first V-window row
+    int cur = 0;
+    for (int ys = y_begin; ys < y_end; ys += kSR) {
+        const int nnew = min(kSR, y_end - ys);
+        __syncthreads();   // the previous H pass has read the other stage buffer
+        if (ys + kSR < y_end) {
+            const bool t = issue(ys + kSR + R, min(kSR, y_end - ys - kSR), cur ^ 1);
+            if (cur) tma0 = t; else tma1 = t;
+        }
+        // the previous level's values at this thread's outputs (DoG / seed),
+        // loaded now so their latency hides behind the passes
+        const int yb = ys + 4 * g;
+        const bool full = x0 + kSW <= w && ys + kSR <= y_end;   // CTA-uniform: no edge checks
+        float2 prev[4];
+        if (MODE == kModeLevel || MODE == kModeDecimate) {
+            const int xa = min(xv, w - 1), xb = min(xv + 1, w - 1);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int y = min(yb + j, y_end - 1);
+                if (MODE == kModeLevel) {
+                    const float* p = src + (long long)y * sp;
+                    prev[j] = full ? __ldg(reinterpret_cast<const float2*>(p + xv)) : make_float2(__ldg(p + xa), __ldg(p + xb));
+                } else {
+                    const float* p = src + (long long)(2 * y) * sp;
+                    if (full) {
+                        const float4 q = __ldg(reinterpret_cast<const float4*>(p + 2 * xv));
+                        prev[j] = make_float2(q.x, q.z);
+                    } else {
+                        prev[j] = make_float2(__ldg(p + 2 * xa), __ldg(p + 2 * xb));
+                    }
+                }
+            }
+        }
+        const bool tcur = cur ? tma1 : tma0;
+        if (!tcur) {
+            __syncthreads();   // gathered rows: visible to all threads
+        } else if (cur) {
+            mbar_wait(&bar[1], ph1);
+            ph1 ^= 1u;
+        } else {
+            mbar_wait(&bar[0], ph0);
+            ph0 ^= 1u;
+        }
+        s3_hpass<R, kAlu>(a, stage0 + cur * kStageF, ring, nnew, kn);
+        kn += nnew;
+        if (kn >= G::kRS) kn -= G::kRS;
+        cur ^= 1;
+        __syncthreads();
+        // V pass: columns xv, xv + 1, rows yb .. yb + 3; the window's ring rows
+        // kv .. kv + 4 + 2R - 1 (mod RS): kv and RS are multiples of 4, so each
+        // aligned block of 4 rows wraps as a whole
+        if (4 * g < nnew) {
+            const double* colp = ring + kv * G::kTP + 2 * cp;
+            double acc[8];   // [row j][column k] = acc[2j + k]
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+            constexpr int kWinV = 4 + 2 * R;
+#pragma unroll
+            for (int e0 = 0; e0 < kWinV; e0 += 4) {
+                const double* cb = (kv + e0 < G::kRS) ? colp + e0 * G::kTP : colp + (e0 - G::kRS) * G::kTP;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const int e = e0 + i;
+                    if (e < kWinV) {
+                        const double2 v = *reinterpret_cast<const double2*>(cb + i * G::kTP);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const int t = e - j;
+                            if (t >= 0 && t < G::kLen) {
+                                acc[2 * j] = __fma_rn(a.taps[t], v.x, acc[2 * j]);
+                                acc[2 * j + 1] = __fma_rn(a.taps[t], v.y, acc[2 * j + 1]);
+                            }
+                        }
+                    }
+                }
+            }
+            float* dp = dst + (long long)yb * pitch + xv;
+            float* gp = dog ? dog + (long long)yb * pitch + xv : nullptr;
+            float* sd = (MODE == kModeDecimate) ? seed + (long long)yb * pitch + xv : nullptr;
+            if (full) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const float2 gv = make_float2((float)acc[2 * j], (float)acc[2 * j + 1]);
+                    out_ok &= alu_widenable(gv.x) & alu_widenable(gv.y);
+                    *reinterpret_cast<float2*>(dp + j * pitch) = gv;
+                    if (MODE == kModeLevel || MODE == kModeDecimate) {
+                        // DoG[i-1] = G[i] - G[i-1] (scalespace.cpp:209); DECIMATE also
+                        // writes this octave's G[0] (scalespace.cpp:133-142)
+                        if (MODE == kModeDecimate) *reinterpret_cast<float2*>(sd + j * pitch) = prev[j];
+                        if (gp) *reinterpret_cast<float2*>(gp + j * pitch) = make_float2(gv.x - prev[j].x, gv.y - prev[j].y);
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (yb + j < y_end) {
+#pragma unroll
+                        for (int k = 0; k < 2; ++k) {
+                            if (xv + k < w) {
+                                const float gv = (float)acc[2 * j + k];
+                                const float pv = k ? prev[j].y : prev[j].x;
+                                out_ok &= alu_widenable(gv);
+                                dp[j * pitch + k] = gv;
+                                if (MODE == kModeDecimate) sd[j * pitch + k] = pv;
+                                if ((MODE == kModeLevel || MODE == kModeDecimate) && gp) gp[j * pitch + k] = gv - pv;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        kv += kSR;
+        if (kv >= G::kRS) kv -= G::kRS;
+    }
+    if (!__syncthreads_and(out_ok) && a.dst_flag && threadIdx.x == 0) atomicOr(a.dst_flag, 1);
+}
+
+template <int R, int MODE>
+__global__ void __launch_bounds__(kS3Threads, 6)
+blur_strip_kernel(const __grid_constant__ BlurArgs a, int seg_h) {
+    using G = S3<R>;
+    extern __shared__ __align__(128) unsigned char sm3_raw[];
+    // 128-byte aligned TMA destination; offset from the array itself so the
+    // compiler keeps every access in the shared window (LDS, not generic LD)
+    unsigned char* base = sm3_raw + ((128u - (smem_u32(sm3_raw) & 127u)) & 127u);
+    float* stage0 = reinterpret_cast<float*>(base);                          // [2][kSR][kInW] (TMA boxes)
+    double* ring = reinterpret_cast<double*>(base + 2 * G::kStageBytes);    // [kRS][kTP]
+    __shared__ __align__(8) uint64_t bar[2];
+    if (threadIdx.x == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+    }
+    __syncthreads();
+    // ALU widening needs every source value to be a positive normal >= 2^-100
+    // (flag written by the level's producer; the input image has none)
+    const bool alu = a.src_flag != nullptr && *a.src_flag == 0;
+    if (alu) blur_strip_body<R, MODE, true>(a, seg_h, stage0, ring, bar);
+    else blur_strip_body<R, MODE, false>(a, seg_h, stage0, ring, bar);
+}
+
+// rows per CTA segment: long segments amortise the 2R-row prologue, short ones
+// give small octaves enough CTAs (>= ~2 waves of 6 per SM)
+static int s3_seg_h(int w, int h, int batch) {
+    const long long strips = (long long)((w + kSW - 1) / kSW) * batch;
+    int nseg = std::max(1, (h + 256) / 512);
+    const long long want = 148LL * 6 * 2;
+    while ((long long)nseg * strips < want && (h + nseg) / (nseg + 1) >= 64) ++nseg;
+    const int per = (h + nseg - 1) / nseg;
+    return ((per + kSR - 1) / kSR) * kSR;
+}
+
+int blur_strip_box_w(int R) {
+    switch (R) {
+#define DSIFT_BW(r) case r: return S3<r>::kInW;
+        DSIFT_BW(1) DSIFT_BW(2) DSIFT_BW(3) DSIFT_BW(4) DSIFT_BW(5) DSIFT_BW(6) DSIFT_BW(7) DSIFT_BW(8)
+        DSIFT_BW(9) DSIFT_BW(10) DSIFT_BW(11) DSIFT_BW(12) DSIFT_BW(13) DSIFT_BW(14) DSIFT_BW(15) DSIFT_BW(16)
+#undef DSIFT_BW
+        default: return 0;
+    }
+}
+
+template <int MODE>
+static cudaError_t launch_strip(const BlurArgs& a, int R, int batch, cudaStream_t st) {
+    const int seg_h = s3_seg_h(a.w, a.h, batch);
+    const dim3 grid((a.w + kSW - 1) / kSW, (a.h + seg_h - 1) / seg_h, batch);
+    size_t smem = 0;
+    void (*fn)(BlurArgs, int) = nullptr;
+    switch (R) {
+#define DSIFT_R3(r) case r: fn = blur_strip_kernel<r, MODE>; smem = S3<r>::kSmem; break;
+        DSIFT_R3(1) DSIFT_R3(2) DSIFT_R3(3) DSIFT_R3(4) DSIFT_R3(5) DSIFT_R3(6) DSIFT_R3(7) DSIFT_R3(8)
+        DSIFT_R3(9) DSIFT_R3(10) DSIFT_R3(11) DSIFT_R3(12) DSIFT_R3(13) DSIFT_R3(14) DSIFT_R3(15)
+        DSIFT_R3(16)
+#undef DSIFT_R3
+        default: return cudaErrorInvalidValue;
+    }
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fn<<<grid, kS3Threads, smem, st>>>(a, seg_h);
+    return cudaGetLastError();
 }
 
 template <int MODE>
@@ -419,11 +756,11 @@ static cudaError_t launch_v2(const BlurArgs& a, int R, int batch, cudaStream_t s
 cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStream_t st) {
     const bool tiled = R >= 1 && R <= 16;
     switch (mode) {
-        case kModeLevel: return tiled ? launch_v2<kModeLevel>(a, R, batch, st) : launch_any<kModeLevel>(a, R, batch, st);
-        case kModeRaw: return tiled ? launch_v2<kModeRaw>(a, R, batch, st) : launch_any<kModeRaw>(a, R, batch, st);
+        case kModeLevel: return tiled ? launch_strip<kModeLevel>(a, R, batch, st) : launch_any<kModeLevel>(a, R, batch, st);
+        case kModeRaw: return tiled ? launch_strip<kModeRaw>(a, R, batch, st) : launch_any<kModeRaw>(a, R, batch, st);
         case kModeUpsample:
             return tiled ? launch_v2<kModeUpsample>(a, R, batch, st) : launch_any<kModeUpsample>(a, R, batch, st);
-        default: return tiled ? launch_v2<kModeDecimate>(a, R, batch, st) : launch_any<kModeDecimate>(a, R, batch, st);
+        default: return tiled ? launch_strip<kModeDecimate>(a, R, batch, st) : launch_any<kModeDecimate>(a, R, batch, st);
     }
 }
 
