@@ -306,7 +306,6 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
                                                   (uint64_t)c->batch, (uint64_t)a.src_pitch,
                                                   (uint64_t)a.src_img_stride, (uint32_t)bw * es, 32u * es, 1u, es)
                         ? 1 : 0;
-        if (!a.use_tma) fprintf(stderr, "DBG strip map failed R=%d w=%d h=%d pitch=%d bw=%d\n", R, a.src_w, a.src_h, a.src_pitch, bw);
     };
     for (int o = 0; o < p.n_oct; ++o) {
         const OctaveDesc& od = d.oct[o];

@@ -438,6 +438,9 @@ struct S3 {
     static constexpr int kTP = kSW + 2;                           // ring pitch (doubles), = 2 (mod 16)
     static constexpr size_t kStageBytes = sizeof(float) * (size_t)kSR * kInW;   // one TMA box
     static constexpr size_t kSmem = 2 * kStageBytes + sizeof(double) * (size_t)kRS * kTP + 128;
+    // UPSAMPLE: the half-resolution patch behind one step's staged rows, as FP64
+    static constexpr int kPW = kInW / 2 + 2, kPH = kSR / 2 + 2;
+    static constexpr size_t kPatchBytes = sizeof(double) * (size_t)kPW * kPH;
 };
 
 __device__ __forceinline__ int reflect_fast(int p, int n) {
@@ -456,17 +459,61 @@ __device__ __forceinline__ double s3_widen(float x) {
 }
 
 // Gather virtual rows [t0, t0 + n) of the level's input (columns [xs, xs + kInW))
-// with reflect-101 into a float stage.
+// into a float stage: reflect-101 at the image border (scalespace.cpp:41-48),
+// the 2x upsample formed on the fly (UPSAMPLE), even samples (DECIMATE).
+// Returns whether every staged value this thread wrote is ALU-widenable.
 template <int R, int MODE>
-__device__ __forceinline__ void s3_gather(const BlurArgs& a, const float* __restrict__ src, float* stg, int t0, int n,
-                                          int xs) {
+__device__ __forceinline__ bool s3_gather(const BlurArgs& a, const float* __restrict__ src, float* stg, int t0, int n,
+                                          int xs, double* patch) {
     using G = S3<R>;
+    bool ok = true;
+    const bool inner = xs >= 0 && xs + G::kInW <= a.w && t0 >= 0 && t0 + n <= a.h;
+    if (MODE == kModeDecimate && inner && ((a.src_pitch | (int)(a.src_img_stride & 3)) & 3) == 0) {
+        // interior rows of the previous octave's level: even samples of
+        // 16-byte loads (decimate2x, scalespace.cpp:133-142), two per staged float4
+        constexpr int kV = G::kInW / 4;
+        for (int q = threadIdx.x; q < n * kV; q += kS3Threads) {
+            const int r = q / kV, c4 = q - r * kV;
+            const float4* p =
+                reinterpret_cast<const float4*>(src + (long long)(2 * (t0 + r)) * a.src_pitch + 2 * xs) + 2 * c4;
+            const float4 u0 = __ldg(p), u1 = __ldg(p + 1);
+            const float4 v = make_float4(u0.x, u0.z, u1.x, u1.z);
+            ok &= alu_widenable(v.x) & alu_widenable(v.y) & alu_widenable(v.z) & alu_widenable(v.w);
+            reinterpret_cast<float4*>(stg)[q] = v;
+        }
+        return ok;
+    }
+    if (MODE == kModeUpsample && inner) {
+        // upsample2x (scalespace.cpp:113-131) from a staged half-resolution patch:
+        // patch row r holds source row min(py0 + r, src_h - 1), so the reference's
+        // edge clamp of the odd neighbour is the patch's next row / column
+        const int py0 = t0 >> 1, px0 = xs >> 1;
+        __syncthreads();   // the previous gather has finished reading the patch
+        for (int q = threadIdx.x; q < G::kPH * G::kPW; q += kS3Threads) {
+            const int r = q / G::kPW, c = q - r * G::kPW;
+            const int y = min(py0 + r, a.src_h - 1), x = min(px0 + c, a.src_w - 1);
+            patch[q] = (double)__ldg(src + (long long)y * a.src_pitch + x);
+        }
+        __syncthreads();
+        for (int q = threadIdx.x; q < n * G::kInW; q += kS3Threads) {
+            const int r = q / G::kInW, c = q - r * G::kInW;
+            const int gy = t0 + r, gx = xs + c;
+            const double* p0 = patch + ((gy >> 1) - py0) * G::kPW + ((gx >> 1) - px0);
+            const double* p1 = p0 + ((gy & 1) ? G::kPW : 0);
+            const int dx = gx & 1;
+            const float v = (float)(0.25 * (((p0[0] + p0[dx]) + p1[0]) + p1[dx]));
+            ok &= alu_widenable(v);
+            stg[q] = v;
+        }
+        return ok;
+    }
     for (int q = threadIdx.x; q < n * G::kInW; q += kS3Threads) {
         const int r = q / G::kInW, c = q - r * G::kInW;
-        const int y = reflect_fast(t0 + r, a.h), x = reflect_fast(xs + c, a.w);
-        stg[q] = (MODE == kModeDecimate) ? __ldg(src + (long long)(2 * y) * a.src_pitch + 2 * x)
-                                         : __ldg(src + (long long)y * a.src_pitch + x);
+        const float v = fetch_input<MODE>(a, src, reflect_fast(xs + c, a.w), reflect_fast(t0 + r, a.h));
+        ok &= alu_widenable(v);
+        stg[q] = v;
     }
+    return ok;
 }
 
 // H pass over n staged rows; their ring slot is (k0 + row) mod RS.
@@ -505,9 +552,9 @@ __device__ __forceinline__ void s3_hpass(const BlurArgs& a, const float* stg, do
         o0[j / 2] = make_double2(s3_widen<kAlu>((float)acc[j]), s3_widen<kAlu>((float)acc[j + 1]));
 }
 
-template <int R, int MODE, bool kAlu>
+template <int R, int MODE>
 __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, float* stage0, double* ring,
-                                                uint64_t* bar) {
+                                                double* patch, uint64_t* bar, bool alu_level) {
     using G = S3<R>;
     const int b = blockIdx.z;
     const int x0 = blockIdx.x * kSW;
@@ -518,18 +565,18 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
     const int xs = x0 - R - G::kM;
     const bool strip_in = a.use_tma && xs >= 0 && xs + G::kInW <= w;
     constexpr int kStageF = (int)(G::kStageBytes / sizeof(float));
-    // rows [t0, t0 + n) come by TMA iff they are inside the image (no reflection)
-    auto issue = [&](int t0, int n, int buf) -> bool {
+    // rows [t0, t0 + n) come by TMA iff they are inside the image (no
+    // reflection); gathered rows report whether they are ALU-widenable
+    auto issue = [&](int t0, int n, int buf, bool& gok) -> bool {
         float* st = stage0 + buf * kStageF;
         if (strip_in && t0 >= 0 && t0 + n <= h) {
             if (threadIdx.x == 0) {
                 mbar_arrive_expect_tx(&bar[buf], (unsigned)G::kStageBytes);
-                const int ds = (MODE == kModeDecimate) ? 2 : 1;
-                tma_load_3d(st, &a.src_map, ds * xs, ds * t0, b, &bar[buf]);
+                tma_load_3d(st, &a.src_map, xs, t0, b, &bar[buf]);
             }
             return true;
         }
-        s3_gather<R, MODE>(a, src, st, t0, n, xs);
+        gok = s3_gather<R, MODE>(a, src, st, t0, n, xs, patch);
         return false;
     };
     float* __restrict__ dst = a.dst + b * a.dst_img_stride;
@@ -542,15 +589,17 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
 
     // prologue: virtual rows [y_begin - R, y_begin + R) through stage 1
     unsigned ph0 = 0u, ph1 = 0u;
-    bool tma0, tma1;
-    tma1 = issue(y_begin - R, 2 * R, 1);
-    tma0 = issue(y_begin + R, min(kSR, y_end - y_begin), 0);   // step 0's rows
+    bool tma0, tma1, gok0 = true, gok1 = true;
+    tma1 = issue(y_begin - R, 2 * R, 1, gok1);
+    const bool alu_pro = tma1 ? alu_level : (bool)__syncthreads_and(gok1);
+    tma0 = issue(y_begin + R, min(kSR, y_end - y_begin), 0, gok0);   // step 0's rows
     __syncthreads();
     if (tma1) {
         mbar_wait(&bar[1], ph1);
         ph1 ^= 1u;
     }
-    s3_hpass<R, kAlu>(a, stage0 + kStageF, ring, 2 * R, 0);
+    if (alu_pro) s3_hpass<R, true>(a, stage0 + kStageF, ring, 2 * R, 0);
+    else s3_hpass<R, false>(a, stage0 + kStageF, ring, 2 * R, 0);
     int kn = 2 * R;   // ring slot of the next new row
     int kv = 4 * g;   // ring slot of this thread's first V-window row
     int cur = 0;
@@ -558,8 +607,8 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
         const int nnew = min(kSR, y_end - ys);
         __syncthreads();   // the previous H pass has read the other stage buffer
         if (ys + kSR < y_end) {
-            const bool t = issue(ys + kSR + R, min(kSR, y_end - ys - kSR), cur ^ 1);
-            if (cur) tma0 = t; else tma1 = t;
+            if (cur) tma0 = issue(ys + kSR + R, min(kSR, y_end - ys - kSR), 0, gok0);
+            else tma1 = issue(ys + kSR + R, min(kSR, y_end - ys - kSR), 1, gok1);
         }
         // the previous level's values at this thread's outputs (DoG / seed),
         // loaded now so their latency hides behind the passes
@@ -586,8 +635,9 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
             }
         }
         const bool tcur = cur ? tma1 : tma0;
+        bool alu_step = alu_level;
         if (!tcur) {
-            __syncthreads();   // gathered rows: visible to all threads
+            alu_step = __syncthreads_and(cur ? gok1 : gok0);   // gathered rows: visible to all threads
         } else if (cur) {
             mbar_wait(&bar[1], ph1);
             ph1 ^= 1u;
@@ -595,7 +645,8 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
             mbar_wait(&bar[0], ph0);
             ph0 ^= 1u;
         }
-        s3_hpass<R, kAlu>(a, stage0 + cur * kStageF, ring, nnew, kn);
+        if (alu_step) s3_hpass<R, true>(a, stage0 + cur * kStageF, ring, nnew, kn);
+        else s3_hpass<R, false>(a, stage0 + cur * kStageF, ring, nnew, kn);
         kn += nnew;
         if (kn >= G::kRS) kn -= G::kRS;
         cur ^= 1;
@@ -679,6 +730,7 @@ blur_strip_kernel(const __grid_constant__ BlurArgs a, int seg_h) {
     unsigned char* base = sm3_raw + ((128u - (smem_u32(sm3_raw) & 127u)) & 127u);
     float* stage0 = reinterpret_cast<float*>(base);                          // [2][kSR][kInW] (TMA boxes)
     double* ring = reinterpret_cast<double*>(base + 2 * G::kStageBytes);    // [kRS][kTP]
+    double* patch = ring + G::kRS * G::kTP;                                 // UPSAMPLE: [kPH][kPW]
     __shared__ __align__(8) uint64_t bar[2];
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -688,8 +740,7 @@ blur_strip_kernel(const __grid_constant__ BlurArgs a, int seg_h) {
     // ALU widening needs every source value to be a positive normal >= 2^-100
     // (flag written by the level's producer; the input image has none)
     const bool alu = a.src_flag != nullptr && *a.src_flag == 0;
-    if (alu) blur_strip_body<R, MODE, true>(a, seg_h, stage0, ring, bar);
-    else blur_strip_body<R, MODE, false>(a, seg_h, stage0, ring, bar);
+    blur_strip_body<R, MODE>(a, seg_h, stage0, ring, patch, bar, alu);
 }
 
 // rows per CTA segment: long segments amortise the 2R-row prologue, short ones
@@ -720,7 +771,8 @@ static cudaError_t launch_strip(const BlurArgs& a, int R, int batch, cudaStream_
     size_t smem = 0;
     void (*fn)(BlurArgs, int) = nullptr;
     switch (R) {
-#define DSIFT_R3(r) case r: fn = blur_strip_kernel<r, MODE>; smem = S3<r>::kSmem; break;
+#define DSIFT_R3(r) case r: fn = blur_strip_kernel<r, MODE>; \
+        smem = S3<r>::kSmem + (MODE == kModeUpsample ? S3<r>::kPatchBytes : 0); break;
         DSIFT_R3(1) DSIFT_R3(2) DSIFT_R3(3) DSIFT_R3(4) DSIFT_R3(5) DSIFT_R3(6) DSIFT_R3(7) DSIFT_R3(8)
         DSIFT_R3(9) DSIFT_R3(10) DSIFT_R3(11) DSIFT_R3(12) DSIFT_R3(13) DSIFT_R3(14) DSIFT_R3(15)
         DSIFT_R3(16)
@@ -758,7 +810,7 @@ cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStrea
     switch (mode) {
         case kModeLevel: return tiled ? launch_strip<kModeLevel>(a, R, batch, st) : launch_any<kModeLevel>(a, R, batch, st);
         case kModeRaw: return tiled ? launch_strip<kModeRaw>(a, R, batch, st) : launch_any<kModeRaw>(a, R, batch, st);
-        case kModeUpsample:
+        case kModeUpsample:   // the tiled kernel stages the half-resolution patch once per tile (faster here)
             return tiled ? launch_v2<kModeUpsample>(a, R, batch, st) : launch_any<kModeUpsample>(a, R, batch, st);
         default: return tiled ? launch_strip<kModeDecimate>(a, R, batch, st) : launch_any<kModeDecimate>(a, R, batch, st);
     }
