@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-extra-configs", action="store_true", help="skip the C4 and C1-latency legs")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="multi-rank control flow on CPU/gloo with the CPU oracle (tests; no GPU)")
     ap.add_argument("--e2e-steps", type=int, default=0, help="0 = same as --steps")
     return ap.parse_args()
 
@@ -350,6 +352,64 @@ def c1_latency_leg(ds, reps=20):
     return out
 
 
+# --------------------------------------------------------------------------- multi-rank plumbing
+def rank_sync(dist, device):
+    """(barrier, max_over_ranks) for the process group `dist` (None: one rank)."""
+    import torch
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=device)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    return barrier, max_over_ranks
+
+
+def run_dry(args, rank, world):
+    """--dry-run: the multi-rank control flow of the GPU arm on CPU / gloo, for
+    tests without a GPU: rank k extracts its contiguous shard (shard.shard_range)
+    of B * world tiny synthetic images with the CPU oracle standing in for the
+    device, the step is bracketed by barriers and timed as the max over ranks,
+    the results go to rank 0 through shard.gather_to_rank0, and rank 0 prints one
+    JSON line (marked dry_run; never a bench value)."""
+    import torch
+    import torch.distributed as dist
+
+    from oracle.oracle import KEYPOINT_DTYPE, Oracle
+    from paper_2605_17869_b200.shard import gather_to_rank0, shard_range
+
+    dist.init_process_group("gloo")
+    barrier, max_over_ranks = rank_sync(dist, "cpu")
+    port = Oracle("port")
+    B, W, H = args.batch, args.width, args.height
+    lo, hi = shard_range(B * world, world, rank)
+    imgs = [port.value_noise(W, H, SEED0 + i, 5, cells_for(W)) for i in range(lo, hi)]
+    for _ in range(args.warmup):
+        [port.extract(im) for im in imgs]
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = [port.extract(im) for im in imgs]
+    dt = max_over_ranks(time.perf_counter() - t0)
+    barrier()
+    kps = np.concatenate([k for k, _ in res]) if res else np.zeros(0, KEYPOINT_DTYPE)
+    des = np.concatenate([d for _, d in res]) if res else np.zeros((0, 128), np.float32)
+    got = gather_to_rank0(kps, des, np.array([len(k) for k, _ in res], np.int64))
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world, "steps": args.steps,
+                          "images_per_step": B * world, "value": B * world * args.steps / dt, "unit": "images/s",
+                          "gathered_keypoints": int(got[0].shape[0]), "gathered_counts": got[2].tolist(),
+                          "gathered_sha": __import__("hashlib").sha256(got[0].numpy().tobytes() +
+                                                                        got[1].numpy().tobytes()).hexdigest()}),
+              flush=True)
+    dist.destroy_process_group()
+
+
 # --------------------------------------------------------------------------- our arm
 def run_ours(args, rank, local_rank, world):
     import torch
@@ -360,17 +420,7 @@ def run_ours(args, rank, local_rank, world):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-
-    def barrier():
-        if dist:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if not dist:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    barrier, max_over_ranks = rank_sync(dist, "cuda")
 
     def sum_over_ranks(x):
         if not dist:
@@ -645,6 +695,9 @@ def main():
     rank, local_rank, world = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.dry_run:
+        run_dry(args, rank, world)
         return
     run_ours(args, rank, local_rank, world)
 

@@ -53,7 +53,10 @@ def _run_rank(rank, world, port_no, out_q):
     d = np.concatenate(descs) if descs else np.zeros((0, 128), np.float32)
     res = gather_to_rank0(k, d, np.array(counts, np.int64))
     if rank == 0:
-        out_q.put((res[0].tobytes(), res[1].tobytes(), res[2].tolist()))
+        gk = res[0].numpy().view(KEYPOINT_DTYPE).reshape(-1)
+        out_q.put((gk.tobytes(), res[1].numpy().tobytes(), res[2].tolist()))
+    else:
+        assert res is None
     dist.barrier()
     dist.destroy_process_group()
 
@@ -76,8 +79,8 @@ def test_assign_mixed_deterministic():
     assert max(loads) / min(loads) < 1.6
 
 
-@pytest.mark.parametrize("world", [2])
-def test_gloo_world2_gather_matches_single_process(world):
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_gloo_gather_matches_single_process(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port_no = _free_port()
