@@ -56,3 +56,12 @@ def test_compute_sanitizer_clean(tool):
     assert r.returncode == 0, out[-4000:]
     assert "sanitize workload ok" in out
     assert "ERROR SUMMARY: 0 errors" in out or "RACECHECK SUMMARY: 0 hazards" in out, out[-2000:]
+
+
+def test_gather_to_rank0_nccl_device_buffers():
+    # shard.gather_to_rank0 on the exported device tensors through NCCL (one
+    # rank on the one GPU: sizes all-gathered, rank-0 assembly on the device)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "native", "gather_nccl.py")], cwd=ROOT,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    assert "nccl gather ok" in r.stdout
