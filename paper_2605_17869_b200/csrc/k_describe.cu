@@ -353,7 +353,7 @@ __device__ __forceinline__ DescSmem carve_exact_smem(unsigned char* pbuf, const 
     S.pval = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * PW;
     S.pfo = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * PW;
     S.omask = reinterpret_cast<unsigned*>(pbuf); pbuf += sizeof(unsigned) * a.chunk_rows * kDescOrients * (PW >> 5);
-    pbuf = reinterpret_cast<unsigned char*>((reinterpret_cast<size_t>(pbuf) + 15) & ~size_t(15));
+    pbuf += (16u - ((unsigned)__cvta_generic_to_shared(pbuf) & 15u)) & 15u;   // 16-byte align, stays a shared pointer
     S.node = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * (kTreeDepth - 3) * kDescThreads;
     S.ring = reinterpret_cast<float*>(pbuf);
     return S;

@@ -99,7 +99,9 @@ __global__ void __launch_bounds__(kDetThreads, 4)
 detect_count_kernel(const __grid_constant__ DetectArgs a) {
     extern __shared__ __align__(128) float lv_raw[];
     // [s+2][34][kDetPitch], 128-byte aligned (TMA destination)
-    float* lv_s = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(lv_raw) + 127) & ~uintptr_t(127));
+    // 128-byte aligned TMA destination, offset from the array itself so every
+    // access stays in the shared window (LDS, not generic LD)
+    float* lv_s = lv_raw + (((128u - (smem_u32(lv_raw) & 127u)) & 127u) >> 2);
     __shared__ int warp_tot[kDetThreads / 32];
     const unsigned t = blockIdx.x;
     const int b = (int)(t / a.tiles_per_image);
