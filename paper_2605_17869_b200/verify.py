@@ -11,6 +11,7 @@ checks it against the reference's own digest).
 
     python -m paper_2605_17869_b200.verify IMAGE.pgm [--runs 10] [--batches 1,2,4,8]
     python -m paper_2605_17869_b200.verify --synthetic 640x480 --seed 0x5EED0000
+    python -m paper_2605_17869_b200.verify --sweep 10000    # C5: 10k mixed images, twice
 
 Prints one line per extraction (run, batch, digest) and a summary; exit code 0
 (one digest) or 3 (several), like the reference.
@@ -48,6 +49,48 @@ def digests_for(img: np.ndarray, runs: int, batches: list[int], cfg: SiftConfig 
     return out
 
 
+C5_SIZES = [(640, 480), (800, 600), (1000, 750), (1024, 768), (1280, 720), (1600, 1200), (1920, 1080),
+            (2048, 1536), (2560, 1440), (3840, 2160)]
+
+
+def c5_sweep_sizes(n: int, seed: int = 0xC5) -> list[tuple[int, int]]:
+    """resolutions of n images drawn by SplitMix64(seed) from
+    the ten 480p-4K sizes."""
+    s = seed & 0xFFFFFFFFFFFFFFFF
+    out = []
+    for _ in range(n):
+        s = (s + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
+        z = ((s ^ (s >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
+        out.append(C5_SIZES[(z ^ (z >> 31)) % len(C5_SIZES)])
+    return out
+
+
+def sweep_digests(n: int, batch: int, device: int = 0, cfg: SiftConfig | None = None,
+                  seed0: int = 0x5EED0000) -> list[str]:
+    """DSF1 SHA-256 of each of the n C5 sweep images (image i: value noise of its
+    drawn size, seed seed0 + i, generated on the device), extracted in same-size
+    batches of up to `batch` images."""
+    import torch
+    sizes = c5_sweep_sizes(n)
+    out = [""] * n
+    with Extractor(cfg, device) as ex:
+        for size in sorted(set(sizes)):
+            w, h = size
+            idx = [i for i, s in enumerate(sizes) if s == size]
+            for k in range(0, len(idx), batch):
+                part = idx[k:k + batch]
+                buf = torch.empty((len(part), h, w), dtype=torch.float32, device=f"cuda:{device}")
+                for j, i in enumerate(part):   # per-image seeds, as the host generator
+                    ex.synth_value_noise(buf[j].data_ptr(), 1, w, h, seed0 + i, 5, max(8, w // 20))
+                torch.cuda.synchronize(device)
+                ex.submit(None, n=len(part), w=w, h=h, device_ptr=buf.data_ptr())
+                ex.sync()
+                for j, i in enumerate(part):
+                    out[i] = ex.sha256(j)
+    return out
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.split("\n\n")[0])
     ap.add_argument("image", nargs="?", help="binary PNM (P5/P6)")
@@ -57,7 +100,20 @@ def main(argv=None) -> int:
     ap.add_argument("--batches", default="1,2,4,8")
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--library", help="another build of libdsift (the test-only negative control)")
+    ap.add_argument("--sweep", type=int, default=0,
+                    help="C5: N mixed-resolution images, extracted twice (batches of 32, then 7); "
+                         "every image's digest must repeat")
     args = ap.parse_args(argv)
+    if args.sweep:
+        first = sweep_digests(args.sweep, 32, args.device)
+        second = sweep_digests(args.sweep, 7, args.device)
+        bad = [i for i in range(args.sweep) if first[i] != second[i]]
+        sizes = c5_sweep_sizes(args.sweep)
+        print(f"sweep: {args.sweep} images over {len(set(sizes))} sizes, 2 runs (batches 32 / 7): "
+              f"{args.sweep - len(bad)} identical digests, {len(bad)} differ")
+        for i in bad[:10]:
+            print(f"image {i} {sizes[i]}: {first[i]} != {second[i]}")
+        return 0 if not bad else 3
     if args.library:
         from . import load_library
         load_library(args.library)

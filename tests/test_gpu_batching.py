@@ -121,3 +121,22 @@ def test_failed_submit_leaves_no_stale_result(port):
         with pytest.raises(ds.DsiftError) as e:
             ex.sync()
         assert e.value.code == ds.DSIFT_ESTATE
+
+
+def test_c5_sweep_twice_identical_and_reference_sample(ref):
+    # C5's determinism check at sweep scale: 256 mixed-resolution images
+    # (SplitMix64(0xC5) over the ten sizes, device-generated value noise) run
+    # twice with different batch compositions give identical per-image digests;
+    # a sample equals the reference's
+    from paper_2605_17869_b200.verify import c5_sweep_sizes, sweep_digests
+    n = 256
+    a = sweep_digests(n, 32)
+    b = sweep_digests(n, 7)
+    assert a == b
+    sizes = c5_sweep_sizes(n)
+    assert len(set(sizes)) == 10
+    for i in (0, 1, 2):
+        w, h = sizes[i]
+        img = ref.value_noise(w, h, 0x5EED0000 + i, 5, max(8, w // 20))
+        k, d = ref.extract(img, None, os.cpu_count() or 1)
+        assert a[i] == ref.hash_features(k, d), sizes[i]
