@@ -596,7 +596,12 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
         double fmax = 0.0;
         for (double f : fs) fmax = std::max(fmax, f);
         const double bw = 3.0 * fmax * smax;
-        if ((2.0 * bw + 2.0) * (2.0 * bw + 2.0) >= 8191.0)
+        // a bin's leaves come from its 2x2 cells: < (2 bw + 2)^2 points; the exact
+        // path's binary counter needs 2^depth above that (13 covers the defaults)
+        const double leaves = (2.0 * bw + 2.0) * (2.0 * bw + 2.0);
+        a.tree_depth = 13;
+        while (a.tree_depth < 24 && std::ldexp(1.0, a.tree_depth) <= leaves) ++a.tree_depth;
+        if (std::ldexp(1.0, a.tree_depth) <= leaves)
             invalid("descriptor: support window exceeds the per-bin tree capacity of this build");
     }
     a.chunk_rows = 8;
@@ -611,7 +616,7 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
     a.desc_u8 = desc_u8;
     a.err = &counters(c)->err;
     if (raw_mode) {
-        const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, 1);
+        const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, 1, a.tree_depth);
         if (smem > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
         int grid = c->sm_count * 4;
         if (n_host >= 0) grid = (int)std::max<long long>(1, std::min<long long>(grid, n_host));
@@ -647,10 +652,10 @@ static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host,
         for (double f : fs) fmax = std::max(fmax, f);
         af.max_span = 2 * (int)std::ceil(2.5 * 3.0 * fmax * smax) + 8;
     }
-    const size_t smem_exact = describe_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp);
+    const size_t smem_exact = describe_smem_bytes(a.max_axis, a.chunk_rows, a.n_dsp, a.tree_depth);
     if (smem_exact > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
     const size_t smem_s = std::max(describe_stream_smem_bytes(af.max_span, a.n_dsp),
-                                   describe_stream_exact_smem_bytes(af.max_axis, af.chunk_rows, a.n_dsp));
+                                   describe_stream_exact_smem_bytes(af.max_axis, af.chunk_rows, a.n_dsp, a.tree_depth));
     if (smem_s > 200 * 1024) invalid("descriptor: lattice too large for shared memory");
     const int per_sm = std::max(1, describe_stream_blocks_per_sm(smem_s));
     int grid = c->sm_count * per_sm;

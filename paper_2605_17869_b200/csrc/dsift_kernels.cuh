@@ -97,6 +97,7 @@ struct DescArgs {
     double raw_scale;
     int max_axis;
     int chunk_rows;
+    int tree_depth;        // levels of the per-bin binary counter: 2^tree_depth > leaves per bin
     const double2* trig;   // [n] (cos, sin) of the angle
     const int* slow_list;  // exact kernel: process only these keypoints (nullable)
     const unsigned* n_slow;
@@ -116,7 +117,7 @@ struct DescArgs {
     unsigned* err;
 };
 cudaError_t launch_describe(const DescArgs& a, int grid, cudaStream_t st);
-size_t describe_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
+size_t describe_smem_bytes(int max_axis, int chunk_rows, int n_dsp, int tree_depth);
 
 // K7 bucket geometry: bucket = image * per_image + (octave * s + interval - 1) * rows + floor(y)
 struct SortGeom {
@@ -137,7 +138,7 @@ cudaError_t launch_value_noise(float* out, int n, int w, int h, unsigned long lo
                                int cells, double* scratch, int nparts, cudaStream_t st);
 
 size_t describe_stream_smem_bytes(int max_span, int n_dsp);
-size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp);
+size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp, int tree_depth);
 int describe_stream_blocks_per_sm(size_t smem);
 cudaError_t launch_describe_stream(const DescArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev, long long n_host, double2* trig,

@@ -31,7 +31,7 @@
 namespace dsift {
 
 constexpr int kDescThreads = 128;
-constexpr int kTreeDepth = 13;   // per-bin leaves < 8192 (checked on the host)
+constexpr int kMaxTreeDepth = 24;   // per-bin leaves < 2^24; the depth in use is DescArgs::tree_depth
 constexpr int kRing = 32;
 constexpr float kUndef = -1.0f;  // describe.cpp:188
 
@@ -51,7 +51,7 @@ struct DescSmem {
     unsigned* omask;  // [chunk][8][nw]: bit cc set iff point o0 == o
     float* raw;     // [n_dsp][128]
     float* ring;    // [kRing][128]: per-bin leaves not yet folded (slot-major)
-    double* node;   // [kTreeDepth-3][128]: per-bin pending 8-leaf-aligned tree nodes
+    double* node;   // [tree_depth-3][128]: per-bin pending 8-leaf-aligned tree nodes
 };
 
 __device__ __forceinline__ int nearest_level_d(const PyramidDesc& p, double sigma_rel) {
@@ -354,7 +354,7 @@ __device__ __forceinline__ DescSmem carve_exact_smem(unsigned char* pbuf, const 
     S.pfo = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * a.chunk_rows * PW;
     S.omask = reinterpret_cast<unsigned*>(pbuf); pbuf += sizeof(unsigned) * a.chunk_rows * kDescOrients * (PW >> 5);
     pbuf += (16u - ((unsigned)__cvta_generic_to_shared(pbuf) & 15u)) & 15u;   // 16-byte align, stays a shared pointer
-    S.node = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * (kTreeDepth - 3) * kDescThreads;
+    S.node = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * (a.tree_depth - 3) * kDescThreads;
     S.ring = reinterpret_cast<float*>(pbuf);
     return S;
 }
@@ -885,7 +885,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
     stream_misc_rearm(misc);   // every thread read misc before the pass barriers
     if (tid < 32) S.cellmin[((npass - 1) & 1) * 32 + tid] = 1 << 20;   // folded before the last barrier
     // certificate (see above): chain <= kchain in a lane slot, <= 51 in
-    // the fold, <= npass across passes; the reference tree is <= 13 deep
+    // the fold, <= npass across passes; the reference tree is <= tree_depth deep
     bool ok;
     float res;
     const int top = (int)((__double_as_longlong(binacc) >> 52) & 0x7ff) - 1023;
@@ -893,7 +893,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         ok = true;
         res = __double2float_rn(binacc);
     } else {
-        const double e = (double)(kchain + npass + 51 + 13 + 64) * 0x1p-53;
+        const double e = (double)(kchain + npass + 51 + a.tree_depth + 64) * 0x1p-53;
         const double lo = binacc * (1.0 - e), hi = binacc * (1.0 + e);
         const float flo = __double2float_rn(lo), fhi = __double2float_rn(hi);
         ok = (flo == fhi);
@@ -980,13 +980,13 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     }
 }
 
-size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp) {
+size_t describe_stream_exact_smem_bytes(int max_axis, int chunk_rows, int n_dsp, int tree_depth) {
     // carve_exact_smem: raw + working set (+16 alignment slack)
     const size_t A = (size_t)max_axis;
     const size_t PW = ((A + 31) / 32) * 32, NW = PW / 32;
     return sizeof(float) * kDescDim * n_dsp + sizeof(double) * 6 * A + sizeof(float) * A + sizeof(int) * A +
            sizeof(float) * (chunk_rows + 2) * A + sizeof(float) * 2 * chunk_rows * PW +
-           sizeof(unsigned) * chunk_rows * kDescOrients * NW + 16 + sizeof(double) * (kTreeDepth - 3) * kDescThreads +
+           sizeof(unsigned) * chunk_rows * kDescOrients * NW + 16 + sizeof(double) * (tree_depth - 3) * kDescThreads +
            sizeof(float) * kRing * kDescThreads;
 }
 
@@ -1012,12 +1012,12 @@ cudaError_t launch_describe_stream(const DescArgs& a, int grid, cudaStream_t st)
     return cudaGetLastError();
 }
 
-size_t describe_smem_bytes(int max_axis, int chunk_rows, int n_dsp) {
+size_t describe_smem_bytes(int max_axis, int chunk_rows, int n_dsp, int tree_depth) {
     const size_t A = (size_t)max_axis;
     const size_t PW = ((A + 31) / 32) * 32, NW = PW / 32;
     return sizeof(double) * 6 * A + sizeof(float) * A + sizeof(int) * A + sizeof(float) * kDescDim * n_dsp +
            sizeof(float) * (chunk_rows + 2) * A + sizeof(float) * 2 * chunk_rows * PW +
-           sizeof(unsigned) * chunk_rows * kDescOrients * NW + 16 + sizeof(double) * (kTreeDepth - 3) * kDescThreads +
+           sizeof(unsigned) * chunk_rows * kDescOrients * NW + 16 + sizeof(double) * (tree_depth - 3) * kDescThreads +
            sizeof(float) * kRing * kDescThreads;
 }
 
@@ -1041,7 +1041,7 @@ cudaError_t launch_trig(const DevKeypoint* kps, const unsigned long long* n_dev,
 }
 
 cudaError_t launch_describe(const DescArgs& a, int grid, cudaStream_t st) {
-    const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, a.raw_mode ? 1 : a.n_dsp);
+    const size_t smem = describe_smem_bytes(a.max_axis, a.chunk_rows, a.raw_mode ? 1 : a.n_dsp, a.tree_depth);
     cudaError_t e = cudaFuncSetAttribute(describe_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     describe_exact_kernel<<<grid, kDescThreads, smem, st>>>(a);

@@ -120,3 +120,21 @@ def test_odd_sizes_bit_exact(ref, size):
         fs = ex.extract(img)
         sha = ex.sha256(0)
     assert_equal_to_reference(ref, img, fs, sha)
+
+
+def test_large_dsp_scales_beyond_default_tree_depth(ref):
+    # DSP support scales far above the defaults (f = 4, 6): a bin then gathers
+    # more than 2^13 leaves, so the per-bin binary counter runs deeper (the depth
+    # is sized from the support window); results stay bit-exact
+    from oracle.oracle import make_config
+    w, h = 192, 144
+    img = ref.value_noise(w, h, SEED0 + 5, 5, cells(w))
+    scales = (1.0, 4.0, 6.0)
+    with ds.Extractor(ds.SiftConfig(dsp_scales=scales)) as ex:
+        fs = ex.extract(img)
+        sha = ex.sha256(0)
+    kps, desc = ref.extract(img, make_config(dsp_scales=scales), os.cpu_count() or 1)
+    assert len(fs) == len(kps) > 0
+    assert fs.keypoints.tobytes() == np.ascontiguousarray(kps).tobytes()
+    assert bits(fs.descriptors).tobytes() == bits(desc).tobytes()
+    assert sha == ref.hash_features(kps, desc)
