@@ -783,6 +783,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
 #pragma unroll
             for (int e = 0; e < 32; ++e) my[e * 16] = 0.0;
             int lmin = 1 << 20;
+            bool nan_seen = false;
             // point pi = part + j*P of the cell in row-major order: (rr, cc),
             // advanced incrementally (dq rows + dr columns per step)
             const int ncs = max(nc, 1);
@@ -808,13 +809,11 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float dv = F_MUL(0.5f, F_SUB(down, up));
                 const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
                 float theta = dsift_atan2f(dv, du);
-                if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
-                if (isnan(theta)) {   // reference: negative bin -> std::out_of_range
-                    atomicOr(a.err, kErrHistogramRange);
-                    theta = 0.0f;
-                }
+                theta = (theta < 0.0f) ? F_ADD(theta, (float)kTwoPi) : theta;
+                nan_seen |= isnan(theta);   // reference: negative bin -> std::out_of_range (reported after the loop)
+                theta = isnan(theta) ? 0.0f : theta;
                 double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
-                if (obin >= (double)kDescOrients) obin = D_SUB(obin, (double)kDescOrients);
+                obin = (obin >= (double)kDescOrients) ? D_SUB(obin, (double)kDescOrients) : obin;
                 const AxisW wu = S.aw[u - kA], wv = S.aw[v - kA];
                 // window weight float(exp(-(uu^2 + vv^2) / 8)) (describe.cpp:96-98) as the
                 // product of the two per-axis factors, proven to round to the same
@@ -852,16 +851,18 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 pb[2 * kSSlotE] = x5;
                 pa[3 * kSSlotE] = x6;
                 pb[3 * kSSlotE] = x7;
-                if (val > 0.0f) {
+                {
                     // the lane's smallest leaf: leaves are RN(t * wo), monotone in t and
                     // wo, so it is RN(min t * min nonzero wo); its exponent bounds every
                     // leaf's lowest bit (a zero t, from an exactly-integral spatial bin,
-                    // only makes the bound pessimistic)
+                    // only makes the bound pessimistic); points with value 0 add nothing
                     const float tmin = fminf(fminf(t00, t01), fminf(t10, t11));
                     const float mo = fo > 0.0f ? fminf(fo, go) : go;
-                    lmin = min(lmin, efield1(F_MUL(tmin, mo)));
+                    const int ef = efield1(F_MUL(tmin, mo));
+                    lmin = (val > 0.0f) ? min(lmin, ef) : lmin;
                 }
             }
+            if (nan_seen) atomicOr(a.err, kErrHistogramRange);
             if (cell < ncells && lmin < (1 << 20)) atomicMin(&S.cellmin[(npass & 1) * 32 + cell], lmin);
 #ifdef DSIFT_NONDET_TEST_HOOK
             if (a.nondet && cell < ncells) {   // order-fragile: float atomics in scheduling order
