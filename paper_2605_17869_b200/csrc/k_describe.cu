@@ -819,7 +819,11 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 // product of the two per-axis factors, proven to round to the same
                 // float; otherwise (~1e-8 of points) evaluated as the reference does
                 float wgt;
-                if (!ds_separable_weight<47>(D_MUL(wu.e8, wv.e8), wgt)) {
+                const bool wok = ds_separable_weight<47>(D_MUL(wu.e8, wv.e8), wgt);
+                // warp-uniform fallback (~1e-8 of points): the reference's own
+                // evaluation equals the certified product wherever that is proven,
+                // so a warp with any unproven lane takes it for all of its lanes
+                if (__any_sync(__activemask(), !wok)) {
                     const double qu = D_DIV((double)u, bw), qv = D_DIV((double)v, bw);
                     wgt = (float)dsift_exp_mid(D_MUL(-D_ADD(D_MUL(qu, qu), D_MUL(qv, qv)), 0.125));
                 }
