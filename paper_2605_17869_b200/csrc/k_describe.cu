@@ -454,13 +454,22 @@ struct __align__(16) AxisW {
     float g, fr;    // (1 - frac, frac): weight of histogram index floor(bin) + {0, 1}
 };
 
+// one 16-byte shared load of an AxisW
+__device__ __forceinline__ AxisW ld_axisw(const AxisW* p) {
+    const double2 d = *reinterpret_cast<const double2*>(p);
+    AxisW w;
+    w.e8 = d.x;
+    const unsigned long long b = (unsigned long long)__double_as_longlong(d.y);
+    w.g = __uint_as_float((unsigned)b);
+    w.fr = __uint_as_float((unsigned)(b >> 32));
+    return w;
+}
+
 struct StreamSmem {
-    double* ax;     // cx + cos*k        [span] indexed k - kA
-    double* cysu;   // cy + sin*k
-    double* sv;     // sin*k
-    double* cv;     // cos*k
+    double2* axy;   // (cx + cos*k, cy + sin*k)   [span] indexed k - kA: one 16-byte load per column
+    double2* svc;   // (sin*k, cos*k)                                     and per row
     AxisW* aw;      // [span]
-    double* slot;   // [8 half-warps][32 entries (ri, ci, o)][16 lanes]
+    double* slot;   // [32 entries (ri, ci, o)][128 lanes]
     float* ring;    // [kSRing][ring_pitch] bilinear samples, -1 = undefined
     float* raw;     // [n_dsp][128]
     int* cellmin;   // [2][32]: per pass (double-buffered), per cell: lower bound on the lowest-bit
@@ -543,10 +552,8 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
         w.g = gr;
         w.fr = fr;
         S.aw[i] = w;
-        S.ax[i] = D_ADD(cx, D_MUL(cosa, (double)k));
-        S.cysu[i] = D_ADD(cy, D_MUL(sina, (double)k));
-        S.sv[i] = D_MUL(sina, (double)k);
-        S.cv[i] = D_MUL(cosa, (double)k);
+        S.axy[i] = make_double2(D_ADD(cx, D_MUL(cosa, (double)k)), D_ADD(cy, D_MUL(sina, (double)k)));
+        S.svc[i] = make_double2(D_MUL(sina, (double)k), D_MUL(cosa, (double)k));
         if (k >= -radius && k <= radius && bn > -1.0 && bn < (double)kDescCells) {
             atomicMin(&misc[0], k);
             atomicMax(&misc[1], k);
@@ -590,8 +597,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
         const int u = (q & 1) ? kmax + 1 : kmin - 1, v = (q & 2) ? kmax + 1 : kmin - 1;
-        const double px = D_SUB(S.ax[u - kA], S.sv[v - kA]);
-        const double py = D_ADD(S.cysu[u - kA], S.cv[v - kA]);
+        const double2 cu_ = S.axy[u - kA], rv_ = S.svc[v - kA];
+        const double px = D_SUB(cu_.x, rv_.x);
+        const double py = D_ADD(cu_.y, rv_.y);
         interior = interior && px >= 0.0 && px <= (double)(w - 2) && py >= 0.0 && py <= (double)(h - 2);
     }
 
@@ -671,8 +679,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                             const int rr = (int)(((float)id + 0.5f) * inv_sw), cc = id - rr * sw;
 #endif
                             const int vv = s0 + rr, u = ub + cc;
-                            const double px = D_SUB(S.ax[u - kA], S.sv[vv - kA]);
-                            const double py = D_ADD(S.cysu[u - kA], S.cv[vv - kA]);
+                            const double2 cu_ = S.axy[u - kA], rv_ = S.svc[vv - kA];
+                            const double px = D_SUB(cu_.x, rv_.x);
+                            const double py = D_ADD(cu_.y, rv_.y);
                             const int ix = (int)px, iy = (int)py;   // px, py >= 0: truncation = floor
                             fx[j] = (float)D_SUB(px, (double)ix);
                             fy[j] = (float)D_SUB(py, (double)iy);
@@ -705,8 +714,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                         const int id = min(idx + j * kDescThreads, ns - 1);
                         const int rr = (int)(((float)id + 0.5f) * inv_sw), cc = id - rr * sw;
                         const int vv = s0 + rr, u = ub + cc;
-                        const double px = D_SUB(S.ax[u - kA], S.sv[vv - kA]);
-                        const double py = D_ADD(S.cysu[u - kA], S.cv[vv - kA]);
+                        const double2 cu_ = S.axy[u - kA], rv_ = S.svc[vv - kA];
+                        const double px = D_SUB(cu_.x, rv_.x);
+                        const double py = D_ADD(cu_.y, rv_.y);
                         inb[j] = !(px < 0.0 || px > wm1 || py < 0.0 || py > hm1);
                         // sample_bilinear (describe.cpp:17-29); the clamp at 0 only
                         // affects samples that are discarded
@@ -818,7 +828,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 theta = isnan(theta) ? 0.0f : theta;
                 double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
                 obin = (obin >= (double)kDescOrients) ? D_SUB(obin, (double)kDescOrients) : obin;
-                const AxisW wu = S.aw[u - kA], wv = S.aw[v - kA];
+                const AxisW wu = ld_axisw(S.aw + (u - kA)), wv = ld_axisw(S.aw + (v - kA));
                 // window weight float(exp(-(uu^2 + vv^2) / 8)) (describe.cpp:96-98) as the
                 // product of the two per-axis factors, proven to round to the same
                 // float; otherwise (~1e-8 of points) evaluated as the reference does
@@ -930,10 +940,8 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     StreamSmem S;
     unsigned char* pbuf = sm;
     S.raw = reinterpret_cast<float*>(pbuf); pbuf += sizeof(float) * kDescDim * a.n_dsp;
-    S.ax = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
-    S.cysu = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
-    S.sv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
-    S.cv = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * SP;
+    S.axy = reinterpret_cast<double2*>(pbuf); pbuf += sizeof(double2) * SP;
+    S.svc = reinterpret_cast<double2*>(pbuf); pbuf += sizeof(double2) * SP;
     S.aw = reinterpret_cast<AxisW*>(pbuf); pbuf += sizeof(AxisW) * SP;
     S.slot = reinterpret_cast<double*>(pbuf); pbuf += sizeof(double) * 32 * kDescThreads;
     S.ring = reinterpret_cast<float*>(pbuf);
