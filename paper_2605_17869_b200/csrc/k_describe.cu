@@ -808,26 +808,29 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const int v = rv0 + rr, u = cu0 + cc;
                 cc += dr;
                 rr += dq;
-                if (cc >= ncs) {
-                    cc -= ncs;
-                    ++rr;
-                }
+                const int wrapc = cc >= ncs;   // branch-free carry
+                cc -= wrapc * ncs;
+                rr += wrapc;
                 const int col = u - ub;
                 const float* mid = S.ring + (v & (kSRing - 1)) * ring_pitch + col;
                 const float left = mid[-1], right = mid[1];
                 const float up = S.ring[((v - 1) & (kSRing - 1)) * ring_pitch + col];
                 const float down = S.ring[((v + 1) & (kSRing - 1)) * ring_pitch + col];
                 if (!interior && (left == kUndef || right == kUndef || up == kUndef || down == kUndef)) continue;
+                // the lanes at this point of the iteration: both votes below are
+                // reached by exactly these (nothing between them diverges)
+                const unsigned am = __activemask();
                 // describe.cpp:89-100
                 const float du = F_MUL(0.5f, F_SUB(right, left));
                 const float dv = F_MUL(0.5f, F_SUB(down, up));
                 const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
-                float theta = dsift_atan2f(dv, du);
+                float theta = dsift_atan2f_mask(dv, du, am);
                 theta = (theta < 0.0f) ? F_ADD(theta, (float)kTwoPi) : theta;
                 nan_seen |= isnan(theta);   // reference: negative bin -> std::out_of_range (reported after the loop)
                 theta = isnan(theta) ? 0.0f : theta;
                 double obin = ds_div_2pi((double)F_MUL(theta, (float)kDescOrients));
-                obin = (obin >= (double)kDescOrients) ? D_SUB(obin, (double)kDescOrients) : obin;
+                const double obw = D_SUB(obin, (double)kDescOrients);
+                obin = (obin >= (double)kDescOrients) ? obw : obin;
                 const AxisW wu = ld_axisw(S.aw + (u - kA)), wv = ld_axisw(S.aw + (v - kA));
                 // window weight float(exp(-(uu^2 + vv^2) / 8)) (describe.cpp:96-98) as the
                 // product of the two per-axis factors, proven to round to the same
@@ -837,7 +840,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 // warp-uniform fallback (~1e-8 of points): the reference's own
                 // evaluation equals the certified product wherever that is proven,
                 // so a warp with any unproven lane takes it for all of its lanes
-                if (__any_sync(__activemask(), !wok)) {
+                if (__any_sync(am, !wok)) {
                     const double qu = D_DIV((double)u, bw), qv = D_DIV((double)v, bw);
                     wgt = (float)dsift_exp_mid(D_MUL(-D_ADD(D_MUL(qu, qu), D_MUL(qv, qv)), 0.125));
                 }
