@@ -134,16 +134,15 @@ static cudaError_t launch_any(const BlurArgs& a, int R, int batch, cudaStream_t 
 }
 
 // ---------------------------------------------------------------------------
-// LEVEL-mode blur, v2 (the 5 incremental levels of every octave).
+// Tiled bridge blur of upsampled configs (UPSAMPLE mode; every other level
+// runs in the strip kernel below).
 //
-// The FP64 tap sums and the f32->f64 conversions (XU pipe, 1/4 of the FP64
-// rate) bound this stage, not HBM.  v2 therefore
-//   * stages the (64+2R)^2 input tile with 16-byte coalesced loads (interior
-//     tiles; border tiles use reflect-101 per element), 16-byte aligned so the
-//     H pass can read its window with LDS.128;
-//   * computes 8 outputs per thread in both passes: each staged value is
-//     converted to FP64 once per 8-output window (v1: per 4) and feeds 8
-//     independent DFMA chains.
+//   * the (64+2R)^2 input tile of the 2x upsampled base is formed from a
+//     staged half-resolution patch (interior tiles) or gathered with
+//     reflect-101 (border tiles), 16-byte aligned so the H pass reads its
+//     window with LDS.128;
+//   * 8 outputs per thread in both passes: each staged value is converted to
+//     FP64 once per 8-output window and feeds 8 independent DFMA chains.
 // Each output is still Sum_t k[t] * x[t] accumulated left to right in FP64
 // and rounded to float once per pass (scalespace.cpp:63-109).
 // ---------------------------------------------------------------------------
@@ -226,17 +225,14 @@ __device__ __forceinline__ void b2_hpass(const BlurArgs& a, float* sm) {
     __syncthreads();
 }
 
-// V pass: item = (column c, 8-row group), lanes along x; writes G and, for
-// LEVEL / DECIMATE, DoG (and the DECIMATE seed = this octave's G[0]).
-template <int R, int MODE, bool kAlu>
+// V pass: item = (column c, 8-row group), lanes along x; writes the bridge
+// level G[0] (the octave's first level has no DoG below it).
+template <int R, bool kAlu>
 __device__ __forceinline__ bool b2_vpass(const BlurArgs& a, const float* sm, int b, int x0, int y0) {
     bool ok = true;   // every output a positive normal >= 2^-100 (the consumer's ALU widen)
     using G = B2Geom<R>;
     const int w = a.w, h = a.h, pitch = a.pitch;
-    const float* __restrict__ src = a.src + b * a.src_img_stride;
     float* __restrict__ dst = a.dst + b * a.dst_img_stride;
-    float* __restrict__ dog = a.dog ? a.dog + b * a.dog_img_stride : nullptr;
-    float* __restrict__ seed = (MODE == kModeDecimate) ? a.seed + b * a.seed_img_stride : nullptr;
     for (int item = threadIdx.x; item < kB2W * (kB2H / kB2Seg); item += kB2Threads) {
         const int c = item & (kB2W - 1), rg = item >> 6;
         const int x = x0 + c;
@@ -255,27 +251,13 @@ __device__ __forceinline__ bool b2_vpass(const BlurArgs& a, const float* sm, int
         }
         if (x < w) {
             const int yb = y0 + rg * kB2Seg;
-            const long long ob = (long long)yb * pitch + x;
-            float* dp = dst + ob;                            // row bases of this item, once
-            const float* sp = src + ob;
-            float* gp = dog ? dog + ob : dst;
+            float* dp = dst + (long long)yb * pitch + x;
 #pragma unroll
             for (int j = 0; j < kB2Seg; ++j) {
-                const int y = yb + j;
-                if (y < h) {
+                if (yb + j < h) {
                     const float g = (float)acc[j];
                     ok &= (unsigned)(__float_as_uint(g) - 0x0d800000u) < (0x7f800000u - 0x0d800000u);
-                    const long long off = ob + j * pitch;
                     dp[j * pitch] = g;
-                    // DoG[i-1] = G[i] - G[i-1] (scalespace.cpp:209); G[i-1] was just read (L2)
-                    if (MODE == kModeLevel) {
-                        if (dog) gp[j * pitch] = g - __ldg(sp + j * pitch);
-                    } else if (MODE == kModeDecimate) {
-                        // G[0] of this octave = even samples of G[s] of the previous one (scalespace.cpp:133-142)
-                        const float prev = __ldg(src + (long long)(2 * y) * a.src_pitch + 2 * x);
-                        seed[off] = prev;
-                        if (dog) gp[j * pitch] = g - prev;
-                    }
                 }
             }
         }
@@ -286,11 +268,12 @@ __device__ __forceinline__ bool b2_vpass(const BlurArgs& a, const float* sm, int
 template <int R, int MODE>
 __global__ void __launch_bounds__(kB2Threads)
 blur_level2_kernel(const __grid_constant__ BlurArgs a) {
+    static_assert(MODE == kModeUpsample, "the tiled kernel is the upsampled bridge; levels use the strip kernel");
     using G = B2Geom<R>;
     extern __shared__ __align__(16) float sm2[];       // staged input [kHR][kInPitch], then tmp [kHR][kTmpPitch]
     const int b = blockIdx.z;
     const int x0 = blockIdx.x * kB2W, y0 = blockIdx.y * kB2H;
-    const int w = a.w, h = a.h, pitch = a.pitch;
+    const int w = a.w, h = a.h;
     const float* __restrict__ src = a.src + b * a.src_img_stride;
     const int cx0 = x0 - R - G::kM;                    // 16-byte aligned column of staged column 0
 
@@ -298,54 +281,7 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
     //      float >= 2^-100 (then the tmp values are positive normals too: the
     //      smallest tap is > 2^-20) so both passes may widen on the ALU pipe
     bool alu_ok = true;
-    const bool interior = MODE == kModeLevel && cx0 >= 0 && cx0 + G::kInW <= pitch && x0 + kB2W + R <= w &&
-                          y0 - R >= 0 && y0 + kB2H + R <= h;
-    if (interior) {
-        // asynchronous 16-byte copies: the whole tile is in flight at once
-        // (chunk i = r * kV + q of thread t: t, t + 256, ...; the row / column
-        // and both addresses advance incrementally)
-        constexpr int kV = G::kInW / 4;
-        constexpr int kDr = kB2Threads / kV, kDq = kB2Threads % kV;
-        const int r0 = threadIdx.x / kV, q0 = threadIdx.x - r0 * kV;
-        {
-            int r = r0, q = q0;
-            const float* gp = src + (long long)(y0 - R + r) * pitch + cx0 + 4 * q;
-            unsigned sa = (unsigned)__cvta_generic_to_shared(sm2 + r * G::kInPitch + 4 * q);
-            while (r < G::kHR) {
-                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gp));
-                r += kDr;
-                q += kDq;
-                gp += kDr * pitch + 4 * kDq;
-                sa += 4 * (kDr * G::kInPitch + 4 * kDq);
-                if (q >= kV) {
-                    q -= kV;
-                    ++r;
-                    gp += pitch - 4 * kV;
-                    sa += 4 * (G::kInPitch - 4 * kV);
-                }
-            }
-        }
-        asm volatile("cp.async.wait_all;\n" ::);
-        __syncthreads();
-        {
-            int r = r0, q = q0, m = 0x7fffffff, M = 0;
-            const float* sp = sm2 + r * G::kInPitch + 4 * q;
-            while (r < G::kHR) {
-                const int4 v = *reinterpret_cast<const int4*>(sp);
-                m = min(m, min(min(v.x, v.y), min(v.z, v.w)));
-                M = max(M, max(max(v.x, v.y), max(v.z, v.w)));
-                r += kDr;
-                q += kDq;
-                sp += kDr * G::kInPitch + 4 * kDq;
-                if (q >= kV) {
-                    q -= kV;
-                    ++r;
-                    sp += G::kInPitch - 4 * kV;
-                }
-            }
-            alu_ok = (m >= 0x0d800000) & (M < 0x7f800000);
-        }
-    } else if (MODE == kModeUpsample && cx0 >= 0 && cx0 + G::kInW <= w - 1 && y0 - R >= 0 &&
+    if (MODE == kModeUpsample && cx0 >= 0 && cx0 + G::kInW <= w - 1 && y0 - R >= 0 &&
                y0 + kB2H + R <= h - 1) {
         // interior bridge tile: stage the half-resolution patch once, then form
         // each 2x sample from shared memory (upsample2x, scalespace.cpp:113-131;
@@ -369,18 +305,6 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
             const double s4 = (((double)p0[0] + (double)p0[dx]) + (double)p1[0]) + (double)p1[dx];
             sm2[r * G::kInPitch + c] = (float)(0.25 * s4);
         }
-    } else if (MODE == kModeDecimate && cx0 >= 0 && cx0 + G::kInW <= w && y0 - R >= 0 && y0 + kB2H + R <= h) {
-        // interior seed tile: even samples of the previous octave's G[s]
-        // (decimate2x, scalespace.cpp:133-142), no reflection needed
-        const float* gsrc = src + (long long)(2 * (y0 - R)) * a.src_pitch + 2 * cx0;
-#pragma unroll 4
-        for (int i = threadIdx.x; i < G::kHR * (G::kInW / 2); i += kB2Threads) {
-            const int r = i / (G::kInW / 2), c2 = i - r * (G::kInW / 2);
-            const float4 v = __ldg(reinterpret_cast<const float4*>(gsrc + (long long)(2 * r) * a.src_pitch) + c2);
-            *reinterpret_cast<float2*>(sm2 + r * G::kInPitch + 2 * c2) = make_float2(v.x, v.z);
-            alu_ok &= (__float_as_int(v.x) >= 0x0d800000) & (__float_as_int(v.x) < 0x7f800000) &
-                      (__float_as_int(v.z) >= 0x0d800000) & (__float_as_int(v.z) < 0x7f800000);
-        }
     } else {   // gather with reflect-101 (scalespace.cpp:41-48) through the mode's input
                // mapping: level / raw pixel, 2x upsample (:113-131), decimation (:133-142)
 #pragma unroll 4
@@ -394,10 +318,10 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
     bool out_ok;
     if (__syncthreads_and(alu_ok)) {
         b2_hpass<R, true>(a, sm2);
-        out_ok = b2_vpass<R, MODE, true>(a, sm2, b, x0, y0);
+        out_ok = b2_vpass<R, true>(a, sm2, b, x0, y0);
     } else {
         b2_hpass<R, false>(a, sm2);
-        out_ok = b2_vpass<R, MODE, false>(a, sm2, b, x0, y0);
+        out_ok = b2_vpass<R, false>(a, sm2, b, x0, y0);
     }
     if (!__syncthreads_and(out_ok) && a.dst_flag && threadIdx.x == 0) atomicOr(a.dst_flag, 1);
 }
@@ -438,9 +362,6 @@ struct S3 {
     static constexpr int kTP = kSW + 2;                           // ring pitch (doubles), = 2 (mod 16)
     static constexpr size_t kStageBytes = sizeof(float) * (size_t)kSR * kInW;   // one TMA box
     static constexpr size_t kSmem = 2 * kStageBytes + sizeof(double) * (size_t)kRS * kTP + 128;
-    // UPSAMPLE: the half-resolution patch behind one step's staged rows, as FP64
-    static constexpr int kPW = kInW / 2 + 2, kPH = kSR / 2 + 2;
-    static constexpr size_t kPatchBytes = sizeof(double) * (size_t)kPW * kPH;
 };
 
 __device__ __forceinline__ int reflect_fast(int p, int n) {
@@ -460,11 +381,11 @@ __device__ __forceinline__ double s3_widen(float x) {
 
 // Gather virtual rows [t0, t0 + n) of the level's input (columns [xs, xs + kInW))
 // into a float stage: reflect-101 at the image border (scalespace.cpp:41-48),
-// the 2x upsample formed on the fly (UPSAMPLE), even samples (DECIMATE).
+// even samples (DECIMATE).
 // Returns whether every staged value this thread wrote is ALU-widenable.
 template <int R, int MODE>
 __device__ __forceinline__ bool s3_gather(const BlurArgs& a, const float* __restrict__ src, float* stg, int t0, int n,
-                                          int xs, double* patch) {
+                                          int xs) {
     using G = S3<R>;
     bool ok = true;
     const bool inner = xs >= 0 && xs + G::kInW <= a.w && t0 >= 0 && t0 + n <= a.h;
@@ -480,30 +401,6 @@ __device__ __forceinline__ bool s3_gather(const BlurArgs& a, const float* __rest
             const float4 v = make_float4(u0.x, u0.z, u1.x, u1.z);
             ok &= alu_widenable(v.x) & alu_widenable(v.y) & alu_widenable(v.z) & alu_widenable(v.w);
             reinterpret_cast<float4*>(stg)[q] = v;
-        }
-        return ok;
-    }
-    if (MODE == kModeUpsample && inner) {
-        // upsample2x (scalespace.cpp:113-131) from a staged half-resolution patch:
-        // patch row r holds source row min(py0 + r, src_h - 1), so the reference's
-        // edge clamp of the odd neighbour is the patch's next row / column
-        const int py0 = t0 >> 1, px0 = xs >> 1;
-        __syncthreads();   // the previous gather has finished reading the patch
-        for (int q = threadIdx.x; q < G::kPH * G::kPW; q += kS3Threads) {
-            const int r = q / G::kPW, c = q - r * G::kPW;
-            const int y = min(py0 + r, a.src_h - 1), x = min(px0 + c, a.src_w - 1);
-            patch[q] = (double)__ldg(src + (long long)y * a.src_pitch + x);
-        }
-        __syncthreads();
-        for (int q = threadIdx.x; q < n * G::kInW; q += kS3Threads) {
-            const int r = q / G::kInW, c = q - r * G::kInW;
-            const int gy = t0 + r, gx = xs + c;
-            const double* p0 = patch + ((gy >> 1) - py0) * G::kPW + ((gx >> 1) - px0);
-            const double* p1 = p0 + ((gy & 1) ? G::kPW : 0);
-            const int dx = gx & 1;
-            const float v = (float)(0.25 * (((p0[0] + p0[dx]) + p1[0]) + p1[dx]));
-            ok &= alu_widenable(v);
-            stg[q] = v;
         }
         return ok;
     }
@@ -554,7 +451,7 @@ __device__ __forceinline__ void s3_hpass(const BlurArgs& a, const float* stg, do
 
 template <int R, int MODE>
 __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, float* stage0, double* ring,
-                                                double* patch, uint64_t* bar, bool alu_level) {
+                                                uint64_t* bar, bool alu_level) {
     using G = S3<R>;
     const int b = blockIdx.z;
     const int x0 = blockIdx.x * kSW;
@@ -576,7 +473,7 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
             }
             return true;
         }
-        gok = s3_gather<R, MODE>(a, src, st, t0, n, xs, patch);
+        gok = s3_gather<R, MODE>(a, src, st, t0, n, xs);
         return false;
     };
     float* __restrict__ dst = a.dst + b * a.dst_img_stride;
@@ -730,7 +627,6 @@ blur_strip_kernel(const __grid_constant__ BlurArgs a, int seg_h) {
     unsigned char* base = sm3_raw + ((128u - (smem_u32(sm3_raw) & 127u)) & 127u);
     float* stage0 = reinterpret_cast<float*>(base);                          // [2][kSR][kInW] (TMA boxes)
     double* ring = reinterpret_cast<double*>(base + 2 * G::kStageBytes);    // [kRS][kTP]
-    double* patch = ring + G::kRS * G::kTP;                                 // UPSAMPLE: [kPH][kPW]
     __shared__ __align__(8) uint64_t bar[2];
     if (threadIdx.x == 0) {
         mbar_init(&bar[0], 1);
@@ -740,7 +636,7 @@ blur_strip_kernel(const __grid_constant__ BlurArgs a, int seg_h) {
     // ALU widening needs every source value to be a positive normal >= 2^-100
     // (flag written by the level's producer; the input image has none)
     const bool alu = a.src_flag != nullptr && *a.src_flag == 0;
-    blur_strip_body<R, MODE>(a, seg_h, stage0, ring, patch, bar, alu);
+    blur_strip_body<R, MODE>(a, seg_h, stage0, ring, bar, alu);
 }
 
 // rows per CTA segment: long segments amortise the 2R-row prologue, short ones
@@ -771,8 +667,7 @@ static cudaError_t launch_strip(const BlurArgs& a, int R, int batch, cudaStream_
     size_t smem = 0;
     void (*fn)(BlurArgs, int) = nullptr;
     switch (R) {
-#define DSIFT_R3(r) case r: fn = blur_strip_kernel<r, MODE>; \
-        smem = S3<r>::kSmem + (MODE == kModeUpsample ? S3<r>::kPatchBytes : 0); break;
+#define DSIFT_R3(r) case r: fn = blur_strip_kernel<r, MODE>; smem = S3<r>::kSmem; break;
         DSIFT_R3(1) DSIFT_R3(2) DSIFT_R3(3) DSIFT_R3(4) DSIFT_R3(5) DSIFT_R3(6) DSIFT_R3(7) DSIFT_R3(8)
         DSIFT_R3(9) DSIFT_R3(10) DSIFT_R3(11) DSIFT_R3(12) DSIFT_R3(13) DSIFT_R3(14) DSIFT_R3(15)
         DSIFT_R3(16)
@@ -810,7 +705,8 @@ cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStrea
     switch (mode) {
         case kModeLevel: return tiled ? launch_strip<kModeLevel>(a, R, batch, st) : launch_any<kModeLevel>(a, R, batch, st);
         case kModeRaw: return tiled ? launch_strip<kModeRaw>(a, R, batch, st) : launch_any<kModeRaw>(a, R, batch, st);
-        case kModeUpsample:   // the tiled kernel stages the half-resolution patch once per tile (faster here)
+        case kModeUpsample:   // the tiled kernel stages the half-resolution patch once per tile (faster here
+                              // than forming the 2x rows per strip step: 1.22 vs 1.33 ms per 32 C3 images)
             return tiled ? launch_v2<kModeUpsample>(a, R, batch, st) : launch_any<kModeUpsample>(a, R, batch, st);
         default: return tiled ? launch_strip<kModeDecimate>(a, R, batch, st) : launch_any<kModeDecimate>(a, R, batch, st);
     }
