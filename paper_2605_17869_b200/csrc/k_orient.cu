@@ -113,6 +113,7 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
         // q / nx without an integer division: exact for q < 2^20 (the window
         // is at most a few thousand pixels)
         const float inv_nx = 1.0f / (float)max(nx, 1);
+        bool nan_seen = false;
         auto pixel = [&](int q, int& bin, float& val) {
             bin = -1;
             val = 0.0f;
@@ -123,19 +124,20 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 const float gx = F_SUB(__ldg(r0 + x + 1), __ldg(r0 + x - 1));
                 const float gy = F_SUB(__ldg(r0 + od.pitch + x), __ldg(r0 - od.pitch + x));
                 const float mag = F_SQRT(F_ADD(F_MUL(gx, gx), F_MUL(gy, gy)));
-                float theta = dsift_atan2f(gy, gx);
-                if (theta < 0.0f) theta = F_ADD(theta, (float)kTwoPi);
-                if (isnan(theta)) {   // the reference's int(NaN) bin is out of range -> it throws
-                    atomicOr(a.err, kErrHistogramRange);
-                    theta = 0.0f;
-                }
+                const unsigned am = __activemask();   // the lanes of both votes below
+                float theta = dsift_atan2f_mask(gy, gx, am);
+                theta = (theta < 0.0f) ? F_ADD(theta, (float)kTwoPi) : theta;
+                nan_seen |= isnan(theta);   // the reference's int(NaN) bin is out of range -> it throws
+                theta = isnan(theta) ? 0.0f : theta;
                 bin = (int)ds_div_2pi((double)F_MUL(theta, (float)bins));
-                if (bin >= bins) bin -= bins;
+                bin = (bin >= bins) ? bin - bins : bin;
                 // float(exp(-(ddx^2 + ddy^2) / denom)) (orient.cpp:54-55) from the
                 // per-axis factors, certified (|arg| <= 9: |P - D| <= 2^-48 D), else
-                // evaluated as the reference does
+                // evaluated as the reference does — warp-uniformly: the reference's
+                // evaluation equals the certified product wherever that is proven
                 float wgt;
-                if (!(sep && ds_separable_weight<45>(D_MUL(wx[x - xa], wy[y - ya]), wgt))) {
+                const bool wok = sep && ds_separable_weight<45>(D_MUL(wx[x - xa], wy[y - ya]), wgt);
+                if (__any_sync(am, !wok)) {
                     const double ddx = D_SUB((double)x, cx), ddy = D_SUB((double)y, cy);
                     const double arg = D_DIV(-D_ADD(D_MUL(ddx, ddx), D_MUL(ddy, ddy)), denom);
                     wgt = (float)dsift_exp_mid(arg);
@@ -165,6 +167,7 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 }
             }
         }
+        if (nan_seen) atomicOr(a.err, kErrHistogramRange);
 #pragma unroll
         for (int d = 16; d; d >>= 1) emin = min(emin, __shfl_xor_sync(0xffffffffu, emin, d));
         __syncwarp();
