@@ -13,6 +13,6 @@ ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --batch 8 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-extra-configs > gpurun_out/r02_launches_b8.csv 2> gpurun_out/r02_launches.err
 # full captures with source: the descriptor, the largest level blur, extrema count
 ncu --set full --import-source on --clock-control none -k regex:describe_stream -c 1 -o gpurun_out/r02_describe_stream $B2 > gpurun_out/ncu_desc.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:"blur_strip_kernel<13" -c 1 -o gpurun_out/r02_blur_strip_r13 $B2 > gpurun_out/ncu_blur.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:blur_strip --launch-skip 4 -c 1 -o gpurun_out/r02_blur_strip_r13 $B2 > gpurun_out/ncu_blur.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:detect_count -c 1 -o gpurun_out/r02_detect_count $B2 > gpurun_out/ncu_det.log 2>&1
 ls -la gpurun_out
