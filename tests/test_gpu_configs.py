@@ -138,3 +138,25 @@ def test_large_dsp_scales_beyond_default_tree_depth(ref):
     assert fs.keypoints.tobytes() == np.ascontiguousarray(kps).tobytes()
     assert bits(fs.descriptors).tobytes() == bits(desc).tobytes()
     assert sha == ref.hash_features(kps, desc)
+
+
+@pytest.mark.parametrize("sigma0,intervals,limit", [(1.2, 2, 4_000_000), (2.4, 3, 4_000_000), (3.2, 2, 0),
+                                                    (3.2, 5, 4_000_000), (1.6, 4, 0)])
+def test_config_sweep_blur_radii(ref, sigma0, intervals, limit):
+    # other sigma ladders put every blur radius 3..37 through the kernels: the
+    # strip kernel (R <= 16, TMA-staged or gathered), the generic kernel beyond
+    # 16 (whose levels carry no positive-normal flag to their consumers), the
+    # tiled bridge and the raw bridge (limit 0: never upsampled)
+    from oracle.oracle import make_config
+    w, h = 200, 150
+    img = ref.value_noise(w, h, SEED0 + int(sigma0 * 10) + intervals, 5, cells(w))
+    cfg = ds.SiftConfig(sigma0=sigma0, intervals_per_octave=intervals, upsample_pixel_limit=limit)
+    with ds.Extractor(cfg) as ex:
+        fs = ex.extract(img)
+        sha = ex.sha256(0)
+    kps, desc = ref.extract(img, make_config(sigma0=sigma0, intervals=intervals, upsample_pixel_limit=limit),
+                            os.cpu_count() or 1)
+    assert len(fs) == len(kps)
+    assert fs.keypoints.tobytes() == np.ascontiguousarray(kps).tobytes()
+    assert bits(fs.descriptors).tobytes() == bits(desc).tobytes()
+    assert sha == ref.hash_features(kps, desc)
