@@ -287,6 +287,12 @@ static void build_pyramid_desc(dsift_ctx* c) {
     c->pyr = d;
 }
 
+// octaves of at most this many pixels are fused into one launch, where the
+// strip launches are pure latency (C3: from 50x37, C1: from 40x30); larger
+// octaves are faster as strips (one CTA per image is conversion-bound there:
+// C1 from 160x120 measured 0.91 ms of pyramid instead of 0.66)
+constexpr long long kSmallOctavePx = 2500;
+
 static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
     const Plan& p = c->plan;
     const PyramidDesc& d = c->pyr;
@@ -307,7 +313,19 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
                                                   (uint64_t)a.src_img_stride, (uint32_t)bw * es, 32u * es, 1u, es)
                         ? 1 : 0;
     };
-    for (int o = 0; o < p.n_oct; ++o) {
+    // small octaves (two whole levels fit in shared memory, every incremental
+    // radius <= 16) go to one fused launch, one CTA per image
+    int o_small = p.n_oct;
+    {
+        bool radii_ok = true;
+        for (int i = 0; i < s + 2; ++i) radii_ok = radii_ok && (int)p.inc[i].size() / 2 <= 16;
+        for (int o = 1; radii_ok && o < p.n_oct; ++o)
+            if ((long long)p.ow[o] * p.oh[o] <= kSmallOctavePx && small_octaves_smem(p.ow[o] * p.oh[o]) <= 200 * 1024) {
+                o_small = o;
+                break;
+            }
+    }
+    for (int o = 0; o < o_small; ++o) {
         const OctaveDesc& od = d.oct[o];
         const long long gstride = d.gauss_img_stride(o), dstride = d.dog_img_stride(o);
         auto fill_taps = [](BlurArgs& a, const std::vector<float>& t) {
@@ -390,6 +408,18 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
             cuda_check(launch_blur(a, kModeLevel, R, c->batch, c->stream), "level blur");
             ++c->launches;
         }
+    }
+    if (o_small < p.n_oct) {
+        SmallOctArgs a{};
+        a.pyr = d;
+        a.o_first = o_small;
+        a.cap_px = p.ow[o_small] * p.oh[o_small];
+        for (int i = 0; i < s + 2; ++i) {
+            a.radius[i] = (int)p.inc[i].size() / 2;
+            for (size_t t = 0; t < p.inc[i].size(); ++t) a.taps[i][t] = (double)p.inc[i][t];
+        }
+        cuda_check(launch_small_octaves(a, c->stream), "small octaves");
+        ++c->launches;
     }
 }
 

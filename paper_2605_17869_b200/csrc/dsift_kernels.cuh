@@ -33,6 +33,18 @@ struct BlurArgs {
 int blur_strip_box_w(int R);
 cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStream_t st);
 
+// fused small octaves o_first..n_oct-1 (one CTA per image, levels in shared memory)
+constexpr int kSmallMaxLevels = kMaxLevels;
+struct SmallOctArgs {
+    PyramidDesc pyr;
+    int o_first;
+    int cap_px;                                // w * h of octave o_first (the largest fused level)
+    int radius[kSmallMaxLevels];               // incremental blur i+1: radius
+    double taps[kSmallMaxLevels][33];          // and taps (radius <= 16)
+};
+size_t small_octaves_smem(int cap_px);
+cudaError_t launch_small_octaves(const SmallOctArgs& a, cudaStream_t st);
+
 struct DetectArgs {
     PyramidDesc pyr;
     int tiles_per_image;

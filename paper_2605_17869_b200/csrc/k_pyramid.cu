@@ -713,3 +713,102 @@ cudaError_t launch_blur(const BlurArgs& a, int mode, int R, int batch, cudaStrea
 }
 
 }  // namespace dsift
+
+namespace dsift {
+
+// ---------------------------------------------------------------------------
+// Small octaves, fused: one CTA per image runs every level of the octaves
+// o_first..n_oct-1 (each small enough for two whole levels in shared memory)
+// in one launch, instead of 5 launches per octave whose CTAs are mostly
+// latency.  Per level: H pass G -> tmp (float-rounded FP64 tap sums,
+// scalespace.cpp:63-86), V pass tmp -> G' (:88-109) writing G' and the DoG
+// G' - G (:209) to HBM and G' over G in shared memory (each element is read
+// and replaced by the same thread).  The next octave's G[0] is the even
+// samples of G[s] (decimate2x, :133-142), kept in a third buffer.  Same
+// arithmetic as the strip kernel; reflect-101 per element (:41-48).
+// ---------------------------------------------------------------------------
+constexpr int kSmallThreads = 1024;
+
+__global__ void __launch_bounds__(kSmallThreads, 1)
+blur_small_octaves_kernel(const __grid_constant__ SmallOctArgs a) {
+    extern __shared__ __align__(16) float smo[];
+    const PyramidDesc& p = a.pyr;
+    const int b = blockIdx.x, s = p.s;
+    const int o0 = a.o_first;
+    const int cap = a.cap_px;              // floats per full buffer
+    float* G = smo;                        // [h][w] current level
+    float* T = smo + cap;                  // [h][w] H-pass tmp
+    float* D = smo + 2 * cap;              // [h/2][w/2] next octave's G[0]
+    for (int o = o0; o < p.n_oct; ++o) {
+        const OctaveDesc& od = p.oct[o];
+        const int w = od.w, h = od.h, pitch = od.pitch, n = w * h;
+        float* gimg = od.gauss + (long long)b * p.gauss_img_stride(o);
+        float* dimg = od.dog + (long long)b * p.dog_img_stride(o);
+        // G[0]: even samples of the previous octave's G[s]
+        if (o == o0) {
+            const OctaveDesc& pd = p.oct[o - 1];
+            const float* src = pd.gauss + (long long)b * p.gauss_img_stride(o - 1) + (long long)s * pd.level_stride;
+            for (int i = threadIdx.x; i < n; i += kSmallThreads) {
+                const int y = i / w, x = i - y * w;
+                const float v = __ldg(src + (long long)(2 * y) * pd.pitch + 2 * x);
+                G[i] = v;
+                gimg[(long long)y * pitch + x] = v;
+            }
+        } else {
+            for (int i = threadIdx.x; i < n; i += kSmallThreads) {
+                const int y = i / w, x = i - y * w;
+                G[i] = D[i];
+                gimg[(long long)y * pitch + x] = D[i];
+            }
+        }
+        __syncthreads();
+        for (int lv = 1; lv < s + 3; ++lv) {
+            const int R = a.radius[lv - 1];
+            const double* taps = a.taps[lv - 1];
+            // H pass (scalespace.cpp:63-86)
+            for (int i = threadIdx.x; i < n; i += kSmallThreads) {
+                const int y = i / w, x = i - y * w;
+                const float* row = G + y * w;
+                double acc = 0.0;
+                for (int t = -R; t <= R; ++t) acc = __fma_rn(taps[t + R], (double)row[reflect101(x + t, w)], acc);
+                T[i] = (float)acc;
+            }
+            __syncthreads();
+            // V pass (scalespace.cpp:88-109) + DoG (scalespace.cpp:209)
+            float* gl = gimg + (long long)lv * od.level_stride;
+            float* dl = dimg + (long long)(lv - 1) * od.level_stride;
+            for (int i = threadIdx.x; i < n; i += kSmallThreads) {
+                const int y = i / w, x = i - y * w;
+                double acc = 0.0;
+                for (int t = -R; t <= R; ++t) acc = __fma_rn(taps[t + R], (double)T[reflect101(y + t, h) * w + x], acc);
+                const float g = (float)acc;
+                const long long off = (long long)y * pitch + x;
+                gl[off] = g;
+                dl[off] = g - G[i];
+                G[i] = g;
+            }
+            __syncthreads();
+            if (lv == s && o + 1 < p.n_oct) {   // decimate2x of G[s] (scalespace.cpp:133-142)
+                const int w2 = p.oct[o + 1].w, h2 = p.oct[o + 1].h;
+                for (int i = threadIdx.x; i < w2 * h2; i += kSmallThreads) {
+                    const int y = i / w2, x = i - y * w2;
+                    D[i] = G[(2 * y) * w + 2 * x];
+                }
+                // D is read only after the next octave's first barrier
+            }
+        }
+    }
+}
+
+size_t small_octaves_smem(int cap_px) { return sizeof(float) * (size_t)(2 * cap_px + (cap_px + 3) / 4 + 4); }
+
+cudaError_t launch_small_octaves(const SmallOctArgs& a, cudaStream_t st) {
+    const size_t smem = small_octaves_smem(a.cap_px);
+    cudaError_t e = cudaFuncSetAttribute(blur_small_octaves_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    blur_small_octaves_kernel<<<a.pyr.batch, kSmallThreads, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace dsift
