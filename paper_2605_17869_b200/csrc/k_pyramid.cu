@@ -393,14 +393,27 @@ __device__ __forceinline__ bool s3_gather(const BlurArgs& a, const float* __rest
         // interior rows of the previous octave's level: even samples of
         // 16-byte loads (decimate2x, scalespace.cpp:133-142), two per staged float4
         constexpr int kV = G::kInW / 4;
-        for (int q = threadIdx.x; q < n * kV; q += kS3Threads) {
-            const int r = q / kV, c4 = q - r * kV;
-            const float4* p =
-                reinterpret_cast<const float4*>(src + (long long)(2 * (t0 + r)) * a.src_pitch + 2 * xs) + 2 * c4;
-            const float4 u0 = __ldg(p), u1 = __ldg(p + 1);
-            const float4 v = make_float4(u0.x, u0.z, u1.x, u1.z);
-            ok &= alu_widenable(v.x) & alu_widenable(v.y) & alu_widenable(v.z) & alu_widenable(v.w);
-            reinterpret_cast<float4*>(stg)[q] = v;
+        constexpr int kIt = (kSR * kV + kS3Threads - 1) / kS3Threads;
+        float4 u0[kIt], u1[kIt];
+#pragma unroll
+        for (int k = 0; k < kIt; ++k) {   // every load of the step in flight at once
+            const int q = threadIdx.x + k * kS3Threads;
+            if (q < n * kV) {
+                const int r = q / kV, c4 = q - r * kV;
+                const float4* p =
+                    reinterpret_cast<const float4*>(src + (long long)(2 * (t0 + r)) * a.src_pitch + 2 * xs) + 2 * c4;
+                u0[k] = __ldg(p);
+                u1[k] = __ldg(p + 1);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kIt; ++k) {
+            const int q = threadIdx.x + k * kS3Threads;
+            if (q < n * kV) {
+                const float4 v = make_float4(u0[k].x, u0[k].z, u1[k].x, u1[k].z);
+                ok &= alu_widenable(v.x) & alu_widenable(v.y) & alu_widenable(v.z) & alu_widenable(v.w);
+                reinterpret_cast<float4*>(stg)[q] = v;
+            }
         }
         return ok;
     }
