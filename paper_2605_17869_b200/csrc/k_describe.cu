@@ -435,12 +435,14 @@ constexpr int kSLanes = 125;               // accumulation lanes: 5 cells x 25 p
 // Lane slots: double slot[lane >> 4][32 entries (ri, ci, o)][lane & 15].  A
 // lane's 32 entries all sit in bank pair (lane & 15), so the random-entry
 // read-modify-writes of a half-warp never conflict.
-constexpr int kSSlotE = 8 * kDescThreads;  // stride between (ri, ci) groups of one lane
+// pair (o, ri) of a lane = {ci = 0, ci = 1}, 16 bytes; lanes contiguous per pair
 // slot e of lane l at e * 128 + l: a lane's 32 entries share one bank pair
 // (l mod 16), so the random-entry read-modify-writes of a half-warp never
 // conflict, and consecutive lanes of one entry are consecutive (P3's fold
 // walks them with one add per read)
-__device__ __forceinline__ int slot_index(int lane, int e) { return e * kDescThreads + lane; }
+__device__ __forceinline__ int slot_index(int lane, int e) {
+    return (((e & 7) * 2 + (e >> 4)) * kDescThreads + lane) * 2 + ((e >> 3) & 1);
+}
 // Ring row pitch: >= the widest ring row 2*ceil(2.5 bw) + 1 (host: max_span = that
 // + 7), and = 16 (mod 32) so two adjacent rows fall in opposite bank halves.
 __host__ __device__ __forceinline__ int ring_pitch_for(int max_span) {
@@ -793,9 +795,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 if (r1 >= r0 && nc > 0) npts = (r1 - r0 + 1) * nc;
             }
             if (tid < 32) S.cellmin[((npass + 1) & 1) * 32 + tid] = 1 << 20;   // next pass's buffer (read two passes ago)
-            double* my = S.slot + tid;
+            double2* myv = reinterpret_cast<double2*>(S.slot) + tid;
 #pragma unroll
-            for (int e = 0; e < 32; ++e) my[e * kDescThreads] = 0.0;
+            for (int e = 0; e < 16; ++e) myv[e * kDescThreads] = make_double2(0.0, 0.0);
             int lmin = 1 << 20;
             bool nan_seen = false;
             // point pi = part + j*P of the cell in row-major order: (rr, cc),
@@ -852,26 +854,22 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float a0 = F_MUL(val, wv.g), a1 = F_MUL(val, wv.fr);
                 const float t00 = F_MUL(a0, wu.g), t01 = F_MUL(a0, wu.fr);
                 const float t10 = F_MUL(a1, wu.g), t11 = F_MUL(a1, wu.fr);
-                double* pa = my + (o0 & 7) * kDescThreads;
-                double* pb = my + ((o0 + 1) & 7) * kDescThreads;
-                double x0 = pa[0], x1 = pb[0], x2 = pa[kSSlotE], x3 = pb[kSSlotE];
-                double x4 = pa[2 * kSSlotE], x5 = pb[2 * kSSlotE], x6 = pa[3 * kSSlotE], x7 = pb[3 * kSSlotE];
-                x0 = x0 + (double)F_MUL(t00, go);
-                x1 = x1 + (double)F_MUL(t00, fo);
-                x2 = x2 + (double)F_MUL(t01, go);
-                x3 = x3 + (double)F_MUL(t01, fo);
-                x4 = x4 + (double)F_MUL(t10, go);
-                x5 = x5 + (double)F_MUL(t10, fo);
-                x6 = x6 + (double)F_MUL(t11, go);
-                x7 = x7 + (double)F_MUL(t11, fo);
+                // 8 leaves = 4 pairs {ci = 0, 1}: (o0, ri 0), (o0, ri 1), (o0+1, ri 0), (o0+1, ri 1)
+                double2* pa = myv + ((o0 & 7) * 2) * kDescThreads;
+                double2* pb = myv + (((o0 + 1) & 7) * 2) * kDescThreads;
+                double2 x0 = pa[0], x1 = pa[kDescThreads], x2 = pb[0], x3 = pb[kDescThreads];
+                x0.x = x0.x + (double)F_MUL(t00, go);
+                x0.y = x0.y + (double)F_MUL(t01, go);
+                x1.x = x1.x + (double)F_MUL(t10, go);
+                x1.y = x1.y + (double)F_MUL(t11, go);
+                x2.x = x2.x + (double)F_MUL(t00, fo);
+                x2.y = x2.y + (double)F_MUL(t01, fo);
+                x3.x = x3.x + (double)F_MUL(t10, fo);
+                x3.y = x3.y + (double)F_MUL(t11, fo);
                 pa[0] = x0;
-                pb[0] = x1;
-                pa[kSSlotE] = x2;
-                pb[kSSlotE] = x3;
-                pa[2 * kSSlotE] = x4;
-                pb[2 * kSSlotE] = x5;
-                pa[3 * kSSlotE] = x6;
-                pb[3 * kSSlotE] = x7;
+                pa[kDescThreads] = x1;
+                pb[0] = x2;
+                pb[kDescThreads] = x3;
                 {
                     // the lane's smallest leaf: leaves are RN(t * wo), monotone in t and
                     // wo, so it is RN(min t * min nonzero wo); its exponent bounds every
@@ -890,8 +888,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const int Rl = Ra + cell / 5, Cl = cell % 5 - 1;
                 for (int e = 0; e < 32; ++e) {
                     const int row = Rl + (e >> 4), col = Cl + ((e >> 3) & 1);
-                    if (row >= 0 && row < kDescCells && col >= 0 && col < kDescCells && my[e * kDescThreads] != 0.0)
-                        atomicAdd(&raw_out[(row * kDescCells + col) * kDescOrients + (e & 7)], (float)my[e * kDescThreads]);
+                    const double sv = S.slot[slot_index(tid, e)];
+                    if (row >= 0 && row < kDescCells && col >= 0 && col < kDescCells && sv != 0.0)
+                        atomicAdd(&raw_out[(row * kDescCells + col) * kDescOrients + (e & 7)], (float)sv);
                 }
             }
 #endif
