@@ -286,23 +286,25 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
         // interior bridge tile: stage the half-resolution patch once, then form
         // each 2x sample from shared memory (upsample2x, scalespace.cpp:113-131;
         // no reflection and no edge clamp can occur inside this tile)
+        // (the patch is widened to FP64 once; each of the ~4 upsampled samples
+        // per patch value then needs no conversion of its own)
         constexpr int kPW = G::kInW / 2 + 2, kPH = G::kHR / 2 + 2;
-        float* patch = sm2 + G::kHR * G::kInPitch;          // [kPH][kPW]
+        double* patch = reinterpret_cast<double*>(sm2 + G::kHR * G::kInPitch);   // [kPH][kPW]
         const int lx0 = cx0 >> 1, ly0 = (y0 - R) >> 1;
         for (int i = threadIdx.x; i < kPH * kPW; i += kB2Threads) {
             const int r = i / kPW, c = i - r * kPW;
             const float v = __ldg(src + (long long)min(ly0 + r, a.src_h - 1) * a.src_pitch + min(lx0 + c, a.src_w - 1));
-            patch[i] = v;
+            patch[i] = (double)v;
             alu_ok &= (__float_as_int(v) >= 0x0d800000) & (__float_as_int(v) < 0x7f800000);
         }
         __syncthreads();
         for (int i = threadIdx.x; i < G::kHR * G::kInW; i += kB2Threads) {
             const int r = i / G::kInW, c = i - r * G::kInW;
             const int gx = cx0 + c, gy = y0 - R + r;
-            const float* p0 = patch + ((gy >> 1) - ly0) * kPW + ((gx >> 1) - lx0);
-            const float* p1 = p0 + ((gy & 1) ? kPW : 0);
+            const double* p0 = patch + ((gy >> 1) - ly0) * kPW + ((gx >> 1) - lx0);
+            const double* p1 = p0 + ((gy & 1) ? kPW : 0);
             const int dx = gx & 1;
-            const double s4 = (((double)p0[0] + (double)p0[dx]) + (double)p1[0]) + (double)p1[dx];
+            const double s4 = ((p0[0] + p0[dx]) + p1[0]) + p1[dx];
             sm2[r * G::kInPitch + c] = (float)(0.25 * s4);
         }
     } else {   // gather with reflect-101 (scalespace.cpp:41-48) through the mode's input
@@ -700,7 +702,7 @@ static cudaError_t launch_v2(const BlurArgs& a, int R, int batch, cudaStream_t s
     void (*fn)(BlurArgs) = nullptr;
     switch (R) {
 #define DSIFT_R2(r) case r: fn = blur_level2_kernel<r, MODE>; smem = B2Geom<r>::kSmem + (MODE == kModeUpsample ? \
-        sizeof(float) * (size_t)(B2Geom<r>::kHR / 2 + 2) * (B2Geom<r>::kInW / 2 + 2) : 0); break;
+        sizeof(double) * (size_t)(B2Geom<r>::kHR / 2 + 2) * (B2Geom<r>::kInW / 2 + 2) : 0); break;
         DSIFT_R2(1) DSIFT_R2(2) DSIFT_R2(3) DSIFT_R2(4) DSIFT_R2(5) DSIFT_R2(6) DSIFT_R2(7) DSIFT_R2(8)
         DSIFT_R2(9) DSIFT_R2(10) DSIFT_R2(11) DSIFT_R2(12) DSIFT_R2(13) DSIFT_R2(14) DSIFT_R2(15)
         DSIFT_R2(16)
