@@ -13,6 +13,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX3: stage ranges for ncu --nvtx / nsys
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -425,6 +427,15 @@ static void launch_pyramid(dsift_ctx* c, const float* dev_images) {
 
 static Counters* counters(dsift_ctx* c) { return c->counters.as<Counters>(); }
 
+// NVTX range around a stage's launches (host enqueue; `ncu --nvtx --nvtx-include
+// "K5 describe/"` selects that stage's kernels).  Free when no tool is attached.
+struct NvtxStage {
+    explicit NvtxStage(const char* name) { nvtxRangePushA(name); }
+    ~NvtxStage() { nvtxRangePop(); }
+    NvtxStage(const NvtxStage&) = delete;
+    NvtxStage& operator=(const NvtxStage&) = delete;
+};
+
 static unsigned detect_tiles(const PyramidDesc& d, int* base, int* per_image) {
     int acc = 0;
     for (int o = 0; o < d.n_oct; ++o) {
@@ -749,16 +760,25 @@ static void run_group(dsift_ctx* c, dsift_result* r, const Group& g, dsift_keypo
     build_pyramid_desc(c);
     reset_counters(c);
     if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[0], c->stream), "event");
-    launch_pyramid(c, g.dev);
+    {
+        NvtxStage r("K1 pyramid");
+        launch_pyramid(c, g.dev);
+    }
     if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[1], c->stream), "event");
     c->cap_det = g.cap_det;
     c->cap_ori = g.cap_ori;
-    run_detect(c, 1, c->cap_det);   // K2: compacted extrema
-    run_refine(c, c->cap_det);      // K3: one thread per candidate
+    {
+        NvtxStage r("K2-K3 detect");
+        run_detect(c, 1, c->cap_det);   // K2: compacted extrema
+        run_refine(c, c->cap_det);      // K3: one thread per candidate
+    }
     if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[2], c->stream), "event");
     c->ori_kps.ensure(sizeof(DevKeypoint) * (size_t)c->cap_ori);
-    run_orient(c, c->det_kps.as<DevKeypoint>(), -1, c->cap_det, c->ori_kps.as<DevKeypoint>(), c->cap_ori, nullptr,
-               orient_depth(c->cfg.c, nullptr, c->plan));
+    {
+        NvtxStage r("K4 orient");
+        run_orient(c, c->det_kps.as<DevKeypoint>(), -1, c->cap_det, c->ori_kps.as<DevKeypoint>(), c->cap_ori, nullptr,
+                   orient_depth(c->cfg.c, nullptr, c->plan));
+    }
     if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[3], c->stream), "event");
     // canonical order (K7, hand-written bucket sort over the actual count)
     const long long cap = c->cap_ori;
@@ -769,12 +789,19 @@ static void run_group(dsift_ctx* c, dsift_result* r, const Group& g, dsift_keypo
     c->sort_work.ensure(sort_work_bytes(cap, sg, n));
     c->sorted_kps.ensure(sizeof(DevKeypoint) * (size_t)cap);
     Counters* ctr = counters(c);
-    cuda_check(launch_canonical_sort(c->ori_kps.as<DevKeypoint>(), &ctr->n_ori, cap, sg, c->sort_work.as<void>(),
-                                     c->sorted_kps.as<DevKeypoint>(), out_kps, n, out_offs, c->stream, &c->launches),
-               "sort");
+    {
+        NvtxStage r("K7 sort");
+        cuda_check(launch_canonical_sort(c->ori_kps.as<DevKeypoint>(), &ctr->n_ori, cap, sg, c->sort_work.as<void>(),
+                                         c->sorted_kps.as<DevKeypoint>(), out_kps, n, out_offs, c->stream,
+                                         &c->launches),
+                   "sort");
+    }
     if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[4], c->stream), "event");
     const double smax = c->cfg.c.sigma0 * std::pow(2.0, (c->cfg.c.intervals + 0.5) / c->cfg.c.intervals) * 1.001;
-    run_describe(c, c->sorted_kps.as<DevKeypoint>(), -1, out_desc, out_u8, 0, 0.0, smax, &ctr->n_ori);
+    {
+        NvtxStage r("K5 describe");
+        run_describe(c, c->sorted_kps.as<DevKeypoint>(), -1, out_desc, out_u8, 0, 0.0, smax, &ctr->n_ori);
+    }
     if (c->profiling) cuda_check(cudaEventRecord(c->stage_ev[5], c->stream), "event");
     cuda_check(launch_fold_totals(ctr, r->totals.as<BatchTotals>(), c->stream), "fold");
     ++c->launches;

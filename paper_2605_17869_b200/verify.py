@@ -12,6 +12,8 @@ checks it against the reference's own digest).
     python -m paper_2605_17869_b200.verify IMAGE.pgm [--runs 10] [--batches 1,2,4,8]
     python -m paper_2605_17869_b200.verify --synthetic 640x480 --seed 0x5EED0000
     python -m paper_2605_17869_b200.verify --sweep 10000    # C5: 10k mixed images, twice
+    python -m paper_2605_17869_b200.verify --sweep 10000 --record c5.txt   # resumable record
+    python -m paper_2605_17869_b200.verify --sweep 10000 --check c5.txt    # a later run against it
 
 Prints one line per extraction (run, batch, digest) and a summary; exit code 0
 (one digest) or 3 (several), like the reference.
@@ -67,17 +69,20 @@ def c5_sweep_sizes(n: int, seed: int = 0xC5) -> list[tuple[int, int]]:
 
 
 def sweep_digests(n: int, batch: int, device: int = 0, cfg: SiftConfig | None = None,
-                  seed0: int = 0x5EED0000) -> list[str]:
+                  seed0: int = 0x5EED0000, skip: set | None = None, sink=None) -> list[str]:
     """DSF1 SHA-256 of each of the n C5 sweep images (image i: value noise of its
     drawn size, seed seed0 + i, generated on the device), extracted in same-size
-    batches of up to `batch` images."""
+    batches of up to `batch` images.  `skip`: indices already done (a resumed
+    sweep; their entries stay ""); `sink(i, size, digest)` sees each result as
+    soon as it exists."""
     import torch
     sizes = c5_sweep_sizes(n)
     out = [""] * n
+    skip = skip or set()
     with Extractor(cfg, device) as ex:
         for size in sorted(set(sizes)):
             w, h = size
-            idx = [i for i, s in enumerate(sizes) if s == size]
+            idx = [i for i, s in enumerate(sizes) if s == size and i not in skip]
             for k in range(0, len(idx), batch):
                 part = idx[k:k + batch]
                 buf = torch.empty((len(part), h, w), dtype=torch.float32, device=f"cuda:{device}")
@@ -88,7 +93,23 @@ def sweep_digests(n: int, batch: int, device: int = 0, cfg: SiftConfig | None = 
                 ex.sync()
                 for j, i in enumerate(part):
                     out[i] = ex.sha256(j)
+                    if sink:
+                        sink(i, size, out[i])
     return out
+
+
+def read_digests(path: str) -> dict[int, str]:
+    """index -> digest from a sweep record ("index WxH sha256" per line)."""
+    got = {}
+    try:
+        with open(path) as f:
+            for line in f:
+                parts = line.split()
+                if len(parts) == 3:
+                    got[int(parts[0])] = parts[2]
+    except FileNotFoundError:
+        pass
+    return got
 
 
 def main(argv=None) -> int:
@@ -103,7 +124,34 @@ def main(argv=None) -> int:
     ap.add_argument("--sweep", type=int, default=0,
                     help="C5: N mixed-resolution images, extracted twice (batches of 32, then 7); "
                          "every image's digest must repeat")
+    ap.add_argument("--record", help="--sweep: append each image's digest to this file (resumes: images "
+                                     "already recorded are skipped)")
+    ap.add_argument("--check", help="--sweep: compare each image's digest with this record; exit 3 on a difference")
     args = ap.parse_args(argv)
+    if args.sweep and (args.record or args.check):
+        sizes = c5_sweep_sizes(args.sweep)
+        if args.record:
+            done = read_digests(args.record)
+            with open(args.record, "a") as f:
+                def sink(i, size, d):
+                    f.write(f"{i} {size[0]}x{size[1]} {d}\n")
+                    f.flush()
+                sweep_digests(args.sweep, 32, args.device, skip=set(done), sink=sink)
+            total = len(read_digests(args.record))
+            print(f"recorded: {total} of {args.sweep} images in {args.record}")
+            return 0
+        ref = read_digests(args.check)
+        bad = []
+
+        def cmp(i, size, d):
+            if ref.get(i) != d:
+                bad.append(i)
+        sweep_digests(args.sweep, 7, args.device, sink=cmp)
+        print(f"sweep check: {args.sweep} images against {args.check}: {args.sweep - len(bad)} identical, "
+              f"{len(bad)} differ")
+        for i in bad[:10]:
+            print(f"image {i} {sizes[i]}: recorded {ref.get(i)}")
+        return 0 if not bad else 3
     if args.sweep:
         first = sweep_digests(args.sweep, 32, args.device)
         second = sweep_digests(args.sweep, 7, args.device)

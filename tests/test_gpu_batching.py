@@ -140,3 +140,25 @@ def test_c5_sweep_twice_identical_and_reference_sample(ref):
         img = ref.value_noise(w, h, 0x5EED0000 + i, 5, max(8, w // 20))
         k, d = ref.extract(img, None, os.cpu_count() or 1)
         assert a[i] == ref.hash_features(k, d), sizes[i]
+
+
+def test_c5_sweep_record_resume_and_check(tmp_path):
+    # the resumable sweep: a record interrupted after part of the images is
+    # completed by a second --record run, and --check of a fresh run against it
+    # passes (exit 0); a corrupted record entry makes --check exit 3
+    from paper_2605_17869_b200 import verify
+    rec = str(tmp_path / "c5.txt")
+    n = 40
+    part = verify.sweep_digests(n, 32, skip=set(range(20, n)))   # "interrupted": images 0..19 only
+    sizes = verify.c5_sweep_sizes(n)
+    with open(rec, "w") as f:
+        for i in range(20):
+            f.write(f"{i} {sizes[i][0]}x{sizes[i][1]} {part[i]}\n")
+    assert verify.main(["--sweep", str(n), "--record", rec]) == 0
+    assert len(verify.read_digests(rec)) == n
+    assert verify.main(["--sweep", str(n), "--check", rec]) == 0
+    lines = open(rec).read().splitlines()
+    i0, size0, _ = lines[0].split()
+    lines[0] = f"{i0} {size0} {'0' * 64}"
+    open(rec, "w").write("\n".join(lines) + "\n")
+    assert verify.main(["--sweep", str(n), "--check", rec]) == 3
