@@ -31,7 +31,7 @@
 namespace dsift {
 
 constexpr int kDescThreads = 128;
-constexpr int kMaxTreeDepth = 24;   // per-bin leaves < 2^24; the depth in use is DescArgs::tree_depth
+// per-bin tree depth: DescArgs::tree_depth (13 for the defaults, at most 24: leaves < 2^24)
 constexpr int kRing = 32;
 constexpr float kUndef = -1.0f;  // describe.cpp:188
 
@@ -431,7 +431,7 @@ describe_exact_kernel(const __grid_constant__ DescArgs a) {
 constexpr int kP1Ilp = DSIFT_P1_ILP;   // interior samples in flight per thread
 constexpr int kSRing = 32;                 // sample rows resident (power of two)
 constexpr int kSMaxPassRows = kSRing - 2;  // lattice rows per pass (+2 guard rows)
-constexpr int kSLanes = 125;               // accumulation lanes: 5 cells x 25 parts ... 25 x 5
+// accumulation lanes: 125 = 5 cells x 25 parts ... 25 cells x 5 parts (tid < 125)
 // Lane slots: double slot[lane >> 4][32 entries (ri, ci, o)][lane & 15].  A
 // lane's 32 entries all sit in bank pair (lane & 15), so the random-entry
 // read-modify-writes of a half-warp never conflict.

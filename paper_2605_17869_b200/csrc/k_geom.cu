@@ -217,12 +217,6 @@ __device__ bool three_collinear(const double* xs, const double* ys, int n) {
     return false;
 }
 
-// One A^T A row update (geom.cpp:122-126): ata[p][q] += row[p] * row[q], q >= p.
-__device__ __forceinline__ void ata_add_row(double* ata, const double (&row)[9]) {
-    for (int p = 0; p < 9; ++p)
-        for (int q = p; q < 9; ++q) ata[p * 9 + q] += row[p] * row[q];
-}
-
 // The two DLT rows of correspondence (x, y) -> (u, v) with weight w (geom.cpp:130-131).
 __device__ __forceinline__ void dlt_rows(double w, double x, double y, double u, double v, double (&r1)[9],
                                          double (&r2)[9]) {
