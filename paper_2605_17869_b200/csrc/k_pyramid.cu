@@ -633,7 +633,7 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kS3Threads, 6)
+__global__ void __launch_bounds__(kS3Threads, 6)   // 5 / 7 / 8 measured slower
 blur_strip_kernel(const __grid_constant__ BlurArgs a, int seg_h) {
     using G = S3<R>;
     extern __shared__ __align__(128) unsigned char sm3_raw[];
@@ -658,7 +658,10 @@ blur_strip_kernel(const __grid_constant__ BlurArgs a, int seg_h) {
 // give small octaves enough CTAs (>= ~2 waves of 6 per SM)
 static int s3_seg_h(int w, int h, int batch) {
     const long long strips = (long long)((w + kSW - 1) / kSW) * batch;
-    int nseg = std::max(1, (h + 256) / 512);
+    // ~256-row segments: swept 128..1024 on C3 (8.39 / 8.38 / 8.38 / 8.43 / 8.84 / 9.64
+    // ms per 32 images at 128 / 192 / 256 / 320 / 512 / 1024) — the 2R-row prologue
+    // per segment costs less than the tail of fewer, longer CTAs
+    int nseg = std::max(1, (h + 128) / 256);
     const long long want = 148LL * 6 * 2;
     while ((long long)nseg * strips < want && (h + nseg) / (nseg + 1) >= 64) ++nseg;
     const int per = (h + nseg - 1) / nseg;
