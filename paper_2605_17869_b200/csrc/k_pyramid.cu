@@ -662,8 +662,11 @@ static int s3_seg_h(int w, int h, int batch) {
     // ms per 32 images at 128 / 192 / 256 / 320 / 512 / 1024) — the 2R-row prologue
     // per segment costs less than the tail of fewer, longer CTAs
     int nseg = std::max(1, (h + 128) / 256);
-    const long long want = 148LL * 6 * 2;
-    while ((long long)nseg * strips < want && (h + nseg) / (nseg + 1) >= 64) ++nseg;
+    // small octaves: split into >= 32-row segments until there are ~16 CTAs per
+    // resident slot (swept: 2 / 8 / 16 / 32 / 64 waves and 64 / 32 / 16-row
+    // minimums: 8.38 / 8.22 / 8.17 / 8.22 / 8.33 ms)
+    const long long want = 148LL * 6 * 16;
+    while ((long long)nseg * strips < want && (h + nseg) / (nseg + 1) >= 32) ++nseg;
     const int per = (h + nseg - 1) / nseg;
     return ((per + kSR - 1) / kSR) * kSR;
 }
