@@ -266,7 +266,7 @@ __device__ __forceinline__ bool b2_vpass(const BlurArgs& a, const float* sm, int
 }
 
 template <int R, int MODE>
-__global__ void __launch_bounds__(kB2Threads)
+__global__ void __launch_bounds__(kB2Threads, 5)   // swept 3-6 CTAs/SM: 5 best
 blur_level2_kernel(const __grid_constant__ BlurArgs a) {
     static_assert(MODE == kModeUpsample, "the tiled kernel is the upsampled bridge; levels use the strip kernel");
     using G = B2Geom<R>;
