@@ -662,11 +662,13 @@ static int s3_seg_h(int w, int h, int batch) {
     // ms per 32 images at 128 / 192 / 256 / 320 / 512 / 1024) — the 2R-row prologue
     // per segment costs less than the tail of fewer, longer CTAs
     int nseg = std::max(1, (h + 128) / 256);
-    // small octaves: split into >= 32-row segments until there are ~16 CTAs per
-    // resident slot (swept: 2 / 8 / 16 / 32 / 64 waves and 64 / 32 / 16-row
-    // minimums: 8.38 / 8.22 / 8.17 / 8.22 / 8.33 ms)
-    const long long want = 148LL * 6 * 16;
-    while ((long long)nseg * strips < want && (h + nseg) / (nseg + 1) >= 32) ++nseg;
+    // small octaves: split into >= 64-row segments until there are ~2 CTAs per
+    // resident slot.  More (8 / 16 waves, 32-row minimums) shortens the device-
+    // resident pyramid (8.37 -> 8.17 ms) but floods the block scheduler while the
+    // other context's descriptor kernel waits for SMs: the two-context end-to-end
+    // number falls from 256 to 241 images/s (measured; from 4 waves on)
+    const long long want = 148LL * 6 * 2;
+    while ((long long)nseg * strips < want && (h + nseg) / (nseg + 1) >= 64) ++nseg;
     const int per = (h + nseg - 1) / nseg;
     return ((per + kSR - 1) / kSR) * kSR;
 }
