@@ -162,3 +162,25 @@ def test_c5_sweep_record_resume_and_check(tmp_path):
     lines[0] = f"{i0} {size0} {'0' * 64}"
     open(rec, "w").write("\n".join(lines) + "\n")
     assert verify.main(["--sweep", str(n), "--check", rec]) == 3
+
+
+def test_concurrent_drop_in_calls_from_host_threads(port):
+    # calls on distinct images may run concurrently: 6 host threads
+    # each call the drop-in extract (one cached context per thread, ctypes drops
+    # the GIL) on their own images; every result equals the single-threaded one
+    from concurrent.futures import ThreadPoolExecutor
+    imgs = [port.value_noise(320, 240, 0x5EED0100 + i, 5, 16) for i in range(12)]
+    want = []
+    with ds.Extractor() as ex:
+        for im in imgs:
+            ex.extract(im)
+            want.append(ex.sha256(0))
+
+    def one(i):
+        fs = ds.extract(imgs[i])
+        k, d = fs.keypoints, fs.descriptors
+        return port.hash_features(k, d)
+
+    with ThreadPoolExecutor(max_workers=6) as pool:
+        got = list(pool.map(one, range(len(imgs))))
+    assert got == want
