@@ -616,6 +616,22 @@ def run_ours(args, rank, local_rank, world):
         match = {"what": "ratio_match(image 0, image 1), ratio 0.8, descriptors on device",
                  "n_a": int(offs[1] - offs[0]), "n_b": int(offs[2] - offs[1]), "ms": e0.elapsed_time(e1),
                  "pairs": int(len(pairs)), "putative_a": pa, "putative_b": pb}
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            # the reference's own ratio_match (match.cpp:77-119) on the same descriptors,
+            # all host threads; the pair list must be the same
+            from oracle.oracle import Oracle, available
+            if available("reference"):
+                ha, hb = da.cpu().numpy(), db.cpu().numpy()
+                workers = os.cpu_count() or 1
+                t1 = time.perf_counter()
+                rp = Oracle("reference").ratio_match(ha, hb, 0.8, workers)
+                match["reference_cpu_ms"] = (time.perf_counter() - t1) * 1e3
+                match["reference_cpu_workers"] = workers
+                mine = np.stack([pairs[pairs.dtype.names[0]].astype(np.int64), pairs[pairs.dtype.names[1]].astype(np.int64),
+                                 np.ascontiguousarray(pairs[pairs.dtype.names[2]]).view(np.int32).astype(np.int64)], 1)
+                match["same_pairs_as_reference"] = bool(mine.shape == rp[0].shape and
+                                                        (mine == rp[0].astype(np.int64)).all() and
+                                                        (pa, pb) == (rp[1], rp[2]))
 
     # ---- robust homography: magsac_lite through the C ABI with host
     # buffers (host sampling + H2D + 3 kernels + D2H inside the wall-clock time)
