@@ -450,6 +450,16 @@ __host__ __device__ __forceinline__ int ring_pitch_for(int max_span) {
     return need + ((16 - need % 32) + 32) % 32;
 }
 
+// floor of 0 <= x < 2^31 on the FP64 pipe: x + 2^52 rounded down is 2^52 +
+// floor(x) exactly (unit ulp), its low word is floor(x) and subtracting 2^52
+// back gives (double)floor(x) exactly; replaces an F2I + I2F pair on the
+// conversion pipe
+__device__ __forceinline__ int floor_nonneg(double x, double& fl) {
+    const double t = __dadd_rd(x, 0x1p52);
+    fl = D_SUB(t, 0x1p52);
+    return __double2loint(t);
+}
+
 // per-axis weights of lattice index k, one 16-byte load
 struct __align__(16) AxisW {
     double e8;      // exp(-(k/bw)^2 / 8): per-axis factor of the window weight
@@ -684,9 +694,10 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                             const double2 cu_ = S.axy[u - kA], rv_ = S.svc[vv - kA];
                             const double px = D_SUB(cu_.x, rv_.x);
                             const double py = D_ADD(cu_.y, rv_.y);
-                            const int ix = (int)px, iy = (int)py;   // px, py >= 0: truncation = floor
-                            fx[j] = (float)D_SUB(px, (double)ix);
-                            fy[j] = (float)D_SUB(py, (double)iy);
+                            double flx, fly;
+                            const int ix = floor_nonneg(px, flx), iy = floor_nonneg(py, fly);
+                            fx[j] = (float)D_SUB(px, flx);
+                            fy[j] = (float)D_SUB(py, fly);
                             off[j] = iy * pitch + ix;
                             slot[j] = (vv & (kSRing - 1)) * ring_pitch + cc;
                         }
@@ -847,8 +858,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                     wgt = (float)dsift_exp_mid(D_MUL(-D_ADD(D_MUL(qu, qu), D_MUL(qv, qv)), 0.125));
                 }
                 const float val = F_MUL(mag, wgt);
-                const int o0 = (int)floor(obin);
-                const float fo = (float)D_SUB(obin, (double)o0);
+                double flo;
+                const int o0 = floor_nonneg(obin, flo);
+                const float fo = (float)D_SUB(obin, flo);
                 const float go = F_SUB(1.0f, fo);
                 // leaves value*wr*wc*wo (describe.cpp:102-124), FP64 slot accumulation
                 const float a0 = F_MUL(val, wv.g), a1 = F_MUL(val, wv.fr);
