@@ -123,6 +123,15 @@ struct Plan {
 };
 
 static int round_pitch(int w) { return (w + 31) & ~31; }
+// Rows per pyramid level: h, rounded up (by at most 3 for a 32-float pitch) so
+// that a level is a multiple of 512 bytes.  With 512-byte aligned octave
+// blocks every level and every image's level stack then starts 512-byte
+// aligned, as a pitched 2D texture over the stack requires (K5's gathers).
+static int level_rows(int pitch, int h) {
+    int r = h;
+    while (((long long)pitch * r) % 128 != 0) ++r;
+    return r;
+}
 
 static Plan make_plan(const Cfg& cfg, int w, int h) {
     const dsift_config& c = cfg.c;
@@ -248,6 +257,13 @@ struct dsift_ctx {
     dsift_result def;
     dsift_result* cur = &def;
     cudaEvent_t stage_ev[6] = {};
+    // K5's bilinear gathers: one pitched 2D texture per (image, octave) over
+    // that image's Gaussian levels stacked vertically, rebuilt when the
+    // pyramid's address or layout changes (gauss_tex_key)
+    std::vector<cudaTextureObject_t> gauss_tex;
+    std::vector<long long> gauss_tex_key;
+    DevBuf gauss_tex_dev;
+    bool gauss_tex_ok = false;
 };
 
 namespace dsift {
@@ -269,16 +285,16 @@ static void build_pyramid_desc(dsift_ctx* c) {
         od.w = p.ow[o];
         od.h = p.oh[o];
         od.pitch = p.pitch[o];
-        od.level_stride = (long long)od.pitch * od.h;
+        od.level_stride = (long long)od.pitch * level_rows(od.pitch, od.h);
         od.tiles_x = od.w >= 3 ? (od.w - 2 + 31) / 32 : 0;
         od.tiles_y = od.h >= 3 ? (od.h - 2 + 31) / 32 : 0;
         if (od.tiles_x == 0 || od.tiles_y == 0) od.tiles_x = od.tiles_y = 0;
         const size_t g = sizeof(float) * (size_t)c->batch * (p.s + 3) * od.level_stride;
         const size_t dg = sizeof(float) * (size_t)c->batch * (p.s + 2) * od.level_stride;
         od.gauss = reinterpret_cast<float*>(off);
-        off += (g + 255) & ~size_t(255);
+        off += (g + 511) & ~size_t(511);
         od.dog = reinterpret_cast<float*>(off);
-        off += (dg + 255) & ~size_t(255);
+        off += (dg + 511) & ~size_t(511);
     }
     c->pyramid.ensure(off);
     char* base = c->pyramid.as<char>();
@@ -617,12 +633,74 @@ static int describe_axis(const dsift_config& cf, const std::vector<double>& dsp,
     return (int)(2 * r + 3);
 }
 
+// Texture objects for K5's 2x2 gathers (tld4): [image][kMaxOctaves] handles
+// on the device.  Per (image, octave) the s + 3 levels are one pitched 2D
+// array of (s + 3) * level_rows rows (level_stride = pitch * level_rows); the
+// pitch is a multiple of 128 bytes and every image's block 512-byte aligned.
+// Returns nullptr (the kernel then gathers with plain loads) when a level
+// stack exceeds the device's pitched-texture limits.
+static const unsigned long long* ensure_gauss_textures(dsift_ctx* c) {
+    const PyramidDesc& d = c->pyr;
+    std::vector<long long> key{(long long)(uintptr_t)c->pyramid.as<void>(), d.batch, d.n_oct, d.s};
+    for (int o = 0; o < d.n_oct; ++o) {
+        key.push_back(d.oct[o].w);
+        key.push_back(d.oct[o].h);
+        key.push_back(d.oct[o].pitch);
+    }
+    if (key == c->gauss_tex_key) return c->gauss_tex_ok ? c->gauss_tex_dev.as<unsigned long long>() : nullptr;
+    cuda_check(cudaStreamSynchronize(c->stream), "sync before texture rebuild");   // no launch still reads the old ones
+    for (cudaTextureObject_t t : c->gauss_tex) cudaDestroyTextureObject(t);
+    c->gauss_tex.clear();
+    c->gauss_tex_key = key;
+    c->gauss_tex_ok = false;
+    cudaDeviceProp prop{};
+    cuda_check(cudaGetDeviceProperties(&prop, c->device), "cudaGetDeviceProperties");
+    for (int o = 0; o < d.n_oct; ++o) {
+        const OctaveDesc& od = d.oct[o];
+        const size_t pitch_b = sizeof(float) * (size_t)od.pitch;
+        if (od.w > prop.maxTexture2DLinear[0] || (d.s + 3) * (od.level_stride / od.pitch) > prop.maxTexture2DLinear[1] ||
+            (long long)pitch_b > prop.maxTexture2DLinear[2] || pitch_b % prop.texturePitchAlignment != 0)
+            return nullptr;
+        const size_t align = std::max<size_t>(prop.textureAlignment, prop.texturePitchAlignment);
+        for (int i = 0; i < d.batch; ++i)
+            if ((uintptr_t)(od.gauss + (long long)i * d.gauss_img_stride(o)) % align != 0) return nullptr;
+    }
+    std::vector<unsigned long long> h((size_t)d.batch * kMaxOctaves, 0ull);
+    for (int i = 0; i < d.batch; ++i)
+        for (int o = 0; o < d.n_oct; ++o) {
+            const OctaveDesc& od = d.oct[o];
+            cudaResourceDesc rd{};
+            rd.resType = cudaResourceTypePitch2D;
+            rd.res.pitch2D.devPtr = od.gauss + (long long)i * d.gauss_img_stride(o);
+            rd.res.pitch2D.desc = cudaCreateChannelDesc<float>();
+            rd.res.pitch2D.width = (size_t)od.w;
+            rd.res.pitch2D.height = (size_t)(d.s + 3) * (od.level_stride / od.pitch);
+            rd.res.pitch2D.pitchInBytes = sizeof(float) * (size_t)od.pitch;
+            cudaTextureDesc td{};
+            td.addressMode[0] = td.addressMode[1] = cudaAddressModeClamp;
+            td.filterMode = cudaFilterModePoint;
+            td.readMode = cudaReadModeElementType;
+            td.normalizedCoords = 0;
+            cudaTextureObject_t t = 0;
+            cuda_check(cudaCreateTextureObject(&t, &rd, &td, nullptr), "cudaCreateTextureObject");
+            c->gauss_tex.push_back(t);
+            h[(size_t)i * kMaxOctaves + o] = (unsigned long long)t;
+        }
+    c->gauss_tex_dev.ensure(sizeof(unsigned long long) * h.size());
+    cuda_check(cudaMemcpyAsync(c->gauss_tex_dev.as<void>(), h.data(), sizeof(unsigned long long) * h.size(),
+                               cudaMemcpyHostToDevice, c->stream),   // pageable: staged before returning
+               "texture handles");
+    c->gauss_tex_ok = true;
+    return c->gauss_tex_dev.as<unsigned long long>();
+}
+
 static void run_describe(dsift_ctx* c, const DevKeypoint* kps, long long n_host, float* desc,
                          unsigned char* desc_u8, int raw_mode, double raw_scale, double smax,
                          const unsigned long long* n_dev) {
     const dsift_config& cf = c->cfg.c;
     DescArgs a{};
     a.pyr = c->pyr;
+    a.gauss_tex = ensure_gauss_textures(c);
     a.kps = kps;
     a.n_dev = n_dev;
     a.n_host = n_host;
@@ -825,8 +903,8 @@ static void run_batch(dsift_ctx* c, dsift_result* r) {
         const Plan p = make_plan(c->cfg, g.w, g.h);
         size_t bytes = 0;
         for (int o = 0; o < p.n_oct; ++o) {
-            const size_t lv = sizeof(float) * (size_t)p.pitch[o] * p.oh[o] * g.idx.size();
-            bytes += ((lv * (p.s + 3) + 255) & ~size_t(255)) + ((lv * (p.s + 2) + 255) & ~size_t(255));
+            const size_t lv = sizeof(float) * (size_t)p.pitch[o] * level_rows(p.pitch[o], p.oh[o]) * g.idx.size();
+            bytes += ((lv * (p.s + 3) + 511) & ~size_t(511)) + ((lv * (p.s + 2) + 511) & ~size_t(511));
         }
         pyr_max = std::max(pyr_max, bytes);
     }
@@ -1122,6 +1200,7 @@ void dsift_destroy(dsift_ctx* c) {
         if (e) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    for (cudaTextureObject_t t : c->gauss_tex) cudaDestroyTextureObject(t);
     delete c;
 }
 

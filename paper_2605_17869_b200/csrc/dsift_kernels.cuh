@@ -99,6 +99,7 @@ int orient_tile_size();
 
 struct DescArgs {
     PyramidDesc pyr;
+    const unsigned long long* gauss_tex;   // [image][kMaxOctaves] texture objects of the Gaussian levels (nullable)
     const DevKeypoint* kps;
     const unsigned long long* n_dev;
     long long n_host;

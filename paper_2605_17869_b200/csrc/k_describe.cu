@@ -477,6 +477,31 @@ __device__ __forceinline__ AxisW ld_axisw(const AxisW* p) {
     return w;
 }
 
+// The 2x2 footprint (ix, iy) .. (ix + 1, iy + 1) of one bilinear sample
+// (describe.cpp:17-29), 0 <= ix <= w - 2, 0 <= iy <= h - 2, as the stored
+// floats bit for bit.  With a texture: one tld4 at unnormalised
+// (ix + 1, row0 + iy + 1), whose footprint is texels floor(c - 0.5) and + 1 on
+// each axis (c - 0.5 is exact), coordinates formed exactly on the FMA pipe
+// (integers < 2^23).  Without: four loads.
+__device__ __forceinline__ void gather2x2_tex(cudaTextureObject_t tex, int row0, int ix, int iy, float& v00,
+                                              float& v10, float& v01, float& v11) {
+    const float xf = F_SUB(__int_as_float(0x4B000000 + ix + 1), 8388608.0f);
+    const float yf = F_SUB(__int_as_float(0x4B000000 + row0 + iy + 1), 8388608.0f);
+    const float4 g = tex2Dgather<float4>(tex, xf, yf, 0);
+    v01 = g.x;   // (ix, iy + 1)
+    v11 = g.y;   // (ix + 1, iy + 1)
+    v10 = g.z;   // (ix + 1, iy)
+    v00 = g.w;   // (ix, iy)
+}
+__device__ __forceinline__ void gather2x2_ldg(const float* __restrict__ img, int pitch, int ix, int iy, float& v00,
+                                              float& v10, float& v01, float& v11) {
+    const float* r0 = img + iy * pitch + ix;
+    v00 = __ldg(r0);
+    v10 = __ldg(r0 + 1);
+    v01 = __ldg(r0 + pitch);
+    v11 = __ldg(r0 + pitch + 1);
+}
+
 struct StreamSmem {
     double2* axy;   // (cx + cos*k, cy + sin*k)   [span] indexed k - kA: one 16-byte load per column
     double2* svc;   // (sin*k, cos*k)                                     and per row
@@ -543,6 +568,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
     const float* __restrict__ img =
         od.gauss + (long long)kp.image * p.gauss_img_stride(kp.octave) + (long long)lvl * od.level_stride;
     const int w = od.w, h = od.h, pitch = od.pitch;
+    // this image's level stack as one texture (level lvl from row tex_row0), if the host made one
+    const cudaTextureObject_t tex = a.gauss_tex ? a.gauss_tex[kp.image * kMaxOctaves + kp.octave] : 0;
+    const int tex_row0 = lvl * (int)(od.level_stride / pitch);   // level_stride = pitch * (rows per level)
     const int tid = threadIdx.x;
     const int span = kB - kA + 1;
     if (span > a.max_span) {   // host sized the tables from the largest sigma; never clip silently
@@ -672,7 +700,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                     const int nsb = ns;
 #endif
                     for (int idx = tid; idx < nsb; idx += kP1Ilp * kDescThreads) {
-                        int off[kP1Ilp], slot[kP1Ilp];
+                        int ixs[kP1Ilp], iys[kP1Ilp], slot[kP1Ilp];
                         float fx[kP1Ilp], fy[kP1Ilp];
                         bool ok[kP1Ilp];
 #pragma unroll
@@ -698,17 +726,19 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                             const int ix = floor_nonneg(px, flx), iy = floor_nonneg(py, fly);
                             fx[j] = (float)D_SUB(px, flx);
                             fy[j] = (float)D_SUB(py, fly);
-                            off[j] = iy * pitch + ix;
+                            ixs[j] = ix;
+                            iys[j] = iy;
                             slot[j] = (vv & (kSRing - 1)) * ring_pitch + cc;
                         }
                         float v00[kP1Ilp], v10[kP1Ilp], v01[kP1Ilp], v11[kP1Ilp];
+                        if (tex) {   // uniform: the loads of all kP1Ilp samples issue back to back
 #pragma unroll
-                        for (int j = 0; j < kP1Ilp; ++j) {
-                            const float* r0 = img + off[j];
-                            v00[j] = __ldg(r0);
-                            v10[j] = __ldg(r0 + 1);
-                            v01[j] = __ldg(r0 + pitch);
-                            v11[j] = __ldg(r0 + pitch + 1);
+                            for (int j = 0; j < kP1Ilp; ++j)
+                                gather2x2_tex(tex, tex_row0, ixs[j], iys[j], v00[j], v10[j], v01[j], v11[j]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < kP1Ilp; ++j)
+                                gather2x2_ldg(img, pitch, ixs[j], iys[j], v00[j], v10[j], v01[j], v11[j]);
                         }
 #pragma unroll
                         for (int j = 0; j < kP1Ilp; ++j) {
@@ -719,7 +749,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                     }
                 } else
                 for (int idx = tid; idx < ns; idx += 2 * kDescThreads) {
-                    int off[2], slot[2];
+                    int ixs[2], iys[2], slot[2];
                     float fx[2], fy[2];
                     bool inb[2];
 #pragma unroll
@@ -737,17 +767,20 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                         const int iy = min(max((int)floor(py), 0), h - 2);
                         fx[j] = (float)D_SUB(px, (double)ix);
                         fy[j] = (float)D_SUB(py, (double)iy);
-                        off[j] = iy * pitch + ix;
+                        ixs[j] = ix;
+                        iys[j] = iy;
                         slot[j] = (vv & (kSRing - 1)) * ring_pitch + cc;
                     }
                     float v00[2], v10[2], v01[2], v11[2];
+                    if (tex) {
 #pragma unroll
-                    for (int j = 0; j < 2; ++j) {
-                        const float* r0 = img + off[j];
-                        v00[j] = __ldg(r0);
-                        v10[j] = __ldg(r0 + 1);
-                        v01[j] = __ldg(r0 + pitch);
-                        v11[j] = __ldg(r0 + pitch + 1);
+                        for (int j = 0; j < 2; ++j)
+                            gather2x2_tex(tex, tex_row0, ixs[j], iys[j], v00[j], v10[j], v01[j], v11[j]);
+                    } else
+                    {
+#pragma unroll
+                        for (int j = 0; j < 2; ++j)
+                            gather2x2_ldg(img, pitch, ixs[j], iys[j], v00[j], v10[j], v01[j], v11[j]);
                     }
 #pragma unroll
                     for (int j = 0; j < 2; ++j) {
