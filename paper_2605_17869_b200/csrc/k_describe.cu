@@ -511,6 +511,7 @@ struct StreamSmem {
     float* raw;     // [n_dsp][128]
     int* cellmin;   // [2][32]: per pass (double-buffered), per cell: lower bound on the lowest-bit
                     // exponent of the cell's leaves (biased: lowest bit >= 2^(e - 127 - 23))
+    const uint32_t* atan_tab;   // atanf's 5-row reduction table (40 words)
     int* misc;      // [2][16]: kmin, kmax, start of cell c = -1..3 (misc[2 + c + 1]);
                     // double-buffered per scale
 };
@@ -870,7 +871,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 const float du = F_MUL(0.5f, F_SUB(right, left));
                 const float dv = F_MUL(0.5f, F_SUB(down, up));
                 const float mag = F_SQRT(F_ADD(F_MUL(du, du), F_MUL(dv, dv)));
-                float theta = dsift_atan2f_mask(dv, du, am);
+                float theta = dsift_atan2f_mask(dv, du, am, S.atan_tab);
                 theta = (theta < 0.0f) ? F_ADD(theta, (float)kTwoPi) : theta;
                 nan_seen |= isnan(theta);   // reference: negative bin -> std::out_of_range (reported after the loop)
                 theta = isnan(theta) ? 0.0f : theta;
@@ -982,6 +983,8 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     __shared__ int misc[32];
     __shared__ int cellmin[64];
     __shared__ ScaleSetup sscale[kMaxDsp];
+    __shared__ __align__(16) uint32_t atan_tab[40];
+    if (threadIdx.x < 40) atan_tab[threadIdx.x] = DS_ATAN_ROW_D[threadIdx.x];
     const int SP = a.max_span;
     const int RP = ring_pitch_for(SP);
     StreamSmem S;
@@ -994,6 +997,7 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
     S.ring = reinterpret_cast<float*>(pbuf);
     S.cellmin = cellmin;
     S.misc = misc;
+    S.atan_tab = atan_tab;
     stream_misc_init(misc);
     if (threadIdx.x < 64) cellmin[threadIdx.x] = 1 << 20;
     __syncthreads();

@@ -45,6 +45,12 @@ __device__ __forceinline__ int nearest_level(const PyramidDesc& p, double sigma_
 __global__ void __launch_bounds__(kOriWarps * 32)
 orient_kernel(const __grid_constant__ OrientArgs a) {
     extern __shared__ __align__(16) unsigned char sm_raw[];
+    // atanf's 5-row reduction table in shared memory: the per-pixel row lookup
+    // sits on the atan2f dependency chain (an LDS instead of a read-only-cache load)
+    __shared__ __align__(16) uint32_t atan_tab[40];
+    if (threadIdx.x < 40) atan_tab[threadIdx.x] = DS_ATAN_ROW_D[threadIdx.x];
+    __syncthreads();
+#endif
     const int bins = a.bins;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // per-warp: union{ acc[bins][32] doubles (certified pass) | node[bins][depth]
@@ -125,7 +131,8 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 const float gy = F_SUB(__ldg(r0 + od.pitch + x), __ldg(r0 - od.pitch + x));
                 const float mag = F_SQRT(F_ADD(F_MUL(gx, gx), F_MUL(gy, gy)));
                 const unsigned am = __activemask();   // the lanes of both votes below
-                float theta = dsift_atan2f_mask(gy, gx, am);
+#if DSIFT_ORI_ATAN_SMEM
+                float theta = dsift_atan2f_mask(gy, gx, am, atan_tab);
                 theta = (theta < 0.0f) ? F_ADD(theta, (float)kTwoPi) : theta;
                 nan_seen |= isnan(theta);   // the reference's int(NaN) bin is out of range -> it throws
                 theta = isnan(theta) ? 0.0f : theta;
