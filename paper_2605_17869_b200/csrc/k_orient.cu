@@ -50,7 +50,6 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
     __shared__ __align__(16) uint32_t atan_tab[40];
     if (threadIdx.x < 40) atan_tab[threadIdx.x] = DS_ATAN_ROW_D[threadIdx.x];
     __syncthreads();
-#endif
     const int bins = a.bins;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // per-warp: union{ acc[bins][32] doubles (certified pass) | node[bins][depth]
@@ -131,7 +130,6 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
                 const float gy = F_SUB(__ldg(r0 + od.pitch + x), __ldg(r0 - od.pitch + x));
                 const float mag = F_SQRT(F_ADD(F_MUL(gx, gx), F_MUL(gy, gy)));
                 const unsigned am = __activemask();   // the lanes of both votes below
-#if DSIFT_ORI_ATAN_SMEM
                 float theta = dsift_atan2f_mask(gy, gx, am, atan_tab);
                 theta = (theta < 0.0f) ? F_ADD(theta, (float)kTwoPi) : theta;
                 nan_seen |= isnan(theta);   // the reference's int(NaN) bin is out of range -> it throws
