@@ -251,6 +251,10 @@ int dsift_set_profiling(dsift_ctx* ctx, int on);
 /* DSIFT_OPT_CAPACITY_SCALE: scale of the automatic work-list capacities in
  * 1/1000 (default 1000; an overflow multiplies it by 4 and replays). */
 #define DSIFT_OPT_CAPACITY_SCALE 2
+/* DSIFT_OPT_TEXTURE_GATHERS: 1 (default) reads the descriptor's bilinear
+ * footprints with texture gathers, 0 with plain loads (the path used when a
+ * level stack exceeds the texture limits); identical results either way. */
+#define DSIFT_OPT_TEXTURE_GATHERS 3
 int dsift_set_option(dsift_ctx* ctx, int key, int64_t value);
 /* Statistics of the last synced result: DSIFT_STAT_EXACT_FALLBACKS = number
  * of keypoints whose descriptor the fast path could not certify. */

@@ -473,6 +473,11 @@ class Extractor:
         """Scale of the automatic work-list capacities in 1/1000 (DSIFT_OPT_CAPACITY_SCALE)."""
         _check(self.lib, self.lib.dsift_set_option(self.ctx, 2, int(permille)))
 
+    def set_texture_gathers(self, on: bool = True) -> None:
+        """Descriptor bilinear footprints by texture gathers (default) or plain
+        loads (DSIFT_OPT_TEXTURE_GATHERS); the results are identical."""
+        _check(self.lib, self.lib.dsift_set_option(self.ctx, 3, int(on)))
+
     def replays(self) -> int:
         """Times the last result was replayed after an automatic capacity overflow."""
         return int(self.lib.dsift_stat(self.ctx, 2))

@@ -264,6 +264,7 @@ struct dsift_ctx {
     std::vector<long long> gauss_tex_key;
     DevBuf gauss_tex_dev;
     bool gauss_tex_ok = false;
+    bool tex_gathers = true;   // DSIFT_OPT_TEXTURE_GATHERS
 };
 
 namespace dsift {
@@ -640,6 +641,7 @@ static int describe_axis(const dsift_config& cf, const std::vector<double>& dsp,
 // Returns nullptr (the kernel then gathers with plain loads) when a level
 // stack exceeds the device's pitched-texture limits.
 static const unsigned long long* ensure_gauss_textures(dsift_ctx* c) {
+    if (!c->tex_gathers) return nullptr;
     const PyramidDesc& d = c->pyr;
     std::vector<long long> key{(long long)(uintptr_t)c->pyramid.as<void>(), d.batch, d.n_oct, d.s};
     for (int o = 0; o < d.n_oct; ++o) {
@@ -682,7 +684,13 @@ static const unsigned long long* ensure_gauss_textures(dsift_ctx* c) {
             td.readMode = cudaReadModeElementType;
             td.normalizedCoords = 0;
             cudaTextureObject_t t = 0;
-            cuda_check(cudaCreateTextureObject(&t, &rd, &td, nullptr), "cudaCreateTextureObject");
+            if (cudaCreateTextureObject(&t, &rd, &td, nullptr) != cudaSuccess || t == 0) {
+                // out of texture resources: the kernels gather with plain loads
+                (void)cudaGetLastError();
+                for (cudaTextureObject_t u : c->gauss_tex) cudaDestroyTextureObject(u);
+                c->gauss_tex.clear();
+                return nullptr;
+            }
             c->gauss_tex.push_back(t);
             h[(size_t)i * kMaxOctaves + o] = (unsigned long long)t;
         }
@@ -2005,6 +2013,9 @@ int dsift_set_option(dsift_ctx* c, int key, int64_t value) {
         } else if (key == DSIFT_OPT_CAPACITY_SCALE) {
             if (value <= 0) invalid("set_option: CAPACITY_SCALE must be > 0 (1/1000 units)");
             c->cap_scale = (double)value / 1000.0;
+        } else if (key == DSIFT_OPT_TEXTURE_GATHERS) {
+            if (value != 0 && value != 1) invalid("set_option: TEXTURE_GATHERS must be 0 or 1");
+            c->tex_gathers = value != 0;
         } else {
             invalid("set_option: unknown key");
         }

@@ -130,3 +130,19 @@ def test_ragged_batch_of_edge_shapes(ref):
         assert res[i].keypoints.tobytes() == want[0]
         assert bits(res[i].descriptors).tobytes() == want[1]
         assert shas[i] == want[2]
+
+
+@pytest.mark.parametrize("size,scale", [((640, 480), 1.0), ((211, 97), 1.0), ((320, 240), 1e-40)])
+def test_texture_and_load_gathers_agree(ref, size, scale):
+    # K5 reads the bilinear footprints with tld4 texture gathers; the plain-load
+    # path (taken when a level stack exceeds the texture limits) must give the
+    # same bytes, and both the reference's
+    w, h = size
+    img = (noise(ref, w, h, 16) * np.float32(scale)).astype(np.float32)
+    want = ref_outcome(ref, img)
+    outs = []
+    for tex in (True, False):
+        with ds.Extractor() as ex:
+            ex.set_texture_gathers(tex)
+            outs.append(gpu_outcome(ex, img))
+    assert outs[0] == outs[1] == want
