@@ -527,7 +527,21 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
         const int yb = ys + 4 * g;
         const bool full = x0 + kSW <= w && ys + kSR <= y_end;   // CTA-uniform: no edge checks
         float2 prev[4];
-        if (MODE == kModeLevel || MODE == kModeDecimate) {
+        if ((MODE == kModeLevel || MODE == kModeDecimate) && full) {
+            // interior step: rows yb .. yb + 3 all exist; one base pointer
+            const float* p0 = src + (long long)(MODE == kModeLevel ? yb : 2 * yb) * sp +
+                              (MODE == kModeLevel ? xv : 2 * xv);
+            const int rstep = MODE == kModeLevel ? sp : 2 * sp;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (MODE == kModeLevel) {
+                    prev[j] = __ldg(reinterpret_cast<const float2*>(p0 + j * rstep));
+                } else {
+                    const float4 q = __ldg(reinterpret_cast<const float4*>(p0 + j * rstep));
+                    prev[j] = make_float2(q.x, q.z);
+                }
+            }
+        } else if (MODE == kModeLevel || MODE == kModeDecimate) {
             const int xa = min(xv, w - 1), xb = min(xv + 1, w - 1);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
