@@ -249,9 +249,19 @@ __device__ __forceinline__ bool b2_vpass(const BlurArgs& a, const float* sm, int
                 if (t >= 0 && t < G::kLen) acc[j] = __fma_rn(a.taps[t], v, acc[j]);
             }
         }
-        if (x < w) {
-            const int yb = y0 + rg * kB2Seg;
-            float* dp = dst + (long long)yb * pitch + x;
+        const int yb = y0 + rg * kB2Seg;
+        float* dp = dst + (long long)yb * pitch + x;
+        if (x < w && yb + kB2Seg <= h) {
+            // every row exists; positive-normal test as one unsigned max
+            unsigned m = 0u;
+#pragma unroll
+            for (int j = 0; j < kB2Seg; ++j) {
+                const float g = (float)acc[j];
+                m = max(m, __float_as_uint(g) - 0x0d800000u);
+                dp[j * pitch] = g;
+            }
+            ok &= m < (0x7f800000u - 0x0d800000u);
+        } else if (x < w) {
 #pragma unroll
             for (int j = 0; j < kB2Seg; ++j) {
                 if (yb + j < h) {
@@ -298,14 +308,26 @@ blur_level2_kernel(const __grid_constant__ BlurArgs a) {
             alu_ok &= (__float_as_int(v) >= 0x0d800000) & (__float_as_int(v) < 0x7f800000);
         }
         __syncthreads();
-        for (int i = threadIdx.x; i < G::kHR * G::kInW; i += kB2Threads) {
-            const int r = i / G::kInW, c = i - r * G::kInW;
-            const int gx = cx0 + c, gy = y0 - R + r;
-            const double* p0 = patch + ((gy >> 1) - ly0) * kPW + ((gx >> 1) - lx0);
-            const double* p1 = p0 + ((gy & 1) ? kPW : 0);
-            const int dx = gx & 1;
-            const double s4 = ((p0[0] + p0[dx]) + p1[0]) + p1[dx];
-            sm2[r * G::kInPitch + c] = (float)(0.25 * s4);
+        // one thread per patch cell (a, b / c, d): the 2x2 block of samples
+        // gx = 2X + {0, 1}, gy = 2Y + {0, 1} it defines, each
+        // ((p0[0] + p0[dx]) + p1[0]) + p1[dx] with the reference's operands
+        // (a + b is shared by the two odd-x samples).  cx0 is even, so block
+        // column X covers staged columns 2X, 2X + 1; block row Y covers
+        // staged rows r0 + 2Y, + 1 with r0 = 0 or -1 (y0 - R odd).
+        static_assert((G::kInW & 1) == 0 && (G::kInPitch & 1) == 0, "float2 block rows");
+        constexpr int kBX = G::kInW / 2;
+        const int r0 = 2 * ly0 - (y0 - R);
+        const int nby = (G::kHR - r0 + 1) >> 1;
+        for (int i = threadIdx.x; i < nby * kBX; i += kB2Threads) {
+            const int by = i / kBX, bx = i - by * kBX;
+            const double* p = patch + by * kPW + bx;
+            const double pa = p[0], pb = p[1], pc = p[kPW], pd = p[kPW + 1];
+            const double a2 = pa + pa, ab = pa + pb;
+            const int r = r0 + 2 * by;
+            float2* o = reinterpret_cast<float2*>(sm2 + r * G::kInPitch + 2 * bx);
+            if (r >= 0) o[0] = make_float2((float)(0.25 * ((a2 + pa) + pa)), (float)(0.25 * ((ab + pa) + pb)));
+            if (r + 1 < G::kHR)
+                o[G::kInPitch / 2] = make_float2((float)(0.25 * ((a2 + pc) + pc)), (float)(0.25 * ((ab + pc) + pd)));
         }
     } else {   // gather with reflect-101 (scalespace.cpp:41-48) through the mode's input
                // mapping: level / raw pixel, 2x upsample (:113-131), decimation (:133-142)
@@ -609,10 +631,11 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
             float* gp = dog ? dog + (long long)yb * pitch + xv : nullptr;
             float* sd = (MODE == kModeDecimate) ? seed + (long long)yb * pitch + xv : nullptr;
             if (full) {
+                unsigned um = 0u;   // positive-normal test of the 8 outputs as one unsigned max
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
                     const float2 gv = make_float2((float)acc[2 * j], (float)acc[2 * j + 1]);
-                    out_ok &= alu_widenable(gv.x) & alu_widenable(gv.y);
+                    um = max(um, max(__float_as_uint(gv.x) - 0x0d800000u, __float_as_uint(gv.y) - 0x0d800000u));
                     *reinterpret_cast<float2*>(dp + j * pitch) = gv;
                     if (MODE == kModeLevel || MODE == kModeDecimate) {
                         // DoG[i-1] = G[i] - G[i-1] (scalespace.cpp:209); DECIMATE also
@@ -621,6 +644,7 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
                         if (gp) *reinterpret_cast<float2*>(gp + j * pitch) = make_float2(gv.x - prev[j].x, gv.y - prev[j].y);
                     }
                 }
+                out_ok &= um < (0x7f800000u - 0x0d800000u);
             } else {
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
