@@ -18,6 +18,34 @@ constexpr int kMaxDsp = 16;         // dsp_scales entries
 constexpr int kMaxOriBins = 64;     // orientation_bins supported on device
 constexpr double kTwoPi = 6.283185307179586476925286766559;  // orient.cpp:37
 
+// Test-only bounds checks (the DSIFT_BOUNDS_CHECK build, tests/native/
+// libdsift_bounds.so; the product build compiles them away).  DSIFT_BOUND(c,
+// site) counts a failed index condition in this translation unit's device
+// counter and records the first failing site id; the host reads the counters
+// through dsift_test_bounds_<unit>() (DSIFT_BOUNDS_UNIT).  The stand-in for
+// compute-sanitizer memcheck, which the GPU pool refuses to run.
+#ifdef DSIFT_BOUNDS_CHECK
+#define DSIFT_BOUNDS_UNIT(unit)                                                           \
+    static __device__ unsigned long long g_bounds[2];                                    \
+    extern "C" int dsift_test_bounds_##unit(unsigned long long* out, int reset) {          \
+        if (cudaMemcpyFromSymbol(out, g_bounds, sizeof(g_bounds)) != cudaSuccess) return -1; \
+        if (reset) {                                                                      \
+            const unsigned long long z[2] = {0ull, 0ull};                                 \
+            if (cudaMemcpyToSymbol(g_bounds, z, sizeof(z)) != cudaSuccess) return -1;     \
+        }                                                                                 \
+        return 0;                                                                         \
+    }
+#define DSIFT_BOUND(cond, site)                                                           \
+    do {                                                                                  \
+        if (!(cond) && atomicAdd(&g_bounds[0], 1ull) == 0ull) g_bounds[1] = (site);       \
+    } while (0)
+#else
+#define DSIFT_BOUNDS_UNIT(unit)
+#define DSIFT_BOUND(cond, site) \
+    do {                        \
+    } while (0)
+#endif
+
 // Pyramid layout in HBM: for octave o, Gaussian levels are a dense array
 // [batch][s+3][h_o][pitch_o] and DoG levels [batch][s+2][h_o][pitch_o]
 // (pitch_o = w_o rounded up to 32 floats = 128 B so every row starts on a

@@ -30,6 +30,16 @@
 
 namespace dsift {
 
+DSIFT_BOUNDS_UNIT(describe)
+#ifdef DSIFT_BOUNDS_CHECK
+// the counters' own check: one deliberately failing condition (site 999)
+__global__ void bounds_selftest_kernel() { DSIFT_BOUND(threadIdx.x > 0, 999); }
+extern "C" int dsift_test_bounds_selftest(void) {
+    bounds_selftest_kernel<<<1, 1>>>();
+    return cudaDeviceSynchronize() == cudaSuccess ? 0 : -1;
+}
+#endif
+
 constexpr int kDescThreads = 128;
 // per-bin tree depth: DescArgs::tree_depth (13 for the defaults, at most 24: leaves < 2^24)
 constexpr int kRing = 32;
@@ -583,6 +593,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
     // ---- per-axis tables (describe.cpp:48-52, 72-73, 84-99 per-axis factors)
     for (int i = tid; i < span; i += kDescThreads) {
         const int k = kA + i;
+        DSIFT_BOUND(i < a.max_span, 508);
         const double q = D_DIV((double)k, bw);
         const double bn = D_ADD(q, (double)(kDescCells / 2 - 0.5));
         const int c = (int)floor(bn);
@@ -732,6 +743,13 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                             slot[j] = (vv & (kSRing - 1)) * ring_pitch + cc;
                         }
                         float v00[kP1Ilp], v10[kP1Ilp], v01[kP1Ilp], v11[kP1Ilp];
+#ifdef DSIFT_BOUNDS_CHECK
+#pragma unroll
+                        for (int j = 0; j < kP1Ilp; ++j) {   // no clamp on this path: the corner bound must hold
+                            DSIFT_BOUND(ixs[j] >= 0 && ixs[j] <= w - 2 && iys[j] >= 0 && iys[j] <= h - 2, 501);
+                            DSIFT_BOUND(!ok[j] || (slot[j] >= 0 && slot[j] < kSRing * ring_pitch), 502);
+                        }
+#endif
                         if (tex) {   // uniform: the loads of all kP1Ilp samples issue back to back
 #pragma unroll
                             for (int j = 0; j < kP1Ilp; ++j)
@@ -788,6 +806,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                         const float top = F_ADD(v00[j], F_MUL(fx[j], F_SUB(v10[j], v00[j])));
                         const float bot = F_ADD(v01[j], F_MUL(fx[j], F_SUB(v11[j], v01[j])));
                         const float sv = F_ADD(top, F_MUL(fy[j], F_SUB(bot, top)));
+                        DSIFT_BOUND(idx + j * kDescThreads >= ns || (slot[j] >= 0 && slot[j] < kSRing * ring_pitch), 503);
                         if (idx + j * kDescThreads < ns) S.ring[slot[j]] = inb[j] ? sv : kUndef;
                     }
                 }
@@ -807,6 +826,7 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                     const int cell = (Rc - pRa) * 5 + (Cc + 1);
                     const int e = ((1 - dr) * 2 + (1 - dc)) * 8 + bori;
                     const int l0 = cell * pP;
+                    DSIFT_BOUND(cell >= 0 && cell < 25 && l0 + pP <= kDescThreads, 507);
                     // lanes in a rotated (per-orientation) fixed order: the 8
                     // orientations of one cell hit 8 different bank pairs
                     int qq = bori < pP ? bori : bori - pP;   // bori % pP (bori < 8 <= 2 * pP)
@@ -859,6 +879,9 @@ __device__ __forceinline__ bool raw_descriptor_stream(const DescArgs& a, const S
                 cc -= wrapc * ncs;
                 rr += wrapc;
                 const int col = u - ub;
+                DSIFT_BOUND(col >= 1 && col + 1 < ring_pitch && col + 1 < sw, 504);
+                DSIFT_BOUND(u - kA >= 0 && u - kA < span && v - kA >= 0 && v - kA < span, 505);
+                DSIFT_BOUND(v - 1 >= have_hi - (kSRing - 1) && v + 1 <= have_hi, 506);   // rows resident in the ring
                 const float* mid = S.ring + (v & (kSRing - 1)) * ring_pitch + col;
                 const float left = mid[-1], right = mid[1];
                 const float up = S.ring[((v - 1) & (kSRing - 1)) * ring_pitch + col];

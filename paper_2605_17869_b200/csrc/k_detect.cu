@@ -19,6 +19,8 @@
 
 namespace dsift {
 
+DSIFT_BOUNDS_UNIT(detect)
+
 constexpr int kDetTile = 32;
 constexpr int kDetThreads = 256;
 constexpr int kDetHalo = kDetTile + 2;
@@ -162,6 +164,7 @@ detect_count_kernel(const __grid_constant__ DetectArgs a) {
     float cc[4], cl[4], cr[4];        // level i: centre, left, right of rows 4g..4g+3
     auto load_level = [&](int l, float (&mx)[6], float (&mn)[6], bool keep_centre) {
         const float* base = lv_s + (l * kDetHalo + 4 * g) * kDetPitch + lx;
+        DSIFT_BOUND(l < nlev && 4 * g + 6 <= kDetHalo && lx + 3 <= kDetPitch, 201);
 #pragma unroll
         for (int r = 0; r < 6; ++r) {
             const float a0 = base[r * kDetPitch], a1 = base[r * kDetPitch + 1], a2 = base[r * kDetPitch + 2];

@@ -23,6 +23,8 @@
 
 namespace dsift {
 
+DSIFT_BOUNDS_UNIT(orient)
+
 constexpr int kOriWarps = 4;
 constexpr int kOriPerWarp = 4;
 constexpr int kOriTile = kOriWarps * kOriPerWarp;
@@ -125,6 +127,8 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
             if (q < npx) {
                 const int qy = (int)(((float)q + 0.5f) * inv_nx);
                 const int x = xa + (q - qy * nx), y = ya + qy;
+                DSIFT_BOUND(x >= 1 && x <= od.w - 2 && y >= 1 && y <= od.h - 2, 301);
+                DSIFT_BOUND(!sep || (x - xa < nx && y - ya < ny && nx <= kOriAxis && ny <= kOriAxis), 302);
                 const float* r0 = img + (long long)y * od.pitch;
                 const float gx = F_SUB(__ldg(r0 + x + 1), __ldg(r0 + x - 1));
                 const float gy = F_SUB(__ldg(r0 + od.pitch + x), __ldg(r0 - od.pitch + x));
@@ -164,6 +168,7 @@ orient_kernel(const __grid_constant__ OrientArgs a) {
             float val;
             pixel(base + lane, bin, val);
             if (bin >= 0) {
+                DSIFT_BOUND(bin < bins, 303);
                 double* slot = acc + bin * 32 + lane;
                 *slot = *slot + (double)val;
                 if (val > 0.0f) {

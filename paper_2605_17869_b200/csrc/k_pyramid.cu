@@ -35,6 +35,8 @@
 
 namespace dsift {
 
+DSIFT_BOUNDS_UNIT(pyramid)
+
 constexpr int kTileW = 64;
 constexpr int kTileH = 64;
 constexpr int kBlurThreads = 256;
@@ -480,6 +482,7 @@ __device__ __forceinline__ void s3_hpass(const BlurArgs& a, const float* stg, do
     }
     int k = k0 + r;
     if (k >= G::kRS) k -= G::kRS;
+    DSIFT_BOUND(k >= 0 && k < G::kRS && 8 * seg + 8 <= G::kTP && r * G::kInW + 8 * seg + 4 * G::kNV <= kSR * G::kInW, 101);
     double2* o0 = reinterpret_cast<double2*>(ring + k * G::kTP + 8 * seg);
 #pragma unroll
     for (int j = 0; j < 8; j += 2)   // the float tmp of scalespace.cpp:86, kept as FP64
@@ -611,6 +614,7 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
 #pragma unroll
             for (int e0 = 0; e0 < kWinV; e0 += 4) {
                 const double* cb = (kv + e0 < G::kRS) ? colp + e0 * G::kTP : colp + (e0 - G::kRS) * G::kTP;
+                DSIFT_BOUND(((kv + e0 < G::kRS) ? kv + e0 : kv + e0 - G::kRS) + 3 < G::kRS && 2 * cp + 2 <= G::kTP, 102);
 #pragma unroll
                 for (int i = 0; i < 4; ++i) {
                     const int e = e0 + i;
@@ -630,6 +634,7 @@ __device__ __forceinline__ void blur_strip_body(const BlurArgs& a, int seg_h, fl
             float* dp = dst + (long long)yb * pitch + xv;
             float* gp = dog ? dog + (long long)yb * pitch + xv : nullptr;
             float* sd = (MODE == kModeDecimate) ? seed + (long long)yb * pitch + xv : nullptr;
+            DSIFT_BOUND(!full || (yb + 3 < y_end && xv + 1 < w), 103);
             if (full) {
                 unsigned um = 0u;   // positive-normal test of the 8 outputs as one unsigned max
 #pragma unroll

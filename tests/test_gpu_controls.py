@@ -8,6 +8,7 @@ race- and error-free.
   then exit 3, and exit 0 with the hook built in but not enabled.
 * compute-sanitizer memcheck / racecheck / synccheck over a small batch that
   runs every extraction kernel (tests/native/sanitize_run.py)."""
+import json
 import os
 import shutil
 import subprocess
@@ -17,6 +18,8 @@ import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 NONDET = os.path.join(ROOT, "tests", "native", "libdsift_nondet.so")
+BOUNDS = os.path.join(ROOT, "tests", "native", "libdsift_bounds.so")
+PRODUCT = os.path.join(ROOT, "paper_2605_17869_b200", "libdsift.so")
 SANITIZER = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
 
 pytestmark = pytest.mark.gpu
@@ -70,3 +73,29 @@ def test_gather_to_rank0_nccl_device_buffers():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
     assert "nccl gather ok" in r.stdout
+
+
+def _bounds_run(lib):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tests", "native", "bounds_run.py"), lib], cwd=ROOT,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout[-2000:], r.stderr[-4000:])
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def test_bounds_build_clean():
+    # the stand-in for compute-sanitizer memcheck (refused by this GPU pool): a
+    # build of the same sources with device-side index checks (DSIFT_BOUND in
+    # K1, K2, K4 and K5: ring / slot / table / staged-tile indices, the
+    # unclamped interior sample footprints, full-tile stores) runs cases that
+    # reach every indexed path; no condition may fail, and the digests must be
+    # the product library's
+    if not os.path.exists(BOUNDS):
+        pytest.fail("tests/native/libdsift_bounds.so missing (run __graft_entry__.build())")
+    chk = _bounds_run(BOUNDS)
+    assert chk["selftest"] == [1, 999]   # a failing condition is counted (and then reset)
+    assert set(chk["bounds"]) == {"pyramid", "detect", "orient", "describe"}, chk["bounds"]
+    for unit, (count, site) in chk["bounds"].items():
+        assert count == 0, f"{unit}: {count} failed index conditions, first at site {site}"
+    prod = _bounds_run(PRODUCT)
+    assert prod["bounds"] == {}
+    assert chk["digests"] == prod["digests"]
