@@ -1036,8 +1036,11 @@ describe_stream_kernel(const __grid_constant__ DescArgs a) {
         __syncthreads();                   // everyone is done with the previous s_k
         if (tid == 0) s_k = atomicAdd(a.ticket, 1u);
         __syncthreads();
-        const long long k = (long long)s_k;
-        if (k >= n) break;
+        if ((long long)s_k >= n) break;
+        // claimed in reverse canonical order: octaves and intervals descending,
+        // so the last claims are the cheapest keypoints (small sigma) and the
+        // CTAs finish together (longest-first, approximately)
+        const long long k = n - 1 - (long long)s_k;
         const DevKeypoint kp = a.kps[k];
         const double2 cs = a.trig[k];
         if (tid < a.n_dsp) sscale[tid] = make_scale_setup(a.pyr, kp, a.dsp[tid]);
