@@ -184,3 +184,27 @@ def test_concurrent_drop_in_calls_from_host_threads(port):
     with ThreadPoolExecutor(max_workers=6) as pool:
         got = list(pool.map(one, range(len(imgs))))
     assert got == want
+
+
+def test_c5_sweep_sample_matches_committed_record():
+    # the committed 10,000-image C5 record of the final round-2 kernels
+    # (profiles/r02/c5_record_final.txt.gz, verify --sweep 10000 --record): a
+    # 64-image sample spread over all ten sizes, extracted now in batches of 5,
+    # must reproduce its digests (a later kernel change that alters any output
+    # bit at any C5 size fails here)
+    import gzip
+    from paper_2605_17869_b200 import verify
+    rec = {}
+    with gzip.open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles", "r02",
+                                "c5_record_final.txt.gz"), "rt") as f:
+        for line in f:
+            i, _, d = line.split()
+            rec[int(i)] = d
+    assert len(rec) == 10000
+    sizes = verify.c5_sweep_sizes(10000)
+    sample = set()
+    for size in sorted(set(sizes)):   # the first 6-7 images of every size
+        sample |= set([i for i, s in enumerate(sizes) if s == size][:7])
+    sample = set(sorted(sample)[:64])
+    got = verify.sweep_digests(10000, 5, skip=set(range(10000)) - sample)
+    assert {i: got[i] for i in sample} == {i: rec[i] for i in sample}
